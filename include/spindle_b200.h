@@ -1,0 +1,197 @@
+/*
+ * spindle_b200 -- C-ABI of the B200-native partitioned-program evaluator.
+ *
+ * This is the drop-in boundary below the reference's `spmd_interpret`
+ * (/root/reference/pkg/src/spindle/spmd_interp.py:157-197).  The reference's
+ * per-op numpy kernels (`_eval_op`, interp.py:35-75) and numpy collective
+ * emulation (`_run_collective`, spmd_interp.py:74-123) are replaced by the
+ * launchers behind `spx_plan_*`; the host mirror of the reference interface
+ * (paper_2401_11202_b200/evaluator.py) compiles a localized module + its
+ * ShardingSpec into a plan of the records declared here and drives it.
+ *
+ * Conventions
+ *   - every function returns 0 on success, a negative code on failure; the
+ *     message is available from spx_last_error() (thread-local);
+ *   - pointers are plain device addresses (uint64_t), sizes are in ELEMENTS
+ *     of 4 bytes unless a name says _bytes.  No torch types cross the ABI;
+ *   - "virtual devices": one process may host V mesh devices on one GPU; their
+ *     buffers live at   base + d * dev_stride   (bytes) for d in [0, V), so
+ *     every record below applies to all V devices in ONE launch.
+ *
+ * Reference interfaces replaced (file:line in /root/reference/pkg/src/spindle):
+ *   SPX_K_EW       interp.py:39-52,58-67  constant/add/mul/neg/exp/transpose/
+ *                                         broadcast/reshape/tag (fused chains)
+ *   SPX_K_REDUCE   interp.py:53-55        reduce sum|max over any dims
+ *   SPX_K_GEMM     interp.py:43-44        matmul (rank-2), operand transposes
+ *                                         folded (interp.py:51-52)
+ *   SPX_K_GATHER   spmd_interp.py:76-91,105-122  all_slice / all_gather /
+ *                                         all_to_all data movement
+ *   SPX_K_CREDUCE  spmd_interp.py:66-71,92-104   all_reduce / reduce_scatter
+ *                                         (left fold in group order)
+ *   SPX_K_NCCL     same collectives across processes (one GPU per mesh device)
+ */
+#ifndef SPINDLE_B200_H
+#define SPINDLE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPX_MAX_RANK 6
+#define SPX_MAX_IN 8
+#define SPX_MAX_OUT 4
+#define SPX_MAX_PROG 28
+
+/* ---- elementwise expression programs (bytecode) ------------------------ */
+enum spx_opcode {
+  SPX_OP_MOV = 0,   /* t = a                  */
+  SPX_OP_ADD = 1,   /* t = a + b   (IEEE fp32, round-to-nearest, no FMA) */
+  SPX_OP_MUL = 2,   /* t = a * b               */
+  SPX_OP_NEG = 3,   /* t = -a                  */
+  SPX_OP_EXP = 4,   /* t = exp(a)              */
+  SPX_OP_MAX = 5,   /* t = maximum(a, b)  (NaN-propagating, like np.maximum) */
+  SPX_OP_IMM = 6,   /* t = imm[i]              */
+  SPX_OP_ADDI = 7,  /* t = a + imm[i]  (constant operand on the right)  */
+  SPX_OP_MULI = 8,  /* t = a * imm[i]          */
+  SPX_OP_IADD = 9,  /* t = imm[i] + a  (constant operand on the left)   */
+  SPX_OP_IMUL = 10  /* t = imm[i] * a          */
+};
+
+/* operand encoding: 0..SPX_MAX_IN-1 = input view j; 32+i = result of insn i */
+#define SPX_REG_T 32
+
+typedef struct {
+  int32_t op, a, b, pad; /* b also indexes imm[] for *I / IMM forms */
+} spx_insn;
+
+typedef struct {
+  int64_t off;                    /* element offset from the device base      */
+  int64_t stride[SPX_MAX_RANK];   /* element strides per output dim (0 = bcast) */
+} spx_view;
+
+typedef struct {
+  uint64_t base;                  /* device 0 arena base address              */
+  int64_t dev_stride;             /* bytes between virtual devices            */
+  int32_t ndev, rank, n_in, n_out, n_prog, vec;  /* vec: 1 = float4 fast path */
+  int64_t dims[SPX_MAX_RANK];     /* logical output shape (row-major)         */
+  int64_t numel;
+  spx_view in[SPX_MAX_IN];
+  int64_t out_off[SPX_MAX_OUT];   /* outputs are contiguous row-major          */
+  int32_t out_reg[SPX_MAX_OUT];   /* which register each output stores         */
+  spx_insn prog[SPX_MAX_PROG];
+  float imm[SPX_MAX_PROG];
+} spx_ew_params;
+
+/* ---- reductions ---------------------------------------------------------- */
+typedef struct {
+  spx_ew_params x;                /* the reduced operand as an expression over
+                                     the INPUT shape (out_reg[0] = value)      */
+  int32_t monoid;                 /* 0 sum, 1 max                              */
+  int32_t n_kept, n_red, pad;
+  int64_t kept_dims[SPX_MAX_RANK], kept_stride[SPX_MAX_RANK]; /* in input index space */
+  int64_t red_dims[SPX_MAX_RANK], red_stride[SPX_MAX_RANK];
+  int64_t n_out, n_red_elems;
+  int64_t out_off;                /* contiguous output                         */
+  int64_t scratch_off;            /* arena scratch for partials (elements)     */
+} spx_reduce_params;
+
+/* ---- matmul -------------------------------------------------------------- */
+typedef struct {
+  uint64_t base;
+  int64_t dev_stride;             /* bytes */
+  int32_t ndev, M, N, K;
+  int64_t a_off, b_off, c_off;    /* elements from device base */
+  int64_t lda, ldb, ldc;          /* row pitch (elements) of the STORED arrays */
+  int32_t a_mn_major;             /* 0: A stored [M][K]; 1: A stored [K][M]    */
+  int32_t b_k_major;              /* 0: B stored [K][N]; 1: B stored [N][K]    */
+  int32_t path;                   /* 0 auto, 1 tcgen05 3xTF32, 2 SIMT fp32     */
+  int32_t pad;
+} spx_gemm_params;
+
+/* ---- collectives over co-located virtual devices ------------------------- */
+/* gather-style (all_slice, all_gather, all_to_all, relayouts):
+ *   out[d][l] = src[table[d * n_combo + combo(l)]] [ base_off[d] + sum_k (l_k % ext_k) * sstride_k ]
+ * where combo(l) = sum_k (l_k / ext_k) * cmul_k.  Tables are device arrays. */
+typedef struct {
+  int32_t ndev, rank, n_combo, pad;
+  int64_t dims[SPX_MAX_RANK];     /* output local shape */
+  int64_t ext[SPX_MAX_RANK];      /* chunk extent per dim (== dims if not split) */
+  int64_t cmul[SPX_MAX_RANK];
+  int64_t sstride[SPX_MAX_RANK];  /* source element strides */
+  int64_t numel;
+  uint64_t src_table;             /* const float** [ndev * n_combo]           */
+  uint64_t base_off;              /* const int64_t* [ndev] (elements)          */
+  uint64_t dst;                   /* float** [ndev]                            */
+} spx_gather_params;
+
+/* reduce-style (all_reduce, reduce_scatter):
+ *   out[d][l] = fold_{j < n_members} src[members[d * n_members + j]] [ base_off[d] + sum_k l_k * sstride_k ] */
+typedef struct {
+  int32_t ndev, rank, n_members, monoid;
+  int64_t dims[SPX_MAX_RANK];
+  int64_t sstride[SPX_MAX_RANK];
+  int64_t numel;
+  uint64_t src;                   /* const float** [ndev] (device input base)  */
+  uint64_t members;               /* const int32_t* [ndev * n_members]          */
+  uint64_t base_off;              /* const int64_t* [ndev]                      */
+  uint64_t dst;                   /* float** [ndev]                             */
+} spx_creduce_params;
+
+/* ---- NCCL collective across processes (one mesh device per GPU) --------- */
+enum spx_nccl_kind { SPX_NCCL_ALLREDUCE = 0, SPX_NCCL_ALLGATHER = 1,
+                     SPX_NCCL_REDUCESCATTER = 2, SPX_NCCL_ALLTOALL = 3 };
+typedef struct {
+  int32_t kind, comm, monoid, pad; /* comm: index returned by spx_comm_init   */
+  uint64_t send, recv;             /* device addresses                          */
+  int64_t count;                   /* elements: per-rank send count (AG/A2A chunk), recv count (RS), total (AR) */
+} spx_nccl_params;
+
+/* ---- plan records --------------------------------------------------------- */
+enum spx_kind { SPX_K_EW = 1, SPX_K_REDUCE = 2, SPX_K_GEMM = 3, SPX_K_GATHER = 4,
+                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6 };
+
+/* library / device */
+const char* spx_last_error(void);
+int spx_version(void);
+int spx_params_size(int kind);                     /* ABI check: sizeof(record params) */
+int spx_device_init(int ordinal);                  /* select + check sm_100 */
+int spx_malloc(uint64_t bytes, uint64_t* out_ptr);  /* arena (cudaMalloc) */
+int spx_free(uint64_t ptr);
+int spx_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream);
+int spx_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, uint64_t stream);
+int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream);
+int spx_stream_create(uint64_t* out_stream);
+int spx_stream_sync(uint64_t stream);
+int spx_stream_destroy(uint64_t stream);
+
+/* NCCL (dlopen'd; the same libnccl torch uses) */
+int spx_nccl_get_unique_id(uint8_t out_id[128]);
+int spx_comm_init(const uint8_t id[128], int nranks, int rank, int* out_comm);
+int spx_comm_destroy(int comm);
+
+/* plans: a sequence of records [kind, param struct] executed in order on a stream */
+int spx_plan_create(uint64_t* out_plan);
+int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t params_bytes);
+int spx_plan_finalize(uint64_t plan);              /* builds TMA descriptors etc. */
+int spx_plan_run(uint64_t plan, uint64_t stream);  /* eager launch of every record */
+int spx_plan_capture(uint64_t plan, uint64_t stream);  /* record into a CUDA graph */
+int spx_plan_replay(uint64_t plan, uint64_t stream);   /* launch the captured graph */
+int spx_plan_launch_count(uint64_t plan);          /* kernel launches per run */
+int spx_plan_destroy(uint64_t plan);
+int spx_plan_record_info(uint64_t plan, int index, int* kind, int* path);
+
+/* timing helpers (CUDA events on the given stream) */
+int spx_event_create(uint64_t* out_event);
+int spx_event_record(uint64_t event, uint64_t stream);
+int spx_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms);
+int spx_event_destroy(uint64_t event);
+
+/* per-record timing of one eager run (ms per record, length = record count) */
+int spx_plan_profile(uint64_t plan, uint64_t stream, float* out_ms, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

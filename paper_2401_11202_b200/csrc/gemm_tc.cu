@@ -1,0 +1,368 @@
+// tcgen05 / TMEM / TMA GEMM for the reference's fp32 `matmul`
+// (interp.py:43-44: numpy `@` on float32 arrays -> sgemm).
+//
+// fp32 parity (<= 1e-5 max-normalised error, SPMD spec SPEC.md:92) on tensor
+// cores uses the 3xTF32 split: x = hi + lo with hi = x truncated to the tf32
+// grid (exact) and lo = x - hi (exact in fp32), and
+//     A.B ~= hi(A).hi(B) + hi(A).lo(B) + lo(A).hi(B)
+// accumulated in fp32 in TMEM; the dropped lo.lo term is ~2^-22 relative.
+//
+// Structure (one 128 x BN output tile per CTA, 1 CTA per SM):
+//   warp 0      TMA producer: A and B k-slabs (32 fp32 = one 128B swizzle row)
+//               into a STAGES-deep ring; transposed operands are loaded as
+//               MN-major tiles, so `transpose` feeding a matmul never
+//               materialises (interp.py:51-52 folded into the descriptor)
+//   warps 2..5  split: hi in place, lo into a twin buffer (same swizzled
+//               layout -- the split is elementwise), fence.proxy.async, arrive
+//   warp 1      MMA issuer (one thread): 4 k-steps x 3 terms of
+//               tcgen05.mma.cta_group::1.kind::tf32 M=128 N=BN K=8 into TMEM,
+//               tcgen05.commit frees the smem stage
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
+// The batch dimension of the TMA tensor maps walks co-located mesh devices.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdlib>
+#include <cstring>
+#include "common.cuh"
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
+constexpr int STAGES = 3;
+constexpr int NTHREADS = 192;
+
+SPX_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SPX_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+SPX_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+SPX_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: a protocol bug traps (error surfaces to the host) instead of
+// hanging the GPU.
+SPX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  long long t0 = 0;
+  for (int it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it == 64) t0 = clock64();
+    if (it > 64 && (it & 1023) == 0 && clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+
+SPX_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, 128B swizzle (layout type 2), sm_100 version 1.
+SPX_DEV uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+SPX_DEV void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+SPX_DEV void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+struct TcArgs {
+  int M, N, K, a_mn_major, b_k_major;
+  uint64_t c_base;     // device 0 address of C
+  int64_t dev_stride;  // bytes
+  int64_t ldc;
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
+};
+
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+               const __grid_constant__ TcArgs args) {
+  using S = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* split = full + STAGES;
+  uint64_t* empty = split + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, dev = blockIdx.z;
+  const int nk = (args.K + BK - 1) / BK;
+
+  auto a_hi = [&](int s) { return smem + s * S::STAGE; };
+  auto a_lo = [&](int s) { return smem + s * S::STAGE + S::A_BYTES; };
+  auto b_hi = [&](int s) { return smem + s * S::STAGE + 2 * S::A_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * S::STAGE + 2 * S::A_BYTES + S::B_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_d = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(S::A_BYTES + S::B_BYTES);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t round = kb / STAGES;
+        mbar_wait(&empty[s], (round & 1) ^ 1);
+        mbar_expect_tx(&full[s], bytes);
+        const int k0 = kb * BK;
+        if (args.a_mn_major) {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_3d(a_hi(s) + c * 4096, &tma_a, &full[s], m0 + 32 * c, k0, dev);
+        } else {
+          tma_load_3d(a_hi(s), &tma_a, &full[s], k0, m0, dev);
+        }
+        if (args.b_k_major) {
+          tma_load_3d(b_hi(s), &tma_b, &full[s], k0, n0, dev);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tma_load_3d(b_hi(s) + c * 4096, &tma_b, &full[s], n0 + 32 * c, k0, dev);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)args.a_mn_major << 15) |
+                             ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);
+      // K-major: LBO unused (16B), SBO = 8 rows x 128B; k-step of 8 fp32 = +32B.
+      // MN-major: LBO = 32-element MN chunk stride (32 rows x 128B), SBO = 8 k-rows x 128B; k-step = +1024B.
+      const uint32_t a_lbo = args.a_mn_major ? 4096u : 16u, a_step = args.a_mn_major ? 1024u : 32u;
+      const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t round = kb / STAGES;
+        mbar_wait(&split[s], round & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ahi = smem_u32(a_hi(s)), alo = smem_u32(a_lo(s));
+        const uint32_t bhi = smem_u32(b_hi(s)), blo = smem_u32(b_lo(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t dah = smem_desc(ahi + kk * a_step, a_lbo, 1024);
+          const uint64_t dal = smem_desc(alo + kk * a_step, a_lbo, 1024);
+          const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, 1024);
+          const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, 1024);
+          const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
+          mma_tf32(tmem_d, dal, dbh, idesc, first);   // small terms first
+          mma_tf32(tmem_d, dah, dbl, idesc, 1u);
+          mma_tf32(tmem_d, dah, dbh, idesc, 1u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(accum);
+    }
+  } else {
+    // ---------------- split (hi/lo) ----------------
+    const int t = threadIdx.x - 64;  // 0..127
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t round = kb / STAGES;
+      mbar_wait(&full[s], round & 1);
+      float4* ah = reinterpret_cast<float4*>(a_hi(s));
+      float4* al = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll 4
+      for (int i = t; i < S::A_BYTES / 16; i += 128) {
+        float4 x = ah[i], h;
+        h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+        h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+        h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+        h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+        ah[i] = h;
+        al[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+      float4* bh = reinterpret_cast<float4*>(b_hi(s));
+      float4* bl = reinterpret_cast<float4*>(b_lo(s));
+#pragma unroll 4
+      for (int i = t; i < S::B_BYTES / 16; i += 128) {
+        float4 x = bh[i], h;
+        h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+        h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+        h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+        h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+        bh[i] = h;
+        bl[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&split[s]);
+    }
+    // ---------------- epilogue ----------------
+    mbar_wait(accum, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int row = m0 + q * 32 + lane;
+    float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
+                  (int64_t)row * args.ldc;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+            "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+            "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < args.M) {
+        const int col0 = n0 + c * 32;
+        if (col0 + 32 <= args.N && (args.ldc & 3) == 0) {
+          float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < args.N) crow[col0 + j] = __uint_as_float(v[j]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D fp32 map {inner, outer, device}; box {32, box_outer, 1}; 128B swizzle.
+int make_map(CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer, uint64_t ndev, uint64_t row_bytes,
+             uint64_t dev_bytes, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return spx_set_error("cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {inner, outer, ndev};
+  cuuint64_t strides[2] = {row_bytes, dev_bytes ? dev_bytes : row_bytes * outer};
+  cuuint32_t box[3] = {32, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, reinterpret_cast<void*>(addr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return spx_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+}  // namespace
+
+struct SpxGemmTC {
+  CUtensorMap ma, mb;
+  TcArgs args;
+  int bn;
+  dim3 grid;
+  spx_gemm_params p;
+};
+
+bool spx_gemm_tc_supported(const spx_gemm_params& p) {
+  // TMA: 16B-aligned base and row pitch; tile sizes make tiny shapes a waste.
+  const uint64_t da = p.base + (uint64_t)(p.a_off * 4), db = p.base + (uint64_t)(p.b_off * 4);
+  if ((da & 15) || (db & 15) || (p.lda & 3) || (p.ldb & 3) || (p.dev_stride & 15)) return false;
+  if (p.M < 64 || p.N < 32 || p.K < 32) return false;
+  return true;
+}
+
+int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
+  SpxGemmTC* g = new SpxGemmTC();
+  g->p = p;
+  g->bn = 128;
+  const uint64_t a = p.base + (uint64_t)(p.a_off * 4), b = p.base + (uint64_t)(p.b_off * 4);
+  int rc;
+  if (p.a_mn_major) rc = make_map(&g->ma, a, p.M, p.K, p.ndev, p.lda * 4, p.dev_stride, 32);
+  else rc = make_map(&g->ma, a, p.K, p.M, p.ndev, p.lda * 4, p.dev_stride, BM);
+  if (rc) { delete g; return rc; }
+  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, g->bn);
+  else rc = make_map(&g->mb, b, p.N, p.K, p.ndev, p.ldb * 4, p.dev_stride, 32);
+  if (rc) { delete g; return rc; }
+  g->args.M = p.M; g->args.N = p.N; g->args.K = p.K;
+  g->args.a_mn_major = p.a_mn_major; g->args.b_k_major = p.b_k_major;
+  g->args.c_base = p.base + (uint64_t)(p.c_off * 4);
+  g->args.dev_stride = p.dev_stride;
+  g->args.ldc = p.ldc;
+  g->grid = dim3((p.N + g->bn - 1) / g->bn, (p.M + BM - 1) / BM, p.ndev);
+  *out = g;
+  return 0;
+}
+
+int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
+  {
+    static bool attr = false;
+    if (!attr) { SPX_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL)); attr = true; }
+    gemm_tc_kernel<128><<<g->grid, NTHREADS, Smem<128>::TOTAL, s>>>(g->ma, g->mb, g->args);
+  }
+  SPX_CHECK_LAUNCH();
+  if (nlaunch) ++*nlaunch;
+  return 0;
+}
+
+void spx_gemm_tc_free(SpxGemmTC* g) { delete g; }

@@ -1,0 +1,379 @@
+// Host runtime of the C-ABI (include/spindle_b200.h): device/arena/stream
+// management, plan records -> kernel launches, CUDA-graph capture of a whole
+// partitioned step, NCCL (dlopen'd, the same libnccl torch loads) for
+// collectives that cross processes.
+#include <dlfcn.h>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "common.cuh"
+
+static thread_local char g_err[1024] = "";
+
+int spx_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return -1;
+}
+
+static int g_num_sms = 148;
+int spx_num_sms() { return g_num_sms; }
+
+// ---------------------------------------------------------------------------
+// NCCL via dlopen (no link-time dependency; reuse the process's libnccl)
+// ---------------------------------------------------------------------------
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+typedef int (*fn_get_uid)(nccl_uid_t*);
+typedef int (*fn_init_rank)(nccl_comm_t*, int, nccl_uid_t, int);
+typedef int (*fn_destroy)(nccl_comm_t);
+typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_allgather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_reducescatter)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_sendrecv)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_group)(void);
+typedef const char* (*fn_errstr)(int);
+typedef int (*fn_count)(nccl_comm_t, int*);
+
+static struct {
+  void* h = nullptr;
+  fn_get_uid get_uid;
+  fn_init_rank init_rank;
+  fn_destroy destroy;
+  fn_allreduce allreduce;
+  fn_allgather allgather;
+  fn_reducescatter reducescatter;
+  fn_sendrecv send, recv;
+  fn_group gstart, gend;
+  fn_errstr errstr;
+  fn_count count;
+} N;
+static std::vector<nccl_comm_t> g_comms;
+
+static int nccl_load() {
+  if (N.h) return 0;
+  const char* env = getenv("SPX_NCCL_LIB");
+  const char* cands[] = {env, "libnccl.so.2", "libnccl.so"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    N.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (N.h) break;
+  }
+  if (!N.h) return spx_set_error("cannot dlopen libnccl (set SPX_NCCL_LIB)");
+#define LOADSYM(field, name)                                            \
+  N.field = reinterpret_cast<decltype(N.field)>(dlsym(N.h, name));      \
+  if (!N.field) return spx_set_error("libnccl lacks %s", name);
+  LOADSYM(get_uid, "ncclGetUniqueId");
+  LOADSYM(init_rank, "ncclCommInitRank");
+  LOADSYM(destroy, "ncclCommDestroy");
+  LOADSYM(allreduce, "ncclAllReduce");
+  LOADSYM(allgather, "ncclAllGather");
+  LOADSYM(reducescatter, "ncclReduceScatter");
+  LOADSYM(send, "ncclSend");
+  LOADSYM(recv, "ncclRecv");
+  LOADSYM(gstart, "ncclGroupStart");
+  LOADSYM(gend, "ncclGroupEnd");
+  LOADSYM(errstr, "ncclGetErrorString");
+  LOADSYM(count, "ncclCommCount");
+#undef LOADSYM
+  return 0;
+}
+
+#define SPX_NCCL(call)                                                              \
+  do {                                                                              \
+    int _r = (call);                                                                \
+    if (_r != 0) return spx_set_error("%s: nccl error %d (%s)", #call, _r, N.errstr(_r)); \
+  } while (0)
+
+static const int NCCL_FLOAT = 7, NCCL_SUM = 0, NCCL_MAX = 2;
+
+static int run_nccl(const spx_nccl_params& p, cudaStream_t s) {
+  if (p.comm < 0 || p.comm >= (int)g_comms.size() || !g_comms[p.comm]) return spx_set_error("bad comm %d", p.comm);
+  nccl_comm_t c = g_comms[p.comm];
+  const int op = p.monoid == 0 ? NCCL_SUM : NCCL_MAX;
+  const void* sb = reinterpret_cast<const void*>(p.send);
+  void* rb = reinterpret_cast<void*>(p.recv);
+  switch (p.kind) {
+    case SPX_NCCL_ALLREDUCE: SPX_NCCL(N.allreduce(sb, rb, (size_t)p.count, NCCL_FLOAT, op, c, s)); break;
+    case SPX_NCCL_ALLGATHER: SPX_NCCL(N.allgather(sb, rb, (size_t)p.count, NCCL_FLOAT, c, s)); break;
+    case SPX_NCCL_REDUCESCATTER: SPX_NCCL(N.reducescatter(sb, rb, (size_t)p.count, NCCL_FLOAT, op, c, s)); break;
+    case SPX_NCCL_ALLTOALL: {
+      int n = 0;
+      SPX_NCCL(N.count(c, &n));
+      SPX_NCCL(N.gstart());
+      for (int r = 0; r < n; ++r) {
+        SPX_NCCL(N.send(static_cast<const float*>(sb) + (size_t)r * p.count, (size_t)p.count, NCCL_FLOAT, r, c, s));
+        SPX_NCCL(N.recv(static_cast<float*>(rb) + (size_t)r * p.count, (size_t)p.count, NCCL_FLOAT, r, c, s));
+      }
+      SPX_NCCL(N.gend());
+      break;
+    }
+    default: return spx_set_error("bad nccl kind %d", p.kind);
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+struct Record {
+  int kind;
+  int path;  // GEMM: 1 tcgen05, 2 simt
+  std::vector<uint8_t> params;
+  SpxGemmTC* tc = nullptr;
+};
+
+struct Plan {
+  std::vector<Record> recs;
+  bool finalized = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+};
+
+static int run_record(Record& r, cudaStream_t s, int* nl) {
+  switch (r.kind) {
+    case SPX_K_EW: return spx_launch_ew(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
+    case SPX_K_REDUCE: return spx_launch_reduce(*reinterpret_cast<const spx_reduce_params*>(r.params.data()), s, nl);
+    case SPX_K_GATHER: return spx_launch_gather(*reinterpret_cast<const spx_gather_params*>(r.params.data()), s, nl);
+    case SPX_K_CREDUCE: return spx_launch_creduce(*reinterpret_cast<const spx_creduce_params*>(r.params.data()), s, nl);
+    case SPX_K_GEMM:
+      if (r.path == 1) return spx_gemm_tc_launch(r.tc, s, nl);
+      return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
+    case SPX_K_NCCL: return run_nccl(*reinterpret_cast<const spx_nccl_params*>(r.params.data()), s);
+  }
+  return spx_set_error("unknown record kind %d", r.kind);
+}
+
+static size_t params_size(int kind) {
+  switch (kind) {
+    case SPX_K_EW: return sizeof(spx_ew_params);
+    case SPX_K_REDUCE: return sizeof(spx_reduce_params);
+    case SPX_K_GEMM: return sizeof(spx_gemm_params);
+    case SPX_K_GATHER: return sizeof(spx_gather_params);
+    case SPX_K_CREDUCE: return sizeof(spx_creduce_params);
+    case SPX_K_NCCL: return sizeof(spx_nccl_params);
+  }
+  return 0;
+}
+
+extern "C" {
+
+const char* spx_last_error(void) { return g_err; }
+int spx_version(void) { return 1; }
+
+int spx_params_size(int kind) { return (int)params_size(kind); }
+
+int spx_device_init(int ordinal) {
+  SPX_CUDA(cudaSetDevice(ordinal));
+  cudaDeviceProp prop;
+  SPX_CUDA(cudaGetDeviceProperties(&prop, ordinal));
+  if (prop.major != 10) return spx_set_error("device %d is sm_%d%d; spindle_b200 needs sm_100 (B200)", ordinal, prop.major, prop.minor);
+  g_num_sms = prop.multiProcessorCount;
+  SPX_CUDA(cudaFree(0));
+  return 0;
+}
+
+int spx_malloc(uint64_t bytes, uint64_t* out) {
+  void* p = nullptr;
+  SPX_CUDA(cudaMalloc(&p, bytes ? bytes : 256));
+  *out = reinterpret_cast<uint64_t>(p);
+  return 0;
+}
+int spx_free(uint64_t ptr) {
+  SPX_CUDA(cudaFree(reinterpret_cast<void*>(ptr)));
+  return 0;
+}
+int spx_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream) {
+  SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice,
+                           reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+int spx_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, uint64_t stream) {
+  SPX_CUDA(cudaMemcpyAsync(dst, reinterpret_cast<const void*>(src), bytes, cudaMemcpyDeviceToHost,
+                           reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream) {
+  SPX_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(dst), value, bytes, reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+int spx_stream_create(uint64_t* out) {
+  cudaStream_t s;
+  SPX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = reinterpret_cast<uint64_t>(s);
+  return 0;
+}
+int spx_stream_sync(uint64_t stream) {
+  SPX_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+int spx_stream_destroy(uint64_t stream) {
+  SPX_CUDA(cudaStreamDestroy(reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int spx_nccl_get_unique_id(uint8_t out_id[128]) {
+  if (nccl_load()) return -1;
+  nccl_uid_t id;
+  SPX_NCCL(N.get_uid(&id));
+  memcpy(out_id, id.internal, 128);
+  return 0;
+}
+int spx_comm_init(const uint8_t id[128], int nranks, int rank, int* out_comm) {
+  if (nccl_load()) return -1;
+  nccl_uid_t uid;
+  memcpy(uid.internal, id, 128);
+  nccl_comm_t c = nullptr;
+  SPX_NCCL(N.init_rank(&c, nranks, uid, rank));
+  g_comms.push_back(c);
+  *out_comm = (int)g_comms.size() - 1;
+  return 0;
+}
+int spx_comm_destroy(int comm) {
+  if (comm < 0 || comm >= (int)g_comms.size() || !g_comms[comm]) return 0;
+  SPX_NCCL(N.destroy(g_comms[comm]));
+  g_comms[comm] = nullptr;
+  return 0;
+}
+
+int spx_plan_create(uint64_t* out) {
+  *out = reinterpret_cast<uint64_t>(new Plan());
+  return 0;
+}
+
+int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (P->finalized) return spx_set_error("plan already finalized");
+  const size_t want = params_size(kind);
+  if (!want) return spx_set_error("unknown record kind %d", kind);
+  if (bytes != want) return spx_set_error("record kind %d: %llu bytes, ABI says %zu", kind, (unsigned long long)bytes, want);
+  Record r;
+  r.kind = kind;
+  r.path = 0;
+  r.params.assign(static_cast<const uint8_t*>(params), static_cast<const uint8_t*>(params) + bytes);
+  if (kind == SPX_K_GEMM) {
+    const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
+    const bool tc_ok = spx_gemm_tc_supported(g);
+    if (g.path == 1 && !tc_ok) return spx_set_error("gemm %dx%dx%d: tcgen05 path requested but operands unsupported", g.M, g.N, g.K);
+    r.path = (g.path == 2 || (g.path == 0 && !tc_ok)) ? 2 : 1;
+  }
+  P->recs.push_back(std::move(r));
+  return 0;
+}
+
+int spx_plan_finalize(uint64_t plan) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  for (auto& r : P->recs) {
+    if (r.kind == SPX_K_GEMM && r.path == 1 && !r.tc) {
+      if (spx_gemm_tc_prepare(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), &r.tc)) return -1;
+    }
+  }
+  P->finalized = true;
+  return 0;
+}
+
+int spx_plan_run(uint64_t plan, uint64_t stream) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (!P->finalized && spx_plan_finalize(plan)) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int nl = 0;
+  for (auto& r : P->recs)
+    if (run_record(r, s, &nl)) return -1;
+  P->launches = nl;
+  return 0;
+}
+
+int spx_plan_capture(uint64_t plan, uint64_t stream) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (!P->finalized && spx_plan_finalize(plan)) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (P->exec) { cudaGraphExecDestroy(P->exec); P->exec = nullptr; }
+  if (P->graph) { cudaGraphDestroy(P->graph); P->graph = nullptr; }
+  SPX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int nl = 0;
+  for (auto& r : P->recs) {
+    if (run_record(r, s, &nl)) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      return -1;
+    }
+  }
+  SPX_CUDA(cudaStreamEndCapture(s, &P->graph));
+  SPX_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
+  P->launches = nl;
+  return 0;
+}
+
+int spx_plan_replay(uint64_t plan, uint64_t stream) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (!P->exec) return spx_set_error("plan has no captured graph");
+  SPX_CUDA(cudaGraphLaunch(P->exec, reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int spx_plan_launch_count(uint64_t plan) { return reinterpret_cast<Plan*>(plan)->launches; }
+
+int spx_plan_record_info(uint64_t plan, int index, int* kind, int* path) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (index < 0 || index >= (int)P->recs.size()) return spx_set_error("record index out of range");
+  *kind = P->recs[index].kind;
+  *path = P->recs[index].path;
+  return 0;
+}
+
+int spx_plan_destroy(uint64_t plan) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (P->exec) cudaGraphExecDestroy(P->exec);
+  if (P->graph) cudaGraphDestroy(P->graph);
+  for (auto& r : P->recs)
+    if (r.tc) spx_gemm_tc_free(r.tc);
+  delete P;
+  return 0;
+}
+
+int spx_event_create(uint64_t* out) {
+  cudaEvent_t e;
+  SPX_CUDA(cudaEventCreate(&e));
+  *out = reinterpret_cast<uint64_t>(e);
+  return 0;
+}
+int spx_event_record(uint64_t ev, uint64_t stream) {
+  SPX_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+int spx_event_elapsed_ms(uint64_t a, uint64_t b, float* out) {
+  SPX_CUDA(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(b)));
+  SPX_CUDA(cudaEventElapsedTime(out, reinterpret_cast<cudaEvent_t>(a), reinterpret_cast<cudaEvent_t>(b)));
+  return 0;
+}
+int spx_event_destroy(uint64_t ev) {
+  SPX_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev)));
+  return 0;
+}
+
+int spx_plan_profile(uint64_t plan, uint64_t stream, float* out_ms, int n) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (!P->finalized && spx_plan_finalize(plan)) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nr = (int)P->recs.size();
+  std::vector<cudaEvent_t> ev(nr + 1);
+  for (auto& e : ev) SPX_CUDA(cudaEventCreate(&e));
+  SPX_CUDA(cudaEventRecord(ev[0], s));
+  int nl = 0;
+  for (int i = 0; i < nr; ++i) {
+    if (run_record(P->recs[i], s, &nl)) return -1;
+    SPX_CUDA(cudaEventRecord(ev[i + 1], s));
+  }
+  SPX_CUDA(cudaEventSynchronize(ev[nr]));
+  for (int i = 0; i < nr && i < n; ++i) SPX_CUDA(cudaEventElapsedTime(&out_ms[i], ev[i], ev[i + 1]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,434 @@
+"""Executable: arena layout + native plan for one compiled localized function.
+
+Two hosting modes for the mesh devices of a localized module:
+
+  "local"  every mesh device lives on this process's GPU (virtual devices at
+           a fixed arena stride); collectives are in-GPU group kernels --
+           this is the drop-in `spmd_interpret` mode and what the parity tests
+           exercise on a single B200;
+  "nccl"   one process per GPU and mesh device (torchrun); collectives are
+           NCCL calls on per-group communicators, with in-GPU relayouts where
+           the chunk order of a layout differs from the communicator order.
+
+Layout of one device slice of the arena: [args | liveness-packed
+intermediates and results | reduce scratch], identical on every device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import runtime as R
+from .plan import ALIGN, Compiler, Leaf, Node, Program, _align, _contig, _prod
+
+
+def _collapse(dims, views):
+    """Merge adjacent dims where every view is mergeable (contiguous or both 0)."""
+    dims = list(dims)
+    views = [list(v) for v in views]
+    k = len(dims) - 2
+    while k >= 0:
+        ok = all(v[k] == v[k + 1] * dims[k + 1] for v in views)
+        if ok:
+            dims[k] = dims[k] * dims[k + 1]
+            del dims[k + 1]
+            for v in views:
+                v[k] = v[k + 1]
+                del v[k + 1]
+        k -= 1
+    return dims, views
+
+
+class Executable:
+    DRY_BASE = 1 << 40
+    DRY_TABLES = 1 << 44
+
+    def __init__(self, module, func="main", device: R.Device | None = None, devices=None,
+                 comm_mode="local", comms=None, gemm_path=0, dry=False):
+        """dry=True builds the records against fake addresses without a GPU
+        (used by the CPU tests and the record simulator)."""
+        self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode).compile()
+        self.dry = dry
+        self.device = None if dry else (device or R.Device(0))
+        self.ndev = len(self.comp.devices)
+        self.gemm_path = gemm_path
+        self.comms = comms or {}
+        self._layout()
+        self._alloc()
+        self._tables = []
+        self._records = []
+        self._emit()
+        self._upload_tables()
+        self.plan = None
+        if not dry:
+            self.plan = R.NativePlan(self.device)
+            for kind, params in self._records:
+                self.plan.add(kind, params)
+            self.plan.finalize()
+
+    # ---------------------------------------------------------------- layout
+    def _layout(self):
+        c = self.comp
+        ks = c.kernels
+        n = len(ks)
+        first, last = {}, {}
+        for i, k in enumerate(ks):
+            for b in k.outs:
+                first.setdefault(b, i)
+            for b in k.ins:
+                last[b] = max(last.get(b, -1), i)
+        off = {}
+        top = 0
+        for a in c.arg_bufs:
+            off[a] = top
+            top += _align(c.buffers[a])
+        base = top
+        keep = set(c.result_bufs)
+        free: list[tuple[int, int]] = []   # (offset, size) holes above `base`
+        hi = base
+        order = sorted((first[b], b) for b in first if b not in off)
+        by_start: dict[int, list[str]] = {}
+        for i, b in order:
+            by_start.setdefault(i, []).append(b)
+        by_end: dict[int, list[str]] = {}
+        for b, e in last.items():
+            if b in off and b in c.arg_bufs:
+                continue
+            by_end.setdefault(e, []).append(b)
+
+        def alloc(size):
+            nonlocal hi
+            for j, (o, s) in enumerate(free):
+                if s >= size:
+                    if s == size:
+                        free.pop(j)
+                    else:
+                        free[j] = (o + size, s - size)
+                    return o
+            o = hi
+            hi += size
+            return o
+
+        def release(o, size):
+            free.append((o, size))
+            free.sort()
+            merged = []
+            for fo, fs in free:
+                if merged and merged[-1][0] + merged[-1][1] == fo:
+                    merged[-1] = (merged[-1][0], merged[-1][1] + fs)
+                else:
+                    merged.append((fo, fs))
+            free[:] = merged
+
+        for i in range(n):
+            for b in by_start.get(i, []):
+                off[b] = alloc(_align(c.buffers[b]))
+            for b in by_end.get(i, []):
+                if b in keep or b not in off or b in c.arg_bufs:
+                    continue
+                if first.get(b, -1) > i:
+                    continue
+                release(off[b], _align(c.buffers[b]))
+            for b in ks[i].outs:          # written but never read and not returned
+                if b not in last and b not in keep:
+                    release(off[b], _align(c.buffers[b]))
+        scratch = 0
+        for k in ks:
+            if k.kind == "reduce":
+                n_out = _prod(d for j, d in enumerate(k.data["in_dims"]) if j not in k.data["red"])
+                scratch = max(scratch, 20480 + 2 * n_out)
+        self.scratch_off = hi
+        hi += _align(scratch)
+        # zero page: source for all_gather chunks no device owns (a layout that
+        # repeats an axis, e.g. [["M", "M"]], leaves zero-filled chunks exactly
+        # like the reference's np.zeros buffer, spmd_interp.py:86)
+        zero = 0
+        for k in ks:
+            if k.kind == "coll" and k.data["kind"] == "all_gather":
+                zero = max(zero, _prod(k.data["in_dims"]))
+        self.zero_off = hi
+        self.zero_elems = _align(zero) if zero else 0
+        hi += self.zero_elems
+        self.off = off
+        self.slice_elems = _align(hi, 1 << 18)           # 1 MiB granularity per device
+        self.peak_bytes = hi * 4
+
+    def _alloc(self):
+        self.dev_stride = self.slice_elems * 4
+        self.base = self.DRY_BASE if self.dry else self.device.malloc(self.dev_stride * self.ndev)
+        if self.zero_elems and not self.dry:
+            self.device.memset(self.base + self.zero_off * 4, self.zero_elems * 4, 0)
+
+    def addr(self, p: int, buf: str, extra: int = 0) -> int:
+        return self.base + p * self.dev_stride + (self.off[buf] + extra) * 4
+
+    # ---------------------------------------------------------------- tables
+    def _table(self, arr: np.ndarray) -> int:
+        """Queue a device table; returns a placeholder index resolved at upload."""
+        self._tables.append(np.ascontiguousarray(arr))
+        return len(self._tables) - 1
+
+    def _upload_tables(self):
+        sizes = [_align(t.nbytes, 16) for t in self._tables]
+        total = max(16, sum(sizes))
+        self.table_base = self.DRY_TABLES if self.dry else self.device.malloc(total)
+        blob = np.zeros(total, dtype=np.uint8)
+        addrs, o = [], 0
+        for t, s in zip(self._tables, sizes):
+            blob[o:o + t.nbytes] = t.view(np.uint8).reshape(-1)
+            addrs.append(self.table_base + o)
+            o += s
+        self.table_blob = blob
+        if not self.dry:
+            self.device.h2d(self.table_base, blob)
+            self.device.sync()
+        for kind, p in self._records:
+            for fld in ("src_table", "base_off", "dst", "src", "members"):
+                if hasattr(p, fld) and getattr(p, fld) >= (1 << 62):
+                    setattr(p, fld, addrs[getattr(p, fld) - (1 << 62)])
+
+    def _tref(self, arr) -> int:
+        return (1 << 62) + self._table(arr)
+
+    # ------------------------------------------------------------------ emit
+    def _ew_params(self, exprs: dict, dims, outs_keep=None) -> R.EwParams:
+        prog = Program.build(exprs)
+        names = list(exprs)
+        dims = tuple(dims) if dims else (1,)
+        views = [list(l.strides) if len(l.strides) else [1] for l in prog.leaves]
+        views = [v if len(v) == len(dims) else [0] * len(dims) for v in views]
+        cdims, cviews = _collapse(dims, [v for v in views] + [list(_contig(dims))])
+        cviews = cviews[:-1]
+        p = R.EwParams()
+        p.base = self.base
+        p.dev_stride = self.dev_stride
+        p.ndev = self.ndev
+        p.rank = len(cdims)
+        p.n_in = len(prog.leaves)
+        p.numel = _prod(dims)
+        for k, d in enumerate(cdims):
+            p.dims[k] = d
+        vec = 1 if (p.numel % 4 == 0 and cdims[-1] % 4 == 0) else 0
+        for j, (l, v) in enumerate(zip(prog.leaves, cviews)):
+            p.inp[j].off = self.off[l.buf] + l.off
+            for k, s in enumerate(v):
+                p.inp[j].stride[k] = s
+            if v[-1] not in (0, 1):
+                vec = 0
+            if v[-1] == 1 and (p.inp[j].off % 4 or any(s % 4 for s in v[:-1])):
+                vec = 0
+        keep = outs_keep or names
+        p.n_out = len(keep)
+        for o, name in enumerate(keep):
+            p.out_off[o] = self.off[name]
+            p.out_reg[o] = prog.out_regs[names.index(name)]
+        p.n_prog = len(prog.insns)
+        for i, (op, a, b, imm) in enumerate(prog.insns):
+            p.prog[i].op, p.prog[i].a, p.prog[i].b = op, a, b
+            p.imm[i] = imm
+        p.vec = vec
+        return p
+
+    def _emit(self):
+        c = self.comp
+        for k in c.kernels:
+            if k.kind == "ew":
+                self._records.append((R.K_EW, self._ew_params(k.data["exprs"], k.data["dims"],
+                                                              k.data.get("outs_keep"))))
+            elif k.kind == "reduce":
+                self._emit_reduce(k)
+            elif k.kind == "gemm":
+                self._emit_gemm(k)
+            elif k.kind == "coll":
+                if c.comm_mode == "local":
+                    self._emit_coll_local(k)
+                else:
+                    self._emit_coll_nccl(k)
+
+    def _emit_reduce(self, k):
+        in_dims = list(k.data["in_dims"]) or [1]
+        red = sorted(k.data["red"])
+        kept = [d for d in range(len(in_dims)) if d not in red]
+        perm = kept + red
+        root = k.data["root"]
+        prog = Program.build({k.outs[0]: root})
+        p = R.ReduceParams()
+        x = p.x
+        x.base, x.dev_stride, x.ndev = self.base, self.dev_stride, self.ndev
+        x.rank = len(perm)
+        for i, d in enumerate(perm):
+            x.dims[i] = in_dims[d]
+        x.numel = _prod(in_dims)
+        x.n_in = len(prog.leaves)
+        for j, l in enumerate(prog.leaves):
+            x.inp[j].off = self.off[l.buf] + l.off
+            st = list(l.strides) if len(l.strides) == len(in_dims) else [0] * len(in_dims)
+            for i, d in enumerate(perm):
+                x.inp[j].stride[i] = st[d]
+        x.n_out = 1
+        x.out_reg[0] = prog.out_regs[0]
+        x.n_prog = len(prog.insns)
+        for i, (op, a, b, imm) in enumerate(prog.insns):
+            x.prog[i].op, x.prog[i].a, x.prog[i].b = op, a, b
+            x.imm[i] = imm
+        p.monoid = 0 if k.data["monoid"] == "sum" else 1
+        p.n_kept, p.n_red = len(kept), len(red)
+        cst = _contig(in_dims)
+        for i, d in enumerate(kept):
+            p.kept_dims[i] = in_dims[d]
+            p.kept_stride[i] = cst[d]
+        for i, d in enumerate(red):
+            p.red_dims[i] = in_dims[d]
+            p.red_stride[i] = cst[d]
+        p.n_out = _prod(in_dims[d] for d in kept)
+        p.n_red_elems = _prod(in_dims[d] for d in red)
+        p.out_off = self.off[k.outs[0]]
+        p.scratch_off = self.scratch_off
+        self._records.append((R.K_REDUCE, p))
+
+    def _emit_gemm(self, k):
+        d = k.data
+        p = R.GemmParams()
+        p.base, p.dev_stride, p.ndev = self.base, self.dev_stride, self.ndev
+        p.M, p.N, p.K = d["M"], d["N"], d["K"]
+        ab, aoff, lda, at = d["a"]
+        bb, boff, ldb, bt = d["b"]
+        p.a_off = self.off[ab] + aoff
+        p.b_off = self.off[bb] + boff
+        p.c_off = self.off[k.outs[0]]
+        p.lda, p.ldb, p.ldc = lda, ldb, d["N"]
+        p.a_mn_major = 1 if at else 0
+        p.b_k_major = 1 if bt else 0
+        p.path = self.gemm_path
+        self._records.append((R.K_GEMM, p))
+
+    # ---- in-GPU collectives (spmd_interp.py:74-123 as group kernels) ----
+    def _ptrs(self, buf, extra=0):
+        return np.array([self.addr(p, buf, extra) for p in range(self.ndev)], dtype=np.uint64)
+
+    def _emit_coll_local(self, k):
+        c = self.comp
+        d = k.data
+        kind, attrs = d["kind"], d["attrs"]
+        src, out = d["src"], k.outs[0]
+        in_dims, out_dims = list(d["in_dims"]), list(d["out_dims"])
+        S = _contig(in_dims)
+        coords = c.coords
+        devs = c.devices
+        assert devs == list(range(len(coords))), "local mode hosts every mesh device"
+        if kind in ("all_slice", "all_gather", "all_to_all"):
+            g = R.GatherParams()
+            g.ndev = self.ndev
+            g.rank = len(out_dims)
+            g.numel = _prod(out_dims)
+            for j, dd in enumerate(out_dims):
+                g.dims[j] = dd
+                g.sstride[j] = S[j]
+            base = np.zeros(self.ndev, dtype=np.int64)
+            if kind == "all_slice":
+                apd = attrs["axes_per_dim"]
+                for j, dd in enumerate(out_dims):
+                    g.ext[j] = dd
+                g.n_combo = 1
+                table = np.array([self.addr(p, src) for p in range(self.ndev)], dtype=np.uint64)
+                for p in range(self.ndev):
+                    base[p] = sum(c._chunk_index(coords[p], apd[j]) * out_dims[j] * S[j]
+                                  for j in range(len(out_dims)))
+            elif kind == "all_gather":
+                apd = attrs["axes_per_dim"]
+                nper = [out_dims[j] // in_dims[j] for j in range(len(out_dims))]
+                cm = _contig(nper)
+                for j in range(len(out_dims)):
+                    g.ext[j] = in_dims[j]
+                    g.cmul[j] = cm[j]
+                g.n_combo = _prod(nper)
+                axes = [a for axs in apd for a in axs]
+                grp = c._group_of(axes)
+                zero = self.base + self.zero_off * 4
+                table = np.full((self.ndev, g.n_combo), zero, dtype=np.uint64)
+                for p in range(self.ndev):
+                    for m in grp[p]:
+                        combo = sum(c._chunk_index(coords[m], apd[j]) * cm[j] for j in range(len(apd)))
+                        table[p, combo] = self.addr(m, src)
+            else:  # all_to_all
+                gd, sd, axes = attrs["gather_dim"], attrs["slice_dim"], attrs["axes"]
+                n = c._axes_n(axes)
+                for j, dd in enumerate(out_dims):
+                    g.ext[j] = dd
+                g.ext[gd] = in_dims[gd]
+                g.cmul[gd] = 1
+                g.n_combo = n
+                grp = c._group_of(axes)
+                table = np.zeros((self.ndev, n), dtype=np.uint64)
+                for p in range(self.ndev):
+                    for m in grp[p]:
+                        table[p, c._chunk_index(coords[m], axes)] = self.addr(m, src)
+                    base[p] = c._chunk_index(coords[p], axes) * out_dims[sd] * S[sd]
+            g.src_table = self._tref(table.reshape(-1))
+            g.base_off = self._tref(base)
+            g.dst = self._tref(self._ptrs(out))
+            self._records.append((R.K_GATHER, g))
+            return
+        # all_reduce / reduce_scatter: left fold in group order (_combine, :66-71)
+        axes = attrs["axes"]
+        grp = c._group_of(axes)
+        nm = len(grp[0])
+        r = R.CreduceParams()
+        r.ndev, r.rank, r.n_members = self.ndev, len(out_dims), nm
+        r.monoid = 0 if attrs.get("monoid", "sum") == "sum" else 1
+        r.numel = _prod(out_dims)
+        for j, dd in enumerate(out_dims):
+            r.dims[j] = dd
+            r.sstride[j] = S[j]
+        members = np.array([grp[p] for p in range(self.ndev)], dtype=np.int32)
+        base = np.zeros(self.ndev, dtype=np.int64)
+        if kind == "reduce_scatter":
+            apd = attrs["axes_per_dim"]
+            for p in range(self.ndev):
+                base[p] = sum(c._chunk_index(coords[p], apd[j]) * out_dims[j] * S[j]
+                              for j in range(len(out_dims)))
+        r.src = self._tref(self._ptrs(src))
+        r.members = self._tref(members.reshape(-1))
+        r.base_off = self._tref(base)
+        r.dst = self._tref(self._ptrs(out))
+        self._records.append((R.K_CREDUCE, r))
+
+    def _emit_coll_nccl(self, k):
+        raise NotImplementedError("nccl mode collectives: see nccl.py")
+
+    # --------------------------------------------------------------- host I/O
+    def upload_args(self, per_device: list[dict]):
+        """per_device[p][arg] = local numpy array for hosted device p."""
+        for p in range(self.ndev):
+            for a in self.comp.arg_bufs:
+                arr = np.ascontiguousarray(per_device[p][a], dtype=np.float32)
+                self.device.h2d(self.addr(p, a), arr)
+
+    def download_results(self) -> list[list[np.ndarray]]:
+        """[result j][device p] local arrays."""
+        f = self.comp.f
+        out = []
+        for j, b in enumerate(self.comp.result_bufs):
+            dims = tuple(f.result_types[j].dims)
+            per = []
+            for p in range(self.ndev):
+                a = np.empty(dims, dtype=np.float32)
+                self.device.d2h(a, self.addr(p, b))
+                per.append(a)
+            out.append(per)
+        self.device.sync()
+        return out
+
+    def run(self):
+        self.plan.run()
+
+    def records(self):
+        return list(self._records)
+
+    def close(self):
+        if self.dry:
+            return
+        self.plan.destroy()
+        self.device.free(self.base)
+        self.device.free(self.table_base)

@@ -1,0 +1,539 @@
+"""Plan compiler: localized SPMD function + ShardingSpec -> device records.
+
+This is the op-to-kernel lowering below the reference's lockstep loop
+(`spmd_interpret`, /root/reference/pkg/src/spindle/spmd_interp.py:184-191).
+Where the reference evaluates every op with numpy per device
+(`interp._eval_op`, interp.py:35-75) and every collective as a numpy group
+operation (`_run_collective`, spmd_interp.py:74-123), the compiler:
+
+  * turns data-movement-free ops into VIEWS of buffers (transpose, broadcast,
+    reshape of contiguous data, tag, all_slice of broadcast dims) or scalar
+    CONSTANTS (constant and anything derived from it, folded with numpy
+    float32 arithmetic so folding is bit-exact);
+  * fuses chains of elementwise ops (add/mul/neg/exp) into expression
+    programs -- single-use subexpressions are inlined, and producer groups
+    whose consumers all run later are merged into multi-output kernels (the
+    momentum update m' = 0.9 m + g; p' = p - 0.01 m' is ONE kernel);
+  * folds the reduced operand of `reduce` into the reduction kernel;
+  * lowers matmul to the tcgen05 3xTF32 GEMM with operand transposes folded
+    into the TMA/UMMA descriptors (SIMT fallback for tiny/misaligned shapes);
+  * lowers collectives either to in-GPU group kernels over co-located mesh
+    devices (bit-exact left folds in group order) or to NCCL calls when each
+    mesh device is its own process/GPU;
+  * assigns arena offsets by liveness (cf. sim.peak_live_bytes, sim.py:126-150).
+
+Every per-device program is identical (SPMD), so buffers sit at the same
+offset in every device's arena slice and one launch covers all co-located
+devices.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import runtime as R
+from .ir import COLLECTIVE_KINDS, COUNTED_COLLECTIVES, op_flops
+
+ALIGN = 64  # elements (256 B)
+EW_KINDS = ("add", "mul", "neg", "exp")
+
+
+def _prod(xs):
+    n = 1
+    for x in xs:
+        n *= int(x)
+    return n
+
+
+def _contig(dims):
+    st, acc = [], 1
+    for d in reversed(dims):
+        st.append(acc)
+        acc *= int(d)
+    return tuple(reversed(st))
+
+
+def _align(n, a=ALIGN):
+    return (n + a - 1) // a * a
+
+
+# --- value descriptors --------------------------------------------------------
+
+@dataclass(frozen=True)
+class Leaf:
+    buf: str          # buffer name
+    off: int          # element offset within the buffer
+    strides: tuple    # per dim of the consuming shape
+
+
+@dataclass
+class Node:
+    """Expression node: op in EW_KINDS, children are Node | Leaf | np.float32."""
+    op: str
+    kids: list
+    uid: int = 0
+
+
+@dataclass
+class Desc:
+    kind: str                 # "buf" | "view" | "const" | "expr"
+    dims: tuple
+    buf: str | None = None    # buf / view source buffer
+    off: int = 0
+    strides: tuple = ()
+    value: np.float32 | None = None
+    node: Node | Leaf | None = None
+
+
+@dataclass
+class Kernel:
+    kind: str                 # "ew" | "reduce" | "gemm" | "coll"
+    outs: list                # buffer names written
+    ins: set = field(default_factory=set)   # buffer names read
+    data: dict = field(default_factory=dict)
+    op_index: int = -1
+    alive: bool = True
+
+
+class UnsupportedProgram(NotImplementedError):
+    pass
+
+
+class Compiler:
+    """Builds the kernel list and buffer table for one localized function.
+
+    devices: mesh device indices hosted by this process ([all] for the
+    in-GPU mode, [rank] for the one-process-per-GPU NCCL mode).
+    """
+
+    def __init__(self, module, func="main", devices=None, comm_mode="local"):
+        self.module = module
+        self.f = module.func(func)
+        self.mesh = module.mesh
+        n_mesh = self.mesh.device_count if self.mesh is not None else 1
+        self.devices = list(range(n_mesh)) if devices is None else list(devices)
+        self.coords = self.mesh.coords() if self.mesh is not None else [{}]
+        self.comm_mode = comm_mode
+        self.types = {}
+        self.desc: dict[str, Desc] = {}
+        self.buffers: dict[str, int] = {}      # name -> numel
+        self.bufdims: dict[str, tuple] = {}
+        self.kernels: list[Kernel] = []
+        self._uid = 0
+        self._tmp = 0
+        self.arg_bufs = []
+        self.result_bufs = []
+        self.counts = {k: 0 for k in COUNTED_COLLECTIVES}
+        self.flops = 0.0
+        self._matcache = {}
+
+    # ---------------------------------------------------------------- helpers
+    def _new_buf(self, dims, hint="t"):
+        self._tmp += 1
+        name = f"%{hint}#{self._tmp}"
+        self.buffers[name] = max(1, _prod(dims))
+        self.bufdims[name] = tuple(dims)
+        return name
+
+    def _node(self, op, kids):
+        self._uid += 1
+        return Node(op, kids, self._uid)
+
+    def _leaf_of(self, d: Desc):
+        if d.kind == "buf":
+            return Leaf(d.buf, 0, _contig(d.dims))
+        if d.kind == "view":
+            return Leaf(d.buf, d.off, tuple(d.strides))
+        if d.kind == "const":
+            return d.value
+        return d.node
+
+    def _uses(self):
+        uses: dict[str, list] = {}
+        for i, op in enumerate(self.f.ops):
+            for j, o in enumerate(op.operands):
+                uses.setdefault(o, []).append((i, op))
+        for r in self.f.results:
+            uses.setdefault(r, []).append((len(self.f.ops), None))
+        return uses
+
+    # ------------------------------------------------------- materialization
+    def materialize(self, name: str) -> str:
+        """Contiguous buffer holding value `name` (emits a copy/fill if needed)."""
+        d = self.desc[name]
+        if d.kind == "buf":
+            return d.buf
+        if name in self._matcache:
+            return self._matcache[name]
+        out = self._new_buf(d.dims, "m")
+        self._emit_ew({out: self._leaf_of(d)}, d.dims)
+        self._matcache[name] = out
+        return out
+
+    def _emit_ew(self, outputs: dict, dims, op_index=-1):
+        k = Kernel("ew", list(outputs), data={"exprs": dict(outputs), "dims": tuple(dims)},
+                   op_index=op_index)
+        k.ins = self._expr_bufs(list(outputs.values()))
+        self.kernels.append(k)
+        return k
+
+    def _expr_bufs(self, roots):
+        seen, out = set(), set()
+
+        def walk(x):
+            if isinstance(x, Leaf):
+                out.add(x.buf)
+            elif isinstance(x, Node):
+                if x.uid in seen:
+                    return
+                seen.add(x.uid)
+                for c in x.kids:
+                    walk(c)
+        for r in roots:
+            walk(r)
+        return out
+
+    # ------------------------------------------------------------------ main
+    def compile(self):
+        f = self.f
+        for n, t in f.args:
+            if t.elem != "f32":
+                raise UnsupportedProgram(f"arg %{n}: element kind {t.elem} (backend computes f32)")
+            self.types[n] = tuple(t.dims)
+            self.buffers[n] = max(1, _prod(t.dims))
+            self.bufdims[n] = tuple(t.dims)
+            self.desc[n] = Desc("buf", tuple(t.dims), buf=n)
+            self.arg_bufs.append(n)
+        uses = self._uses()
+        for i, op in enumerate(f.ops):
+            for r, t in zip(op.results, op.result_types):
+                if t.elem != "f32":
+                    raise UnsupportedProgram(f"%{r}: element kind {t.elem}")
+                self.types[r] = tuple(t.dims)
+            self._lower(i, op, uses)
+            if op.kind not in COLLECTIVE_KINDS:
+                self.flops += op_flops(op, [self.types[o] for o in op.operands])
+            if op.kind in self.counts:
+                self.counts[op.kind] += 1
+        for r in f.results:
+            self.result_bufs.append(self.materialize(r))
+        self._merge_ew()
+        return self
+
+    def _lower(self, i, op, uses):
+        k = op.kind
+        r = op.results[0] if op.results else None
+        dims = tuple(op.result_types[0].dims) if op.result_types else ()
+        D = self.desc
+        if k == "constant":
+            D[r] = Desc("const", dims, value=np.float32(op.attrs["value"]))
+            return
+        if k == "tag":
+            D[r] = D[op.operands[0]]
+            return
+        if k in EW_KINDS:
+            kids = [self._leaf_of(D[o]) for o in op.operands]
+            if all(isinstance(c, np.float32) for c in kids):          # constant folding
+                with np.errstate(all="ignore"):
+                    if k == "add":
+                        v = np.float32(kids[0] + kids[1])
+                    elif k == "mul":
+                        v = np.float32(kids[0] * kids[1])
+                    elif k == "neg":
+                        v = np.float32(-kids[0])
+                    else:
+                        v = np.float32(np.exp(kids[0]))
+                D[r] = Desc("const", dims, value=v)
+                return
+            node = self._node(k, kids)
+            u = uses.get(r, [])
+            inline = (len(u) == 1 and u[0][1] is not None and
+                      (u[0][1].kind in EW_KINDS or u[0][1].kind == "reduce"))
+            if inline:
+                D[r] = Desc("expr", dims, node=node)
+            else:
+                out = self._new_buf(dims, "v")
+                self._emit_ew({out: node}, dims, op_index=i)
+                D[r] = Desc("buf", dims, buf=out)
+            return
+        if k == "transpose":
+            x = D[op.operands[0]]
+            perm = op.attrs["perm"]
+            if x.kind == "const":
+                D[r] = Desc("const", dims, value=x.value)
+                return
+            src = x if x.kind in ("buf", "view") else self.desc_of_buf(self.materialize(op.operands[0]))
+            st = src.strides if src.kind == "view" else _contig(src.dims)
+            D[r] = Desc("view", dims, buf=src.buf, off=src.off if src.kind == "view" else 0,
+                        strides=tuple(st[p] for p in perm))
+            return
+        if k == "broadcast":
+            x = D[op.operands[0]]
+            if x.kind == "const":
+                D[r] = Desc("const", dims, value=x.value)
+                return
+            if x.kind == "expr":
+                x = self.desc_of_buf(self.materialize(op.operands[0]))
+            st_x = x.strides if x.kind == "view" else _contig(x.dims)
+            st = [0] * len(dims)
+            for j, dd in enumerate(op.attrs["dims"]):
+                st[dd] = st_x[j]
+            D[r] = Desc("view", dims, buf=x.buf, off=x.off if x.kind == "view" else 0, strides=tuple(st))
+            return
+        if k == "reshape":
+            x = D[op.operands[0]]
+            if x.kind == "const":
+                D[r] = Desc("const", dims, value=x.value)
+                return
+            if x.kind == "view" and tuple(x.strides) == _contig(x.dims):
+                D[r] = Desc("view", dims, buf=x.buf, off=x.off, strides=_contig(dims))
+                return
+            b = self.materialize(op.operands[0])
+            D[r] = Desc("view", dims, buf=b, off=0, strides=_contig(dims))
+            return
+        if k == "matmul":
+            self._lower_matmul(i, op, dims)
+            return
+        if k == "reduce":
+            self._lower_reduce(i, op, dims)
+            return
+        if k in COLLECTIVE_KINDS:
+            self._lower_collective(i, op, dims)
+            return
+        raise UnsupportedProgram(f"op {k!r} has no dense semantics; lower and use spmd_interpret")
+
+    def desc_of_buf(self, b):
+        return Desc("buf", self.bufdims[b], buf=b)
+
+    # ----------------------------------------------------------------- matmul
+    def _mm_operand(self, name, dims):
+        d = self.desc[name]
+        if d.kind == "buf":
+            return d.buf, 0, dims[1], False
+        if d.kind == "view":
+            s0, s1 = d.strides
+            if s1 == 1 and s0 >= dims[1]:
+                return d.buf, d.off, s0, False
+            if s0 == 1 and s1 >= dims[0]:
+                return d.buf, d.off, s1, True
+        b = self.materialize(name)
+        return b, 0, dims[1], False
+
+    def _lower_matmul(self, i, op, dims):
+        a_dims = self.types[op.operands[0]]
+        b_dims = self.types[op.operands[1]]
+        ab, aoff, lda, at = self._mm_operand(op.operands[0], a_dims)
+        bb, boff, ldb, bt = self._mm_operand(op.operands[1], b_dims)
+        out = self._new_buf(dims, "mm")
+        M, K = a_dims
+        N = b_dims[1]
+        k = Kernel("gemm", [out], {ab, bb}, op_index=i,
+                   data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt)))
+        self.kernels.append(k)
+        self.desc[op.results[0]] = Desc("buf", dims, buf=out)
+
+    # ----------------------------------------------------------------- reduce
+    def _lower_reduce(self, i, op, dims):
+        x = self.desc[op.operands[0]]
+        in_dims = self.types[op.operands[0]]
+        root = self._leaf_of(x)
+        out = self._new_buf(dims, "red")
+        k = Kernel("reduce", [out], op_index=i,
+                   data=dict(root=root, in_dims=tuple(in_dims), red=list(op.attrs["dims"]),
+                             monoid=op.attrs.get("monoid", "sum")))
+        k.ins = self._expr_bufs([root])
+        self.kernels.append(k)
+        self.desc[op.results[0]] = Desc("buf", dims, buf=out)
+
+    # ------------------------------------------------------------ collectives
+    def _chunk_index(self, coord, axes):
+        idx = 0
+        for ax in axes:
+            idx = idx * self.mesh.size(ax) + coord[ax]
+        return idx
+
+    def _axes_n(self, axes):
+        return _prod(self.mesh.size(a) for a in axes)
+
+    def _groups(self, axes):
+        others = [n for n in self.mesh.names() if n not in axes]
+        out: dict = {}
+        for i, c in enumerate(self.coords):
+            out.setdefault(tuple(c[n] for n in others), []).append(i)
+        return list(out.values())
+
+    def _group_of(self, axes):
+        g = {}
+        for grp in self._groups(axes):
+            for d in grp:
+                g[d] = grp
+        return g
+
+    def _lower_collective(self, i, op, dims):
+        k = op.kind
+        r = op.results[0]
+        src_name = op.operands[0]
+        x = self.desc[src_name]
+        in_dims = tuple(self.types[src_name])
+        if k == "all_slice":
+            apd = op.attrs["axes_per_dim"]
+            if x.kind == "const":
+                self.desc[r] = Desc("const", dims, value=x.value)
+                return
+            sliced = [dd for dd, axes in enumerate(apd) if axes]
+            if x.kind == "view" and all(x.strides[dd] == 0 for dd in sliced):
+                self.desc[r] = Desc("view", dims, buf=x.buf, off=x.off, strides=x.strides)
+                return
+        src = self.materialize(src_name)
+        out = self._new_buf(dims, "c")
+        kern = Kernel("coll", [out], {src}, op_index=i,
+                      data=dict(kind=k, attrs=dict(op.attrs), in_dims=in_dims, out_dims=tuple(dims),
+                                src=src))
+        self.kernels.append(kern)
+        self.desc[r] = Desc("buf", dims, buf=out)
+
+    # ------------------------------------------------------ multi-output merge
+    def _merge_ew(self):
+        """Merge an EW kernel into a later EW kernel that reads one of its outputs
+        when every other reader of the producer's outputs runs after the
+        consumer (so computing the producer late is safe)."""
+        ks = self.kernels
+        readers: dict[str, list[int]] = {}
+        for idx, kk in enumerate(ks):
+            for b in kk.ins:
+                readers.setdefault(b, []).append(idx)
+        result_set = set(self.result_bufs)
+        producer = {}
+        for idx, kk in enumerate(ks):
+            for b in kk.outs:
+                producer[b] = idx
+        for xi, X in enumerate(ks):
+            if X.kind != "ew" or not X.alive:
+                continue
+            changed = True
+            while changed:
+                changed = False
+                for b in sorted(X.ins):
+                    yi = producer.get(b)
+                    if yi is None or yi >= xi:
+                        continue
+                    Y = ks[yi]
+                    if Y.kind != "ew" or not Y.alive or Y.data["dims"] != X.data["dims"]:
+                        continue
+                    ok = True
+                    for ob in Y.outs:
+                        for rd in readers.get(ob, []):
+                            if rd != xi and rd != yi and rd <= xi and ks[rd].alive:
+                                ok = False
+                    if not ok:
+                        continue
+                    # substitute leaves of Y's outputs in X by Y's expression roots
+                    sub = {ob: Y.data["exprs"][ob] for ob in Y.outs}
+                    dims = X.data["dims"]
+                    new_exprs = {}
+                    memo = {}
+                    for ob, e in X.data["exprs"].items():
+                        new_exprs[ob] = _substitute(e, sub, _contig(dims), memo)
+                    merged = dict(sub)
+                    merged.update(new_exprs)
+                    if not _fits(merged):
+                        continue
+                    X.data["exprs"] = merged
+                    X.outs = list(merged)
+                    X.ins = self._expr_bufs(list(merged.values()))
+                    Y.alive = False
+                    for ob in Y.outs:
+                        producer[ob] = xi
+                    for bb in X.ins:
+                        readers.setdefault(bb, []).append(xi)
+                    changed = True
+                    break
+        # drop outputs nobody reads any more (internal registers only)
+        for xi, X in enumerate(ks):
+            if X.kind != "ew" or not X.alive or len(X.outs) == 1:
+                continue
+            keep = [ob for ob in X.outs if ob in result_set or
+                    any(rd != xi and ks[rd].alive for rd in readers.get(ob, []))]
+            if not keep:
+                keep = X.outs[-1:]
+            X.data["outs_keep"] = keep
+        self.kernels = [kk for kk in ks if kk.alive]
+
+
+def _substitute(e, sub, contig, memo):
+    if isinstance(e, Leaf):
+        if e.buf in sub and e.off == 0 and tuple(e.strides) == tuple(contig):
+            return sub[e.buf]
+        return e
+    if isinstance(e, Node):
+        if e.uid in memo:
+            return memo[e.uid]
+        n = Node(e.op, [_substitute(c, sub, contig, memo) for c in e.kids], e.uid)
+        memo[e.uid] = n
+        return n
+    return e
+
+
+def _fits(exprs) -> bool:
+    try:
+        prog = Program.build(exprs)
+    except ValueError:
+        return False
+    return len(prog.leaves) <= R.MAX_IN and len(prog.insns) <= R.MAX_PROG and len(exprs) <= R.MAX_OUT
+
+
+class Program:
+    """Expression DAG -> SSA bytecode (spx_insn)."""
+
+    def __init__(self):
+        self.leaves: list[Leaf] = []
+        self.insns: list[tuple] = []   # (op, a, b, imm)
+        self.out_regs: list[int] = []
+
+    @staticmethod
+    def build(exprs) -> "Program":
+        p = Program()
+        memo = {}
+
+        def leaf_reg(l):
+            if l not in p.leaves:
+                p.leaves.append(l)
+            return p.leaves.index(l)
+
+        def emit(op, a=0, b=0, imm=0.0):
+            p.insns.append((op, a, b, float(imm)))
+            return R.REG_T + len(p.insns) - 1
+
+        def reg(x):
+            if isinstance(x, Leaf):
+                return leaf_reg(x)
+            if isinstance(x, np.float32) or isinstance(x, float):
+                return emit(R.OP["IMM"], 0, 0, x)
+            if x.uid in memo:
+                return memo[x.uid]
+            if x.op in ("add", "mul"):
+                a, b = x.kids
+                ca, cb = isinstance(a, (np.float32, float)), isinstance(b, (np.float32, float))
+                if cb and not ca:
+                    r = emit(R.OP["ADDI" if x.op == "add" else "MULI"], reg(a), 0, b)
+                elif ca and not cb:
+                    r = emit(R.OP["IADD" if x.op == "add" else "IMUL"], reg(b), 0, a)
+                else:
+                    ra, rb = reg(a), reg(b)
+                    r = emit(R.OP["ADD" if x.op == "add" else "MUL"], ra, rb)
+            elif x.op == "neg":
+                r = emit(R.OP["NEG"], reg(x.kids[0]))
+            elif x.op == "exp":
+                r = emit(R.OP["EXP"], reg(x.kids[0]))
+            else:
+                raise ValueError(x.op)
+            memo[x.uid] = r
+            return r
+
+        for e in exprs.values() if isinstance(exprs, dict) else exprs:
+            p.out_regs.append(reg(e))
+        if len(p.insns) > R.MAX_PROG or len(p.leaves) > R.MAX_IN:
+            raise ValueError("expression too large")
+        return p

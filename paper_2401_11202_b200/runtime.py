@@ -1,0 +1,264 @@
+"""ctypes binding of the C-ABI (include/spindle_b200.h).
+
+The structures below mirror the header field for field; `check_abi()` asks
+the library for its record sizes so a header/binding mismatch fails loudly.
+There is no CPU fallback: if the library is missing the product path raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspindle_b200.so")
+
+MAX_RANK, MAX_IN, MAX_OUT, MAX_PROG = 6, 8, 4, 28
+REG_T = 32
+
+OP = dict(MOV=0, ADD=1, MUL=2, NEG=3, EXP=4, MAX=5, IMM=6, ADDI=7, MULI=8, IADD=9, IMUL=10)
+K_EW, K_REDUCE, K_GEMM, K_GATHER, K_CREDUCE, K_NCCL = 1, 2, 3, 4, 5, 6
+NCCL_ALLREDUCE, NCCL_ALLGATHER, NCCL_REDUCESCATTER, NCCL_ALLTOALL = 0, 1, 2, 3
+
+I64R = C.c_int64 * MAX_RANK
+
+
+class Insn(C.Structure):
+    _fields_ = [("op", C.c_int32), ("a", C.c_int32), ("b", C.c_int32), ("pad", C.c_int32)]
+
+
+class View(C.Structure):
+    _fields_ = [("off", C.c_int64), ("stride", I64R)]
+
+
+class EwParams(C.Structure):
+    _fields_ = [("base", C.c_uint64), ("dev_stride", C.c_int64),
+                ("ndev", C.c_int32), ("rank", C.c_int32), ("n_in", C.c_int32),
+                ("n_out", C.c_int32), ("n_prog", C.c_int32), ("vec", C.c_int32),
+                ("dims", I64R), ("numel", C.c_int64),
+                ("inp", View * MAX_IN),
+                ("out_off", C.c_int64 * MAX_OUT), ("out_reg", C.c_int32 * MAX_OUT),
+                ("prog", Insn * MAX_PROG), ("imm", C.c_float * MAX_PROG)]
+
+
+class ReduceParams(C.Structure):
+    _fields_ = [("x", EwParams), ("monoid", C.c_int32), ("n_kept", C.c_int32),
+                ("n_red", C.c_int32), ("pad", C.c_int32),
+                ("kept_dims", I64R), ("kept_stride", I64R),
+                ("red_dims", I64R), ("red_stride", I64R),
+                ("n_out", C.c_int64), ("n_red_elems", C.c_int64),
+                ("out_off", C.c_int64), ("scratch_off", C.c_int64)]
+
+
+class GemmParams(C.Structure):
+    _fields_ = [("base", C.c_uint64), ("dev_stride", C.c_int64),
+                ("ndev", C.c_int32), ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32),
+                ("a_off", C.c_int64), ("b_off", C.c_int64), ("c_off", C.c_int64),
+                ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
+                ("a_mn_major", C.c_int32), ("b_k_major", C.c_int32),
+                ("path", C.c_int32), ("pad", C.c_int32)]
+
+
+class GatherParams(C.Structure):
+    _fields_ = [("ndev", C.c_int32), ("rank", C.c_int32), ("n_combo", C.c_int32), ("pad", C.c_int32),
+                ("dims", I64R), ("ext", I64R), ("cmul", I64R), ("sstride", I64R),
+                ("numel", C.c_int64), ("src_table", C.c_uint64), ("base_off", C.c_uint64),
+                ("dst", C.c_uint64)]
+
+
+class CreduceParams(C.Structure):
+    _fields_ = [("ndev", C.c_int32), ("rank", C.c_int32), ("n_members", C.c_int32),
+                ("monoid", C.c_int32), ("dims", I64R), ("sstride", I64R), ("numel", C.c_int64),
+                ("src", C.c_uint64), ("members", C.c_uint64), ("base_off", C.c_uint64),
+                ("dst", C.c_uint64)]
+
+
+class NcclParams(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("comm", C.c_int32), ("monoid", C.c_int32), ("pad", C.c_int32),
+                ("send", C.c_uint64), ("recv", C.c_uint64), ("count", C.c_int64)]
+
+
+PARAMS = {K_EW: EwParams, K_REDUCE: ReduceParams, K_GEMM: GemmParams,
+          K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams}
+
+EXPORTS = [
+    "spx_last_error", "spx_version", "spx_params_size", "spx_device_init", "spx_malloc", "spx_free",
+    "spx_memcpy_h2d", "spx_memcpy_d2h", "spx_memset", "spx_stream_create", "spx_stream_sync",
+    "spx_stream_destroy", "spx_nccl_get_unique_id", "spx_comm_init", "spx_comm_destroy",
+    "spx_plan_create", "spx_plan_add", "spx_plan_finalize", "spx_plan_run", "spx_plan_capture",
+    "spx_plan_replay", "spx_plan_launch_count", "spx_plan_destroy", "spx_plan_record_info",
+    "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
+    "spx_plan_profile",
+]
+
+_lib = None
+
+
+class BackendError(RuntimeError):
+    pass
+
+
+def load(build_if_missing: bool = True):
+    """Load libspindle_b200.so (building it in-tree if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH) and build_if_missing:
+        from .build import build
+        build()
+    if not os.path.exists(LIB_PATH):
+        raise BackendError(f"{LIB_PATH} missing: the CUDA backend is not built "
+                           "(python -m paper_2401_11202_b200.build)")
+    lib = C.CDLL(LIB_PATH)
+    lib.spx_last_error.restype = C.c_char_p
+    u64p = C.POINTER(C.c_uint64)
+    sigs = {
+        "spx_malloc": [C.c_uint64, u64p], "spx_free": [C.c_uint64],
+        "spx_memcpy_h2d": [C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64],
+        "spx_memcpy_d2h": [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64],
+        "spx_memset": [C.c_uint64, C.c_int, C.c_uint64, C.c_uint64],
+        "spx_stream_create": [u64p], "spx_stream_sync": [C.c_uint64],
+        "spx_stream_destroy": [C.c_uint64],
+        "spx_plan_create": [u64p], "spx_plan_add": [C.c_uint64, C.c_int, C.c_void_p, C.c_uint64],
+        "spx_plan_finalize": [C.c_uint64], "spx_plan_run": [C.c_uint64, C.c_uint64],
+        "spx_plan_capture": [C.c_uint64, C.c_uint64], "spx_plan_replay": [C.c_uint64, C.c_uint64],
+        "spx_plan_launch_count": [C.c_uint64], "spx_plan_destroy": [C.c_uint64],
+        "spx_plan_record_info": [C.c_uint64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "spx_event_create": [u64p], "spx_event_record": [C.c_uint64, C.c_uint64],
+        "spx_event_elapsed_ms": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float)],
+        "spx_event_destroy": [C.c_uint64],
+        "spx_plan_profile": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float), C.c_int],
+        "spx_nccl_get_unique_id": [C.c_void_p],
+        "spx_comm_init": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)],
+        "spx_comm_destroy": [C.c_int], "spx_device_init": [C.c_int], "spx_params_size": [C.c_int],
+    }
+    for name, args in sigs.items():
+        getattr(lib, name).argtypes = args
+    _lib = lib
+    check_abi(lib)
+    return lib
+
+
+def check_abi(lib):
+    for kind, cls in PARAMS.items():
+        n = lib.spx_params_size(kind)
+        if n != C.sizeof(cls):
+            raise BackendError(f"ABI mismatch for record kind {kind}: C {n} bytes, Python {C.sizeof(cls)}")
+
+
+def call(fn, *args):
+    rc = fn(*args)
+    if rc != 0:
+        raise BackendError(_lib.spx_last_error().decode(errors="replace"))
+    return rc
+
+
+class Device:
+    """One GPU: arena allocations + a stream."""
+
+    def __init__(self, ordinal: int = 0):
+        self.lib = load()
+        self.ordinal = ordinal
+        call(self.lib.spx_device_init, ordinal)
+        s = C.c_uint64()
+        call(self.lib.spx_stream_create, C.byref(s))
+        self.stream = s.value
+        self._allocs = []
+
+    def malloc(self, nbytes: int) -> int:
+        p = C.c_uint64()
+        call(self.lib.spx_malloc, int(nbytes), C.byref(p))
+        self._allocs.append(p.value)
+        return p.value
+
+    def free(self, ptr: int):
+        if ptr in self._allocs:
+            self._allocs.remove(ptr)
+            call(self.lib.spx_free, ptr)
+
+    def h2d(self, dst: int, arr: np.ndarray):
+        arr = np.ascontiguousarray(arr)
+        call(self.lib.spx_memcpy_h2d, dst, arr.ctypes.data, arr.nbytes, self.stream)
+
+    def d2h(self, arr: np.ndarray, src: int):
+        assert arr.flags.c_contiguous
+        call(self.lib.spx_memcpy_d2h, arr.ctypes.data, src, arr.nbytes, self.stream)
+
+    def memset(self, dst: int, nbytes: int, value: int = 0):
+        call(self.lib.spx_memset, dst, value, nbytes, self.stream)
+
+    def sync(self):
+        call(self.lib.spx_stream_sync, self.stream)
+
+    def event(self) -> int:
+        e = C.c_uint64()
+        call(self.lib.spx_event_create, C.byref(e))
+        return e.value
+
+    def record(self, ev: int):
+        call(self.lib.spx_event_record, ev, self.stream)
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        out = C.c_float()
+        call(self.lib.spx_event_elapsed_ms, a, b, C.byref(out))
+        return float(out.value)
+
+    def close(self):
+        for p in list(self._allocs):
+            self.free(p)
+
+
+class NativePlan:
+    """A finalized sequence of records on one device."""
+
+    def __init__(self, device: Device):
+        self.dev = device
+        self.lib = device.lib
+        h = C.c_uint64()
+        call(self.lib.spx_plan_create, C.byref(h))
+        self.h = h.value
+        self.n_records = 0
+        self.captured = False
+
+    def add(self, kind: int, params):
+        assert isinstance(params, PARAMS[kind])
+        call(self.lib.spx_plan_add, self.h, kind, C.byref(params), C.sizeof(params))
+        self.n_records += 1
+
+    def finalize(self):
+        call(self.lib.spx_plan_finalize, self.h)
+
+    def run(self):
+        call(self.lib.spx_plan_run, self.h, self.dev.stream)
+
+    def capture(self):
+        call(self.lib.spx_plan_capture, self.h, self.dev.stream)
+        self.captured = True
+
+    def replay(self):
+        call(self.lib.spx_plan_replay, self.h, self.dev.stream)
+
+    def launch_count(self) -> int:
+        return int(self.lib.spx_plan_launch_count(self.h))
+
+    def record_info(self, i: int):
+        k, p = C.c_int(), C.c_int()
+        call(self.lib.spx_plan_record_info, self.h, i, C.byref(k), C.byref(p))
+        return k.value, p.value
+
+    def profile(self) -> np.ndarray:
+        out = (C.c_float * self.n_records)()
+        call(self.lib.spx_plan_profile, self.h, self.dev.stream, out, self.n_records)
+        return np.array(out[:], dtype=np.float64)
+
+    def destroy(self):
+        if self.h:
+            self.lib.spx_plan_destroy(self.h)
+            self.h = 0
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass

@@ -1,0 +1,212 @@
+"""CPU simulator of the native plan records (test infrastructure only).
+
+Executes the records an `Executable(dry=True)` emits against a numpy model of
+the device arena, following the kernel contracts in include/spindle_b200.h.
+It lets the CPU suite check the plan compiler (views, fusion, multi-output
+merging, liveness packing, collective tables) against the oracle without a
+GPU; the GPU tests then check the kernels themselves.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2401_11202_b200 import runtime as R
+
+
+class Sim:
+    def __init__(self, ex):
+        self.ex = ex
+        self.arena = np.full(ex.slice_elems * ex.ndev, np.nan, dtype=np.float32)
+        self.tables = ex.table_blob
+        self.arena[ex.zero_off:ex.zero_off + ex.zero_elems] = 0.0
+
+    # addresses -> arena element index
+    def idx(self, addr):
+        return (int(addr) - self.ex.base) // 4
+
+    def table(self, addr, dtype, n):
+        o = int(addr) - self.ex.table_base
+        return np.frombuffer(self.tables[o:o + n * np.dtype(dtype).itemsize].tobytes(), dtype=dtype)
+
+    def dev_base(self, p):
+        return p * self.ex.slice_elems
+
+    def gather_view(self, p, off, strides, dims):
+        dims = [int(d) for d in dims]
+        index = np.full(dims, self.dev_base(p) + int(off), dtype=np.int64)
+        for k, d in enumerate(dims):
+            shape = [1] * len(dims)
+            shape[k] = d
+            index = index + np.arange(d, dtype=np.int64).reshape(shape) * int(strides[k])
+        return self.arena[index]
+
+    def eval_prog(self, x, ins):
+        regs = {}
+        for j, a in enumerate(ins):
+            regs[j] = a
+        shape = ins[0].shape if ins else None
+        with np.errstate(all="ignore"):
+            for i in range(x.n_prog):
+                ins_ = x.prog[i]
+                op, a, b, imm = ins_.op, ins_.a, ins_.b, np.float32(x.imm[i])
+                A = regs.get(a)
+                B = regs.get(b)
+                if op == R.OP["MOV"]:
+                    v = A
+                elif op == R.OP["ADD"]:
+                    v = np.add(A, B)
+                elif op == R.OP["MUL"]:
+                    v = np.multiply(A, B)
+                elif op == R.OP["NEG"]:
+                    v = -A
+                elif op == R.OP["EXP"]:
+                    v = np.exp(A)
+                elif op == R.OP["MAX"]:
+                    v = np.maximum(A, B)
+                elif op == R.OP["IMM"]:
+                    v = imm
+                elif op == R.OP["ADDI"]:
+                    v = np.add(A, imm)
+                elif op == R.OP["MULI"]:
+                    v = np.multiply(A, imm)
+                elif op == R.OP["IADD"]:
+                    v = np.add(imm, A)
+                elif op == R.OP["IMUL"]:
+                    v = np.multiply(imm, A)
+                else:
+                    raise AssertionError(op)
+                regs[R.REG_T + i] = np.asarray(v, dtype=np.float32)
+        return regs
+
+    def run_ew(self, x: R.EwParams):
+        dims = [x.dims[k] for k in range(x.rank)]
+        for p in range(x.ndev):
+            ins = [self.gather_view(p, x.inp[j].off, x.inp[j].stride, dims) for j in range(x.n_in)]
+            regs = self.eval_prog(x, ins)
+            for o in range(x.n_out):
+                v = np.broadcast_to(regs[x.out_reg[o]], dims).reshape(-1)
+                s = self.dev_base(p) + x.out_off[o]
+                self.arena[s:s + v.size] = v
+
+    def run_reduce(self, r: R.ReduceParams):
+        x = r.x
+        dims = [x.dims[k] for k in range(x.rank)]
+        for p in range(x.ndev):
+            ins = [self.gather_view(p, x.inp[j].off, x.inp[j].stride, dims) for j in range(x.n_in)]
+            regs = self.eval_prog(x, ins)
+            v = np.broadcast_to(regs[x.out_reg[0]], dims)
+            axes = tuple(range(r.n_kept, x.rank))
+            red = np.sum(v, axis=axes, dtype=np.float32) if r.monoid == 0 else np.max(v, axis=axes)
+            red = np.asarray(red, dtype=np.float32).reshape(-1)
+            s = self.dev_base(p) + r.out_off
+            self.arena[s:s + red.size] = red
+
+    def run_gemm(self, g: R.GemmParams):
+        for p in range(g.ndev):
+            if g.a_mn_major:
+                A = self.gather_view(p, g.a_off, (1, g.lda), (g.M, g.K))
+            else:
+                A = self.gather_view(p, g.a_off, (g.lda, 1), (g.M, g.K))
+            if g.b_k_major:
+                B = self.gather_view(p, g.b_off, (1, g.ldb), (g.K, g.N))
+            else:
+                B = self.gather_view(p, g.b_off, (g.ldb, 1), (g.K, g.N))
+            C = (A.astype(np.float64) @ B.astype(np.float64)).astype(np.float32)
+            for m in range(g.M):
+                s = self.dev_base(p) + g.c_off + m * g.ldc
+                self.arena[s:s + g.N] = C[m]
+
+    def run_gather(self, g: R.GatherParams):
+        dims = [g.dims[k] for k in range(g.rank)]
+        n = g.ndev * g.n_combo
+        table = self.table(g.src_table, np.uint64, n)
+        base = self.table(g.base_off, np.int64, g.ndev)
+        dst = self.table(g.dst, np.uint64, g.ndev)
+        l = np.indices(dims).reshape(len(dims), -1) if dims else np.zeros((0, 1), np.int64)
+        for p in range(g.ndev):
+            combo = np.zeros(l.shape[1], np.int64)
+            soff = np.full(l.shape[1], base[p], np.int64)
+            for k in range(g.rank):
+                q, r = l[k] // g.ext[k], l[k] % g.ext[k]
+                combo += q * g.cmul[k]
+                soff += r * g.sstride[k]
+            src = np.array([self.idx(table[p * g.n_combo + c]) for c in combo], dtype=np.int64)
+            vals = self.arena[src + soff]
+            d0 = self.idx(dst[p])
+            self.arena[d0:d0 + vals.size] = vals
+
+    def run_creduce(self, r: R.CreduceParams):
+        dims = [r.dims[k] for k in range(r.rank)]
+        src = self.table(r.src, np.uint64, r.ndev)
+        mem = self.table(r.members, np.int32, r.ndev * r.n_members)
+        base = self.table(r.base_off, np.int64, r.ndev)
+        dst = self.table(r.dst, np.uint64, r.ndev)
+        l = np.indices(dims).reshape(len(dims), -1) if dims else np.zeros((0, 1), np.int64)
+        out = []
+        for p in range(r.ndev):
+            soff = np.full(l.shape[1], base[p], np.int64)
+            for k in range(r.rank):
+                soff += l[k] * r.sstride[k]
+            acc = None
+            for j in range(r.n_members):
+                v = self.arena[self.idx(src[mem[p * r.n_members + j]]) + soff]
+                acc = v if acc is None else (np.add(acc, v) if r.monoid == 0 else np.maximum(acc, v))
+            out.append(acc)
+        for p in range(r.ndev):          # all reads before writes (distinct buffers anyway)
+            d0 = self.idx(dst[p])
+            self.arena[d0:d0 + out[p].size] = out[p]
+
+    def run(self):
+        for kind, p in self.ex.records():
+            {R.K_EW: self.run_ew, R.K_REDUCE: self.run_reduce, R.K_GEMM: self.run_gemm,
+             R.K_GATHER: self.run_gather, R.K_CREDUCE: self.run_creduce}[kind](p)
+
+    def upload(self, per_device):
+        for p in range(self.ex.ndev):
+            for a in self.ex.comp.arg_bufs:
+                v = np.asarray(per_device[p][a], dtype=np.float32).reshape(-1)
+                s = self.dev_base(p) + self.ex.off[a]
+                self.arena[s:s + v.size] = v
+
+    def results(self):
+        f = self.ex.comp.f
+        out = []
+        for j, b in enumerate(self.ex.comp.result_bufs):
+            dims = tuple(f.result_types[j].dims)
+            n = int(np.prod(dims)) if dims else 1
+            per = []
+            for p in range(self.ex.ndev):
+                s = self.dev_base(p) + self.ex.off[b]
+                per.append(self.arena[s:s + n].reshape(dims).copy())
+            out.append(per)
+        return out
+
+
+def sim_spmd(module, spec, inputs, tol=1e-5):
+    """spmd_interpret through the record simulator (mirrors evaluator.spmd_interpret)."""
+    from paper_2401_11202_b200.evaluator import _chunk_slices, unshard
+    from paper_2401_11202_b200.executable import Executable
+    f = module.func("main")
+    mesh = module.mesh
+    coords = mesh.coords()
+    arrays = [np.asarray(inputs[n]) for n in f.arg_names()]
+    per = []
+    for c in coords:
+        per.append({n: a[_chunk_slices(a.shape, spec.args[n], mesh, c)] for a, (n, _) in zip(arrays, f.args)})
+    ex = Executable(module, dry=True)
+    sim = Sim(ex)
+    sim.upload(per)
+    sim.run()
+    res = sim.results()
+    return [unshard(res[j], spec.results[j], mesh, coords, tol, f"result {j}") for j in range(len(res))], ex
+
+
+def sim_dense(module, inputs):
+    from paper_2401_11202_b200.evaluator import _Dense
+    from paper_2401_11202_b200.executable import Executable
+    f = module.func("main")
+    ex = Executable(_Dense(module), devices=[0], dry=True)
+    sim = Sim(ex)
+    sim.upload([{n: np.asarray(inputs[n]) for n in f.arg_names()}])
+    sim.run()
+    return [r[0] for r in sim.results()], ex

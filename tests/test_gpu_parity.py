@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path against the reference's golden outputs and the
+oracle restatement, through the drop-in `spmd_interpret` / `interpret`.
+
+Bars: bit-exact for data movement and fp32 add/mul/neg;
+<= 1e-5 max-normalised relative error (`relative_error`, spmd_interp.py:25-31)
+for matmul, reduce, all_reduce/reduce_scatter sums and exp.  All outputs are
+checked finite first.
+"""
+import numpy as np
+import pytest
+
+from conftest import TOL, case_expected, case_inputs, golden_cases, requires_gpu
+from oracle import spmd_oracle as O
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+
+CASES = golden_cases()
+
+
+def _pkg():
+    import paper_2401_11202_b200 as pkg
+    return pkg
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "local_ir" in c], ids=lambda c: c["key"])
+def test_spmd_golden(case):
+    pkg = _pkg()
+    m = pkg.parse_module(case["local_ir"])
+    spec = pkg.ShardingSpec.from_json(case["sharding"])
+    base = pkg.parse_module(case["dense_ir"]) if "dense_ir" in case else m
+    for s in case["seeds"]:
+        ins = case_inputs(case, base, s)
+        if case.get("error") == "DivergenceError":
+            with pytest.raises(pkg.DivergenceError):
+                pkg.spmd_interpret(m, spec, ins)
+            continue
+        got = pkg.spmd_interpret(m, spec, ins)
+        for g, w in zip(got, case_expected(case, s, "spmd")):
+            assert np.all(np.isfinite(g))
+            if case["group"] == "rule" and "exp" not in case["local_ir"]:
+                np.testing.assert_array_equal(g, w)
+            else:
+                assert O.relative_error(g, w) < TOL
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "dense_ir" in c], ids=lambda c: c["key"])
+def test_dense_golden(case):
+    pkg = _pkg()
+    m = pkg.parse_module(case["dense_ir"])
+    for s in case["seeds"]:
+        ins = case_inputs(case, m, s)
+        got = pkg.interpret(m, ins)
+        for g, w in zip(got, case_expected(case, s, "dense")):
+            assert np.all(np.isfinite(g))
+            if case["key"] in ("op_add", "op_mul", "op_neg", "op_tag", "op_transpose2", "op_transpose3",
+                               "op_reshape1", "op_reshape2", "op_reshape3", "op_broadcast0",
+                               "op_broadcast1", "op_broadcast2", "op_reduce1max", "op_reduce0max3"):
+                np.testing.assert_array_equal(g, w)
+            else:
+                assert O.relative_error(g, w) < TOL
+
+
+def _mm_module(M, K, N, at=False, bt=False):
+    """matmul with optionally transposed operands (stored transposed, then a
+    `transpose` op feeds the matmul -- the pattern of matmul_grads, models.py:64-71)."""
+    a_t = f"tensor<{K}x{M}xf32>" if at else f"tensor<{M}x{K}xf32>"
+    b_t = f"tensor<{N}x{K}xf32>" if bt else f"tensor<{K}x{N}xf32>"
+    lines = [f"func @main(%a: {a_t}, %b: {b_t}) -> tensor<{M}x{N}xf32> {{"]
+    a, b = "%a", "%b"
+    if at:
+        lines.append(f"  %at = transpose %a {{perm = [1, 0]}} : tensor<{M}x{K}xf32>")
+        a = "%at"
+    if bt:
+        lines.append(f"  %bt = transpose %b {{perm = [1, 0]}} : tensor<{K}x{N}xf32>")
+        b = "%bt"
+    lines.append(f"  %c = matmul {a}, {b} : tensor<{M}x{N}xf32>")
+    lines.append("  return %c\n}\n")
+    return _pkg().parse_module("\n".join(lines))
+
+
+GEMM_SHAPES = [
+    (128, 128, 128), (256, 512, 384), (1024, 1024, 1024), (2048, 1024, 4096),
+    (1024, 2048, 1024), (192, 96, 160), (130, 70, 200), (1024, 128, 1024),
+]
+
+
+@pytest.mark.parametrize("at,bt", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("shape", GEMM_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_gemm_tcgen05_3xtf32(shape, at, bt):
+    """tcgen05 3xTF32 GEMM vs float64 numpy: <= 1e-5 max-normalised (fp32 parity)."""
+    pkg = _pkg()
+    M, K, N = shape
+    if shape == (130, 70, 200) and (at or bt):
+        pytest.skip("TMA needs 16B row pitch; 130/70 rows exercise the SIMT fallback elsewhere")
+    rng = np.random.default_rng(hash(shape) % 1000)
+    a = rng.standard_normal((K, M) if at else (M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K) if bt else (K, N)).astype(np.float32)
+    m = _mm_module(M, K, N, at, bt)
+    A = a.T if at else a
+    B = b.T if bt else b
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    path = 0 if (M % 4 or K % 4 or N % 4) else 1
+    (got,) = pkg.interpret(m, {"a": a, "b": b}, gemm_path=path)
+    assert np.all(np.isfinite(got))
+    err = O.relative_error(got, want)
+    assert err < TOL, err
+    # and vs numpy's own float32 matmul (the oracle's arithmetic)
+    assert O.relative_error(got, A @ B) < TOL
+
+
+@pytest.mark.parametrize("shape", [(5, 7, 3), (64, 48, 80), (130, 70, 200), (256, 512, 384)])
+def test_gemm_simt(shape):
+    pkg = _pkg()
+    M, K, N = shape
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    (got,) = pkg.interpret(_mm_module(M, K, N), {"a": a, "b": b}, gemm_path=2)
+    assert O.relative_error(got, a.astype(np.float64) @ b) < TOL
+
+
+def test_elementwise_bitexact_large():
+    """Fused add/mul/neg chains are bit-exact vs numpy at HBM-scale sizes."""
+    pkg = _pkg()
+    text = """func @main(%p: tensor<2048x4096xf32>, %m: tensor<2048x4096xf32>, %g: tensor<2048x4096xf32>, %b: tensor<4096xf32>) -> (tensor<2048x4096xf32>, tensor<2048x4096xf32>, tensor<2048x4096xf32>) {
+  %c1 = constant 0.9 : tensor<2048x4096xf32>
+  %a = mul %c1, %m : tensor<2048x4096xf32>
+  %new_m = add %a, %g : tensor<2048x4096xf32>
+  %c2 = constant 0.01 : tensor<2048x4096xf32>
+  %s = mul %c2, %new_m : tensor<2048x4096xf32>
+  %n = neg %s : tensor<2048x4096xf32>
+  %new_p = add %p, %n : tensor<2048x4096xf32>
+  %bb = broadcast %b {dims = [1]} : tensor<2048x4096xf32>
+  %z = add %g, %bb : tensor<2048x4096xf32>
+  %sq = mul %z, %z : tensor<2048x4096xf32>
+  return %new_p, %new_m, %sq
+}
+"""
+    m = pkg.parse_module(text)
+    rng = np.random.default_rng(0)
+    ins = {n: rng.standard_normal(t.dims).astype(np.float32) for n, t in m.func("main").args}
+    got = pkg.interpret(m, ins)
+    want = O.interpret(m, ins)
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g, w)
+
+
+@pytest.mark.parametrize("dims,red", [((2048, 1024), [0]), ((2048, 1024), [0, 1]), ((2048, 1024), [1]),
+                                      ((16, 64, 32), [0, 2]), ((8, 8, 8, 16), [1, 3])])
+def test_reduce_large(dims, red):
+    pkg = _pkg()
+    t = "x".join(map(str, dims))
+    kept = [d for i, d in enumerate(dims) if i not in red]
+    rt = "tensor<" + "x".join(map(str, kept)) + ("x" if kept else "") + "f32>"
+    text = (f"func @main(%x: tensor<{t}xf32>) -> {rt} {{\n"
+            f"  %sq = mul %x, %x : tensor<{t}xf32>\n"
+            f"  %r = reduce %sq {{dims = {red}}} : {rt}\n  return %r\n}}\n")
+    m = pkg.parse_module(text)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(dims).astype(np.float32)
+    (got,) = pkg.interpret(m, {"x": x})
+    want = np.sum(x.astype(np.float64) ** 2, axis=tuple(red))
+    assert O.relative_error(got, want) < TOL
+
+
+def test_launch_counts_and_graph_replay():
+    """A compiled plan replays as one CUDA graph and reproduces the eager run."""
+    pkg = _pkg()
+    from paper_2401_11202_b200.executable import Executable
+    from paper_2401_11202_b200.evaluator import default_device
+    case = next(c for c in CASES if c["key"] == "step_tf2_bpmp_B2M2")
+    m = pkg.parse_module(case["local_ir"])
+    spec = pkg.ShardingSpec.from_json(case["sharding"])
+    base = pkg.parse_module(case["dense_ir"])
+    ins = case_inputs(case, base, 0)
+    from paper_2401_11202_b200.evaluator import _chunk_slices
+    mesh = m.mesh
+    f = m.func("main")
+    per = [{n: ins[n][_chunk_slices(ins[n].shape, spec.args[n], mesh, c)] for n, _ in f.args}
+           for c in mesh.coords()]
+    ex = Executable(m, device=default_device())
+    ex.upload_args(per)
+    ex.run()
+    eager = ex.download_results()
+    n_eager = ex.plan.launch_count()
+    ex.plan.capture()
+    ex.plan.replay()
+    ex.device.sync()
+    replay = ex.download_results()
+    ex.close()
+    assert n_eager > 0
+    for a, b in zip(eager, replay):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)

@@ -1,0 +1,81 @@
+"""Plan compiler on CPU: lower every golden program to native records, execute
+them with the record simulator, and compare with the reference's outputs.
+Also checks the executed collective counts and FLOPs against the simulator
+(`collective_counts`, spmd.py:264-271; `simulate().compute_flops`,
+sim.py:209-229) as recorded in the golden cases."""
+import numpy as np
+import pytest
+
+from conftest import TOL, case_expected, case_inputs, golden_cases
+from oracle.spmd_oracle import DivergenceError as OracleDivergence
+from paper_2401_11202_b200.evaluator import DivergenceError, relative_error
+from paper_2401_11202_b200.ir import ShardingSpec, parse_module
+from record_sim import sim_dense, sim_spmd
+
+CASES = golden_cases()
+
+# data movement / elementwise programs must be bit-exact (SURVEY §8c parity rules)
+BITEXACT_GROUPS = ("rule",)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "local_ir" in c], ids=lambda c: c["key"])
+def test_plan_spmd_sim(case):
+    m = parse_module(case["local_ir"])
+    spec = ShardingSpec.from_json(case["sharding"])
+    base = parse_module(case["dense_ir"]) if "dense_ir" in case else m
+    for s in case["seeds"]:
+        ins = case_inputs(case, base, s)
+        if case.get("error") == "DivergenceError":
+            with pytest.raises(DivergenceError):
+                sim_spmd(m, spec, ins)
+            continue
+        got, ex = sim_spmd(m, spec, ins)
+        assert ex.comp.counts == case["counts"]
+        if "compute_flops" in case:
+            assert ex.comp.flops == case["compute_flops"]
+        for g, w in zip(got, case_expected(case, s, "spmd")):
+            assert np.all(np.isfinite(g))
+            if case["group"] in BITEXACT_GROUPS and "exp" not in case["local_ir"]:
+                np.testing.assert_array_equal(g, w)
+            else:
+                assert relative_error(g, w) < TOL
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "dense_ir" in c], ids=lambda c: c["key"])
+def test_plan_dense_sim(case):
+    m = parse_module(case["dense_ir"])
+    for s in case["seeds"]:
+        ins = case_inputs(case, m, s)
+        got, _ = sim_dense(m, ins)
+        for g, w in zip(got, case_expected(case, s, "dense")):
+            assert g.shape == w.shape
+            assert relative_error(g, w) < TOL
+
+
+def test_momentum_update_is_one_kernel():
+    """m' = 0.9 m + g ; p' = p + -(0.01 m') fuses into one two-output kernel."""
+    from paper_2401_11202_b200.executable import Executable
+    text = """func @main(%p: tensor<64x64xf32>, %m: tensor<64x64xf32>, %g: tensor<64x64xf32>) -> (tensor<64x64xf32>, tensor<64x64xf32>) {
+  %c1 = constant 0.9 : tensor<64x64xf32>
+  %a = mul %c1, %m : tensor<64x64xf32>
+  %new_m = add %a, %g : tensor<64x64xf32>
+  %c2 = constant 0.01 : tensor<64x64xf32>
+  %b = mul %c2, %new_m : tensor<64x64xf32>
+  %n = neg %b : tensor<64x64xf32>
+  %new_p = add %p, %n : tensor<64x64xf32>
+  return %new_p, %new_m
+}
+"""
+    m = parse_module(text)
+    ex = Executable(m, devices=[0], dry=True)
+    kinds = [k for k, _ in ex.records()]
+    assert kinds == [1]                     # a single EW record
+    (_, p), = ex.records()
+    assert p.n_out == 2 and p.n_in == 3 and p.vec == 1
+    rng = np.random.default_rng(0)
+    ins = {n: rng.standard_normal((64, 64)).astype(np.float32) for n in ("p", "m", "g")}
+    got, _ = sim_dense(m, ins)
+    from oracle.spmd_oracle import interpret
+    want = interpret(m, ins)
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g, w)
