@@ -107,7 +107,7 @@ typedef struct {
   int32_t a_mn_major;             /* 0: A stored [M][K]; 1: A stored [K][M]    */
   int32_t b_k_major;              /* 0: B stored [K][N]; 1: B stored [N][K]    */
   int32_t path;                   /* 0 auto, 1 tcgen05 3xTF32, 2 SIMT fp32     */
-  int32_t pad;
+  int32_t debug;                  /* 0; diagnostics bits for the tcgen05 path  */
 } spx_gemm_params;
 
 /* ---- collectives over co-located virtual devices ------------------------- */

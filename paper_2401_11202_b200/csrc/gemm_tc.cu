@@ -30,7 +30,7 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
 constexpr int STAGES = 3;
-constexpr int NTHREADS = 192;
+constexpr int NTHREADS = 320;   // TMA, MMA, 4 split warps, 4 drain warps
 
 SPX_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -72,10 +72,12 @@ SPX_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c
       : "memory");
 }
 
-// UMMA shared-memory descriptor, 128B swizzle (layout type 2), sm_100 version 1.
-SPX_DEV uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (sm_100 version 1).  Layout type 2 =
+// SWIZZLE_128B (16B atoms; K-major operands), 1 = SWIZZLE_128B_BASE32B (32B
+// atoms; the only MN-major layout tf32 operands support).
+SPX_DEV uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 
 SPX_DEV void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -92,7 +94,7 @@ SPX_DEV void mma_commit(uint64_t* bar) {
 }
 
 struct TcArgs {
-  int M, N, K, a_mn_major, b_k_major;
+  int M, N, K, a_mn_major, b_k_major, promote;  // promote: k-blocks per TMEM chunk
   uint64_t c_base;     // device 0 address of C
   int64_t dev_stride;  // bytes
   int64_t ldc;
@@ -107,6 +109,25 @@ struct Smem {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
 };
 
+SPX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+// Tensor-core accumulation is not IEEE fp32 round-to-nearest: measured on
+// B200 its error grows linearly with K (3e-5 at K=4096).  The kernel
+// therefore accumulates `promote` k-blocks at a time in one of two TMEM
+// accumulators and folds each finished chunk into fp32 registers
+// (__fadd_rn) held by the drain warps, while the tensor core fills the other
+// accumulator -- error stays ~1e-6 independent of K.
 template <int BN>
 __global__ void __launch_bounds__(NTHREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -117,12 +138,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* split = full + STAGES;
   uint64_t* empty = split + STAGES;
-  uint64_t* accum = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* tfull = empty + STAGES;     // [2] chunk accumulated (MMA commit)
+  uint64_t* tempty = tfull + 2;         // [2] chunk drained (128 drain threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, dev = blockIdx.z;
   const int nk = (args.K + BK - 1) / BK;
+  const int P = args.promote;
+  const int nchunks = (nk + P - 1) / P;
 
   auto a_hi = [&](int s) { return smem + s * S::STAGE; };
   auto a_lo = [&](int s) { return smem + s * S::STAGE + S::A_BYTES; };
@@ -135,14 +159,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       mbar_init(&split[s], 128);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -180,33 +207,44 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)args.a_mn_major << 15) |
                              ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
-      // K-major: LBO unused (16B), SBO = 8 rows x 128B; k-step of 8 fp32 = +32B.
-      // MN-major: LBO = 32-element MN chunk stride (32 rows x 128B), SBO = 8 k-rows x 128B; k-step = +1024B.
+      // K-major (SW128, 16B atoms): LBO unused, SBO = 8 rows x 128B; a k-step of
+      //   8 fp32 advances the start address by 32B inside the swizzle row.
+      // MN-major (SW128_BASE32B): LBO = stride of 32-element MN chunks (32 k-rows
+      //   x 128B), SBO = 4 k-rows x 128B; a k-step (8 rows) advances 1024B.
       const uint32_t a_lbo = args.a_mn_major ? 4096u : 16u, a_step = args.a_mn_major ? 1024u : 32u;
       const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
+      const uint32_t a_sbo = args.a_mn_major ? 512u : 1024u, b_sbo = args.b_k_major ? 1024u : 512u;
+      const uint32_t a_lay = args.a_mn_major ? 1u : 2u, b_lay = args.b_k_major ? 2u : 1u;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         const uint32_t round = kb / STAGES;
+        const int c = kb / P, buf = c & 1;
+        const bool chunk_first = (kb % P) == 0;
+        const bool chunk_last = (kb % P) == P - 1 || kb == nk - 1;
+        if (chunk_first) {
+          mbar_wait(&tempty[buf], ((c >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
         mbar_wait(&split[s], round & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t ahi = smem_u32(a_hi(s)), alo = smem_u32(a_lo(s));
         const uint32_t bhi = smem_u32(b_hi(s)), blo = smem_u32(b_lo(s));
+        const uint32_t dacc = tmem_d + (uint32_t)(buf * BN);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t dah = smem_desc(ahi + kk * a_step, a_lbo, 1024);
-          const uint64_t dal = smem_desc(alo + kk * a_step, a_lbo, 1024);
-          const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, 1024);
-          const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, 1024);
-          const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
-          mma_tf32(tmem_d, dal, dbh, idesc, first);   // small terms first
-          mma_tf32(tmem_d, dah, dbl, idesc, 1u);
-          mma_tf32(tmem_d, dah, dbh, idesc, 1u);
+          const uint64_t dah = smem_desc(ahi + kk * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = smem_desc(alo + kk * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
+          mma_tf32(dacc, dal, dbh, idesc, (chunk_first && kk == 0) ? 0u : 1u);   // small terms first
+          mma_tf32(dacc, dah, dbl, idesc, 1u);
+          mma_tf32(dacc, dah, dbh, idesc, 1u);
         }
         mma_commit(&empty[s]);
+        if (chunk_last) mma_commit(&tfull[buf]);
       }
-      mma_commit(accum);
     }
-  } else {
+  } else if (warp < 6) {
     // ---------------- split (hi/lo) ----------------
     const int t = threadIdx.x - 64;  // 0..127
     for (int kb = 0; kb < nk; ++kb) {
@@ -240,40 +278,44 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&split[s]);
     }
-    // ---------------- epilogue ----------------
-    mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  } else {
+    // ---------------- drain + epilogue ----------------
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(&tfull[buf], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + cc * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __fadd_rn(acc[cc * 32 + j], __uint_as_float(v[j]));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[buf]);
+    }
     const int row = m0 + q * 32 + lane;
-    float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
-                  (int64_t)row * args.ldc;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-            "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-            "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < args.M) {
-        const int col0 = n0 + c * 32;
+    if (row < args.M) {
+      float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
+                    (int64_t)row * args.ldc;
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        const int col0 = n0 + cc * 32;
         if (col0 + 32 <= args.N && (args.ldc & 3) == 0) {
           float4* dst = reinterpret_cast<float4*>(crow + col0);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+            dst[j] = make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
+                                 acc[cc * 32 + 4 * j + 3]);
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (col0 + j < args.N) crow[col0 + j] = __uint_as_float(v[j]);
+            if (col0 + j < args.N) crow[col0 + j] = acc[cc * 32 + j];
         }
       }
     }
@@ -282,7 +324,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(2 * BN));
   }
 }
 
@@ -298,9 +340,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 3-D fp32 map {inner, outer, device}; box {32, box_outer, 1}; 128B swizzle.
+// 3-D fp32 map {inner, outer, device}; box {32, box_outer, 1}; 128B swizzle
+// with 16B atoms (K-major operands) or 32B atoms (MN-major operands).
 int make_map(CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer, uint64_t ndev, uint64_t row_bytes,
-             uint64_t dev_bytes, uint32_t box_outer) {
+             uint64_t dev_bytes, uint32_t box_outer, bool mn_major) {
   auto enc = get_encode();
   if (!enc) return spx_set_error("cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {inner, outer, ndev};
@@ -308,7 +351,9 @@ int make_map(CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer, ui
   cuuint32_t box[3] = {32, box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, reinterpret_cast<void*>(addr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return spx_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
   return 0;
@@ -338,14 +383,15 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   g->bn = 128;
   const uint64_t a = p.base + (uint64_t)(p.a_off * 4), b = p.base + (uint64_t)(p.b_off * 4);
   int rc;
-  if (p.a_mn_major) rc = make_map(&g->ma, a, p.M, p.K, p.ndev, p.lda * 4, p.dev_stride, 32);
-  else rc = make_map(&g->ma, a, p.K, p.M, p.ndev, p.lda * 4, p.dev_stride, BM);
+  if (p.a_mn_major) rc = make_map(&g->ma, a, p.M, p.K, p.ndev, p.lda * 4, p.dev_stride, 32, true);
+  else rc = make_map(&g->ma, a, p.K, p.M, p.ndev, p.lda * 4, p.dev_stride, BM, false);
   if (rc) { delete g; return rc; }
-  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, g->bn);
-  else rc = make_map(&g->mb, b, p.N, p.K, p.ndev, p.ldb * 4, p.dev_stride, 32);
+  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, g->bn, false);
+  else rc = make_map(&g->mb, b, p.N, p.K, p.ndev, p.ldb * 4, p.dev_stride, 32, true);
   if (rc) { delete g; return rc; }
   g->args.M = p.M; g->args.N = p.N; g->args.K = p.K;
   g->args.a_mn_major = p.a_mn_major; g->args.b_k_major = p.b_k_major;
+  g->args.promote = p.debug > 0 ? p.debug : 4;   // debug field: override promote
   g->args.c_base = p.base + (uint64_t)(p.c_off * 4);
   g->args.dev_stride = p.dev_stride;
   g->args.ldc = p.ldc;

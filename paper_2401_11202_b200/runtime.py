@@ -57,7 +57,7 @@ class GemmParams(C.Structure):
                 ("a_off", C.c_int64), ("b_off", C.c_int64), ("c_off", C.c_int64),
                 ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
                 ("a_mn_major", C.c_int32), ("b_k_major", C.c_int32),
-                ("path", C.c_int32), ("pad", C.c_int32)]
+                ("path", C.c_int32), ("debug", C.c_int32)]
 
 
 class GatherParams(C.Structure):
