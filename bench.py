@@ -1,0 +1,343 @@
+"""Benchmark: partitioned fwd+bwd+momentum-SGD step throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Metric (BASELINE.json): "Partitioned fwd+bwd samples/s at 1/2/4/8 B200; %
+of tensor-core/HBM roofline".  One STEP = one execution of the localized
+training-step program of the configured model (forward, hand-written
+backward and momentum update of every parameter -- models.py:152-220) on the
+global batch; samples/s = global batch / step time.  N=1 runs the
+unpartitioned module (the reference's 1-device semantics); N>1 runs
+the partitioned program one mesh device per GPU (torchrun), collectives over
+NCCL.  Scaling is STRONG (global batch fixed).
+
+`value` is device-timed (CUDA events, max over ranks) with every input
+resident in HBM; `e2e` repeats the measurement through the Session API with
+each step's batch (x, y) copied host->device from pinned memory and the loss
+read back device->host inside the timed region.  `--impl reference` times the
+reference's CPU evaluator (the oracle restatement, numpy) on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Partitioned fwd+bwd samples/s at 1/2/4/8 B200; % of tensor-core/HBM roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9 or not f[0].isdigit() or int(f[0]) not in self.gpus:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    smax = float(f[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, rank):
+    if world == 1:
+        return None
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+def max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_reference(prog, n, inputs, steps, warmup):
+    """The reference evaluator (oracle restatement; numpy on host cores)."""
+    from oracle import spmd_oracle as O
+    if n == 1:
+        fn = lambda: O.interpret(prog.dense, inputs)
+    else:
+        fn = lambda: O.spmd_interpret(prog.local, prog.sharding, inputs)
+    for _ in range(warmup):
+        fn()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)), ts
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-out", default=None, help="write per-record timings (json)")
+    args = ap.parse_args()
+
+    from paper_2401_11202_b200.programs import WORKLOADS, load_program, synthetic_inputs
+    world, rank, local = dist_env()
+    n = args.gpus
+    if world != n and not (world == 1 and n == 1):
+        raise SystemExit(f"--gpus {n} needs torchrun with {n} processes (WORLD_SIZE={world})")
+    wl = WORKLOADS[args.config]
+    prog = load_program(wl["programs"][n])
+    batch = prog.batch
+    base = prog.dense
+    mesh = prog.meta.get("mesh") or "dense (1 device)"
+    config = {"workload": f"{args.config.upper()}: {wl['desc']}", "mesh": mesh,
+              "program": prog.name, "global_batch": batch,
+              "schedule": prog.meta.get("schedule") or [], "parallelism":
+              ("none (unpartitioned)" if n == 1 else f"mesh {mesh}, one device per GPU"),
+              "l2": "working set > 126 MB L2 (params+momenta alone exceed it); no flush needed",
+              "inputs": f"synthetic N(0, {wl['scale']}^2) float32 (random_inputs generator, seed 0)"}
+    dtype = "f32"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        inputs = synthetic_inputs(base, seed=0, scale=wl["scale"])
+        steps = max(1, min(args.steps, 3))
+        warm = min(args.warmup, 1)
+        med, ts = time_reference(prog, n, inputs, steps, warm)
+        v = batch / med
+        line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": n, "steps": steps,
+                "warmup": warm, "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config,
+                "impl": "reference",
+                "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cpu_threads(), "kind": "port",
+                                 "sample": f"{steps} full steps of the workload through the oracle "
+                                           f"restatement of the reference evaluator ("
+                                           f"{'interpret' if n == 1 else 'spmd_interpret'}); numpy "
+                                           f"{np.__version__}, BLAS threads = host cores"},
+                "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    dist = init_dist(world, rank)
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.session import Session
+    inputs = synthetic_inputs(base, seed=0, scale=wl["scale"])
+    if n == 1:
+        sess = Session(base, local_rank=local)
+    else:
+        sess = Session(prog.local, prog.sharding, mode="nccl", rank=rank, world=world, local_rank=local)
+    sess.load(inputs)
+    dev = sess.device
+    # eager run once (validates), then capture the whole step as one CUDA graph
+    sess.run()
+    sess.sync()
+    sess.capture()
+    for _ in range(max(3, args.warmup)):
+        sess.step()
+    sess.sync()
+    launches_per_step = sess.launch_count()
+
+    e0, e1 = dev.event(), dev.event()
+    with ClockSampler([local] if world == 1 else list(range(world))) as clk:
+        barrier(dist)
+        sess.sync()
+        dev.record(e0)
+        for _ in range(args.steps):
+            sess.step()
+        dev.record(e1)
+        sess.sync()
+        barrier(dist)
+        # keep sampling clocks under the same load for a short while if the region was short
+        ms = dev.elapsed_ms(e0, e1)
+        extra = 0
+        while ms * (1 + extra) < 1500 and extra < 2000:
+            for _ in range(args.steps):
+                sess.step()
+            extra += 1
+        sess.sync()
+        barrier(dist)
+    ms_total = max_over_ranks(dist, ms)
+    ms_step = ms_total / args.steps
+    value = batch / (ms_step / 1e3)
+
+    # ---- end to end: batch H2D from pinned host memory + loss D2H, per step
+    f = sess.func
+    bx = sess.local_inputs(inputs)[0]
+    pin = {nm: dev.pinned(bx[nm].shape) for nm in ("x", "y") if nm in bx}
+    for nm, arr in pin.items():
+        arr[...] = bx[nm]
+    loss_pin = dev.pinned((1,))
+    loss_addr = sess.result_addr(0)
+    h2d = sum(a.nbytes for a in pin.values())
+    import ctypes
+    barrier(dist)
+    sess.sync()
+    t0 = time.perf_counter()
+    dev.record(e0)
+    for _ in range(args.steps):
+        for nm, arr in pin.items():
+            R.call(dev.lib.spx_memcpy_h2d, sess.arg_addr(nm), arr.ctypes.data, arr.nbytes, dev.stream)
+        sess.step()
+        R.call(dev.lib.spx_memcpy_d2h, loss_pin.ctypes.data, loss_addr, 4, dev.stream)
+        sess.sync()
+    dev.record(e1)
+    sess.sync()
+    wall = time.perf_counter() - t0
+    e2e_ms = max_over_ranks(dist, max(dev.elapsed_ms(e0, e1), wall * 1e3))
+    e2e_value = batch / (e2e_ms / args.steps / 1e3)
+    h2d_total = sum_over_ranks(dist, h2d)
+    d2h_total = sum_over_ranks(dist, 4)
+    loss = float(loss_pin[0])
+
+    # ---- per-record profile (eager, events between records) for the roofline
+    rec_ms = sess.ex.plan.profile()
+    recs = sess.ex.records()
+    gemm_flops = gemm_ms = 0.0
+    cls_ms = {}
+    for (kind, p), t in zip(recs, rec_ms):
+        name = {R.K_EW: "elementwise", R.K_REDUCE: "reduce", R.K_GEMM: "gemm", R.K_GATHER: "relayout",
+                R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl"}[kind]
+        cls_ms[name] = cls_ms.get(name, 0.0) + float(t)
+        if kind == R.K_GEMM:
+            gemm_flops += 2.0 * p.M * p.N * p.K * p.ndev
+            gemm_ms += float(t)
+    hbm, bf16, src = peaks()
+    tf32_peak = bf16 / 2.0
+    achieved = 3.0 * gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    roofline = {"bound": "tensor", "kernel": "tcgen05 3xTF32 GEMM (gemm_tc_kernel)",
+                "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+                "traffic": None,
+                "note": (f"achieved = tensor-core TF32 work (3 MMAs per fp32 FLOP: hi.hi + hi.lo + lo.hi) "
+                         f"/ GEMM time, summed over the {sum(1 for k, _ in recs if k == R.K_GEMM)} GEMM launches "
+                         f"of one step; peak = dense tf32 = 1/2 x {src} bf16 burst {bf16:.1f} TF/s "
+                         f"(B200 tf32:bf16 = 1.1:2.25). fp32-equivalent GEMM rate "
+                         f"{gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0:.1f} TFLOP/s"),
+                "step_ms_by_class": {k: round(v, 4) for k, v in sorted(cls_ms.items())},
+                "gemm_share_of_step": (gemm_ms / float(np.sum(rec_ms))) if np.sum(rec_ms) > 0 else None}
+    if args.profile_out and rank == 0:
+        with open(args.profile_out, "w") as fh:
+            json.dump({"records": [[int(k), float(t)] for (k, _), t in zip(recs, rec_ms)],
+                       "class_ms": cls_ms}, fh, indent=0)
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        med, ts = time_reference(prog, n, inputs, 2, 0)
+        cpu = {"value": batch / med, "unit": "samples/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"2 full steps (median {med:.2f} s) of the same workload through the oracle "
+                         f"restatement of the reference's dense interpreter (interp.py:117-132), numpy "
+                         f"{np.__version__}, BLAS on all host cores"}
+
+    counts = sess.ex.comp.counts
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+                "config": config, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_total),
+                        "d2h_bytes_per_step": int(d2h_total),
+                        "note": "Session.step with the batch (x, y) H2D from pinned memory and the "
+                                "loss D2H each step, host sync per step"},
+                "gpu_launches": int(launches_per_step * args.steps),
+                "launches_per_step": int(launches_per_step),
+                "clocks": clk.summary(), "loss": loss,
+                "collectives_per_step": counts,
+                "flops_per_device_step": sess.ex.comp.flops}
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,8 @@ int spx_free(uint64_t ptr);
 int spx_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream);
 int spx_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, uint64_t stream);
 int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream);
+int spx_host_alloc(uint64_t bytes, void** out_ptr); /* pinned host memory */
+int spx_host_free(void* ptr);
 int spx_stream_create(uint64_t* out_stream);
 int spx_stream_sync(uint64_t stream);
 int spx_stream_destroy(uint64_t stream);

@@ -202,6 +202,14 @@ int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream) {
   SPX_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(dst), value, bytes, reinterpret_cast<cudaStream_t>(stream)));
   return 0;
 }
+int spx_host_alloc(uint64_t bytes, void** out) {
+  SPX_CUDA(cudaHostAlloc(out, bytes ? bytes : 16, cudaHostAllocDefault));
+  return 0;
+}
+int spx_host_free(void* p) {
+  SPX_CUDA(cudaFreeHost(p));
+  return 0;
+}
 int spx_stream_create(uint64_t* out) {
   cudaStream_t s;
   SPX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

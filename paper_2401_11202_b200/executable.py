@@ -45,7 +45,7 @@ class Executable:
     DRY_TABLES = 1 << 44
 
     def __init__(self, module, func="main", device: R.Device | None = None, devices=None,
-                 comm_mode="local", comms=None, gemm_path=0, dry=False):
+                 comm_mode="local", comms=None, gemm_path=0, dry=False, comm_factory=None):
         """dry=True builds the records against fake addresses without a GPU
         (used by the CPU tests and the record simulator)."""
         self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode).compile()
@@ -56,6 +56,8 @@ class Executable:
         self.comms = comms or {}
         self._layout()
         self._alloc()
+        if comm_mode == "nccl" and comm_factory is not None:
+            self.comms = comm_factory(self)
         self._tables = []
         self._records = []
         self._emit()
@@ -150,6 +152,17 @@ class Executable:
         self.zero_off = hi
         self.zero_elems = _align(zero) if zero else 0
         hi += self.zero_elems
+        # NCCL mode: staging for collectives whose chunk order differs from the
+        # communicator's rank order (send/recv relayouts around the NCCL call)
+        stage = 0
+        if c.comm_mode == "nccl":
+            for k in ks:
+                if k.kind == "coll" and k.data["kind"] != "all_slice":
+                    stage = max(stage, _prod(k.data["in_dims"]), _prod(k.data["out_dims"]))
+        self.stage_elems = _align(stage)
+        self.stage_a = hi
+        self.stage_b = hi + self.stage_elems
+        hi += 2 * self.stage_elems
         self.off = off
         self.slice_elems = _align(hi, 1 << 18)           # 1 MiB granularity per device
         self.peak_bytes = hi * 4
@@ -394,8 +407,114 @@ class Executable:
         r.dst = self._tref(self._ptrs(out))
         self._records.append((R.K_CREDUCE, r))
 
+    # ---- NCCL collectives (one mesh device per process) ----
+    def comm_keys(self):
+        """(axes key, group) for every communicator this program needs, in a
+        deterministic order shared by all ranks."""
+        c = self.comp
+        keys = []
+        for k in c.kernels:
+            if k.kind != "coll" or k.data["kind"] == "all_slice":
+                continue
+            a = k.data["attrs"]
+            axes = a["axes"] if "axes" in a else [x for axs in a["axes_per_dim"] for x in axs]
+            key = tuple(sorted(set(axes), key=c.mesh.names().index))
+            if key not in keys:
+                keys.append(key)
+        return keys
+
+    def _nccl(self, kind, comm, send, recv, count, monoid=0):
+        p = R.NcclParams()
+        p.kind, p.comm, p.monoid = kind, comm, monoid
+        p.send, p.recv, p.count = send, recv, count
+        self._records.append((R.K_NCCL, p))
+
+    def _gather1(self, out_addr, dims, ext, cmul, sstride, table, base=0):
+        g = R.GatherParams()
+        g.ndev, g.rank, g.numel = 1, len(dims), _prod(dims)
+        for j, dd in enumerate(dims):
+            g.dims[j], g.ext[j], g.cmul[j], g.sstride[j] = dd, ext[j], cmul[j], sstride[j]
+        g.n_combo = len(table)
+        g.src_table = self._tref(np.array(table, dtype=np.uint64))
+        g.base_off = self._tref(np.array([base], dtype=np.int64))
+        g.dst = self._tref(np.array([out_addr], dtype=np.uint64))
+        self._records.append((R.K_GATHER, g))
+
     def _emit_coll_nccl(self, k):
-        raise NotImplementedError("nccl mode collectives: see nccl.py")
+        c = self.comp
+        d = k.data
+        kind, attrs = d["kind"], d["attrs"]
+        me = c.devices[0]
+        coords = c.coords
+        src, out = d["src"], k.outs[0]
+        in_dims, out_dims = list(d["in_dims"]), list(d["out_dims"])
+        S = _contig(in_dims)
+        src_a, out_a = self.addr(0, src), self.addr(0, out)
+        sa = self.base + self.stage_a * 4
+        sb = self.base + self.stage_b * 4
+        if kind == "all_slice":
+            apd = attrs["axes_per_dim"]
+            base = sum(c._chunk_index(coords[me], apd[j]) * out_dims[j] * S[j] for j in range(len(out_dims)))
+            self._gather1(out_a, out_dims, out_dims, [0] * len(out_dims), S, [src_a], base)
+            return
+        axes = attrs["axes"] if "axes" in attrs else [x for axs in attrs["axes_per_dim"] for x in axs]
+        key = tuple(sorted(set(axes), key=c.mesh.names().index))
+        grp = c._group_of(list(key))[me]
+        comm = self.comms[key]
+        n = len(grp)
+        monoid = 0 if attrs.get("monoid", "sum") == "sum" else 1
+        if kind == "all_reduce":
+            self._nccl(R.NCCL_ALLREDUCE, comm, src_a, out_a, _prod(in_dims), monoid)
+            return
+        if kind == "all_gather":
+            apd = attrs["axes_per_dim"]
+            nloc = _prod(in_dims)
+            nper = [out_dims[j] // in_dims[j] for j in range(len(out_dims))]
+            cm = _contig(nper)
+            combo_of = [sum(c._chunk_index(coords[m], apd[j]) * cm[j] for j in range(len(apd))) for m in grp]
+            direct = (all(not apd[j] for j in range(1, len(apd))) and combo_of == list(range(n))
+                      and _prod(nper) == n)
+            if direct:
+                self._nccl(R.NCCL_ALLGATHER, comm, src_a, out_a, nloc)
+                return
+            self._nccl(R.NCCL_ALLGATHER, comm, src_a, sa, nloc)
+            table = [self.base + self.zero_off * 4] * _prod(nper)
+            for j, cb in enumerate(combo_of):
+                table[cb] = sa + j * nloc * 4
+            self._gather1(out_a, out_dims, in_dims, cm, _contig(in_dims), table)
+            return
+        if kind == "reduce_scatter":
+            apd = attrs["axes_per_dim"]
+            nout = _prod(out_dims)
+            offs = [sum(c._chunk_index(coords[m], apd[j]) * out_dims[j] * S[j] for j in range(len(apd)))
+                    for m in grp]
+            if offs == [j * nout for j in range(n)]:
+                self._nccl(R.NCCL_REDUCESCATTER, comm, src_a, out_a, nout, monoid)
+                return
+            # relayout send buffer as [member j][chunk of member j]
+            self._gather1(sa, [n] + out_dims, [1] + out_dims, [1] + [0] * len(out_dims),
+                          [0] + list(S), [src_a + o * 4 for o in offs])
+            self._nccl(R.NCCL_REDUCESCATTER, comm, sa, out_a, nout, monoid)
+            return
+        if kind == "all_to_all":
+            gd, sd = attrs["gather_dim"], attrs["slice_dim"]
+            piece = list(in_dims)
+            piece[sd] = out_dims[sd]
+            npiece = _prod(piece)
+            chunk = [c._chunk_index(coords[m], list(attrs["axes"])) for m in grp]
+            self._gather1(sa, [n] + piece, [1] + piece, [1] + [0] * len(piece), [0] + list(S),
+                          [src_a + ch * out_dims[sd] * S[sd] * 4 for ch in chunk])
+            self._nccl(R.NCCL_ALLTOALL, comm, sa, sb, npiece)
+            ext = list(out_dims)
+            ext[gd] = in_dims[gd]
+            cmul = [0] * len(out_dims)
+            cmul[gd] = 1
+            table = [0] * n
+            for j, ch in enumerate(chunk):
+                table[ch] = sb + j * npiece * 4
+            self._gather1(out_a, out_dims, ext, cmul, _contig(piece), table)
+            return
+        raise AssertionError(kind)
 
     # --------------------------------------------------------------- host I/O
     def upload_args(self, per_device: list[dict]):

@@ -64,3 +64,30 @@ def load_program(name: str) -> Program:
         with open(os.path.join(d, "sharding.json")) as fh:
             sharding = json.load(fh)
     return Program(name, meta, dense, local, sharding)
+
+
+def synthetic_inputs(module, seed: int = 0, scale: float = 0.02, func: str = "main") -> dict:
+    """Deterministic N(0, scale^2) float32 inputs in signature order -- the
+    same generator and draw order as the reference's `random_inputs`
+    (interp.py:135-145), so a seed names the same arrays on every machine.
+    scale 0.02 keeps deep transformer steps finite."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    f = module.func(func)
+    return {n: (scale * rng.standard_normal(t.dims)).astype(np.float32) for n, t in f.args}
+
+
+# benchmark workloads: BASELINE.json configs -> program per GPU count
+WORKLOADS = {
+    "c1": {"desc": "mlp_train(hidden_layers=1, batch=256, width=1024), BP",
+           "scale": 0.25, "programs": {1: "c1_mlp_dense", 2: "c1_mlp_bp_B2"}},
+    "c2": {"desc": "mini_transformer_train(blocks=8, batch=2048, d_model=1024, d_ff=4096), BP+MP",
+           "scale": 0.02, "programs": {1: "c2_tf8_dense", 2: "c2_tf8_bp_B2", 4: "c2_tf8_bpmp_B2M2",
+                                       8: "c2_tf8_bpmp_B2M4"}},
+    "c3": {"desc": "mini_transformer_train(blocks=32, batch=8192, d_model=2048, d_ff=8192), BP+Z3",
+           "scale": 0.02, "programs": {1: "c3_tf32_dense", 2: "c3_tf32_bpz3_B2", 4: "c3_tf32_bpz3_B4",
+                                       8: "c3_tf32_bpz3_B8"}},
+    "c5": {"desc": "mini_transformer_train(blocks=8, batch=2048, d_model=1024, d_ff=4096), BP+MP+Z3+EMB",
+           "scale": 0.02, "programs": {1: "c2_tf8_dense", 2: "c5_tf8_bpz3_B2", 4: "c5_tf8_bpmpz3_B2M2",
+                                       8: "c5_tf8_bpmpz3emb_B2M2E2"}},
+}

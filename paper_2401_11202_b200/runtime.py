@@ -89,7 +89,7 @@ EXPORTS = [
     "spx_plan_create", "spx_plan_add", "spx_plan_finalize", "spx_plan_run", "spx_plan_capture",
     "spx_plan_replay", "spx_plan_launch_count", "spx_plan_destroy", "spx_plan_record_info",
     "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
-    "spx_plan_profile",
+    "spx_plan_profile", "spx_host_alloc", "spx_host_free",
 ]
 
 _lib = None
@@ -132,6 +132,7 @@ def load(build_if_missing: bool = True):
         "spx_nccl_get_unique_id": [C.c_void_p],
         "spx_comm_init": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)],
         "spx_comm_destroy": [C.c_int], "spx_device_init": [C.c_int], "spx_params_size": [C.c_int],
+        "spx_host_alloc": [C.c_uint64, C.POINTER(C.c_void_p)], "spx_host_free": [C.c_void_p],
     }
     for name, args in sigs.items():
         getattr(lib, name).argtypes = args
@@ -165,6 +166,7 @@ class Device:
         call(self.lib.spx_stream_create, C.byref(s))
         self.stream = s.value
         self._allocs = []
+        self._pinned = []
 
     def malloc(self, nbytes: int) -> int:
         p = C.c_uint64()
@@ -204,9 +206,22 @@ class Device:
         call(self.lib.spx_event_elapsed_ms, a, b, C.byref(out))
         return float(out.value)
 
+    def pinned(self, shape, dtype=np.float32) -> np.ndarray:
+        """Pinned (page-locked) host array for async H2D/D2H."""
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        call(self.lib.spx_host_alloc, max(nbytes, 16), C.byref(p))
+        buf = (C.c_uint8 * max(nbytes, 16)).from_address(p.value)
+        arr = np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
+        self._pinned.append(p.value)
+        return arr
+
     def close(self):
         for p in list(self._allocs):
             self.free(p)
+        for p in self._pinned:
+            self.lib.spx_host_free(C.c_void_p(p))
+        self._pinned = []
 
 
 class NativePlan:

@@ -1,0 +1,153 @@
+"""Resident sessions: compile once, keep inputs in HBM, step many times.
+
+`Session` is the API the benchmark and long-running users call (the drop-in
+`spmd_interpret` is one-shot: shard, upload, run, download, unshard).  Two
+hosting modes (see executable.py):
+
+  Session(module, sharding)                      all mesh devices on this GPU
+  Session(module, sharding, mode="nccl")         one mesh device per process;
+      rank/world/local_rank from torch.distributed (torchrun), NCCL
+      communicators per mesh-axis group created through ncclCommInitRank with
+      unique ids broadcast over torch.distributed (`make_nccl_comms`).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import runtime as R
+from .evaluator import _Dense, _chunk_slices, unshard
+from .executable import Executable
+
+
+def nccl_uid() -> bytes:
+    lib = R.load()
+    buf = (R.C.c_uint8 * 128)()
+    R.call(lib.spx_nccl_get_unique_id, R.C.cast(buf, R.C.c_void_p))
+    return bytes(buf)
+
+
+def nccl_comm_init(uid: bytes, nranks: int, rank: int) -> int:
+    lib = R.load()
+    buf = (R.C.c_uint8 * 128).from_buffer_copy(uid)
+    out = R.C.c_int()
+    R.call(lib.spx_comm_init, R.C.cast(buf, R.C.c_void_p), nranks, rank, R.C.byref(out))
+    return out.value
+
+
+def comm_plan(ex: Executable):
+    """[(axes key, groups)] in the shared deterministic order."""
+    c = ex.comp
+    return [(key, c._groups(list(key))) for key in ex.comm_keys()]
+
+
+def make_nccl_comms(ex: Executable, rank: int, broadcast, get_uid=nccl_uid, init=nccl_comm_init):
+    """One communicator per axes key; NCCL rank = position in the group's
+    device order (the reference's group order, spmd_interp.py:57-63).
+    `broadcast(obj) -> obj` shares rank 0's unique ids with every rank."""
+    plan = comm_plan(ex)
+    uids = None
+    if rank == 0:
+        uids = {(key, gi): get_uid() for key, groups in plan for gi in range(len(groups))}
+    uids = broadcast(uids)
+    comms = {}
+    for key, groups in plan:
+        gi = next(i for i, g in enumerate(groups) if rank in g)
+        grp = groups[gi]
+        comms[key] = init(uids[(key, gi)], len(grp), grp.index(rank))
+    return comms
+
+
+def torch_broadcast(obj):
+    import torch.distributed as dist
+    box = [obj]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
+class Session:
+    def __init__(self, module, sharding=None, *, mode="local", device: R.Device | None = None,
+                 rank: int = 0, world: int = 1, local_rank: int = 0, gemm_path: int = 0,
+                 func: str = "main", broadcast=torch_broadcast):
+        self.module = module
+        self.sharding = sharding
+        self.mode = mode
+        self.func = module.func(func)
+        if sharding is None or module.mesh is None:
+            target = _Dense(module) if module.mesh is not None else module
+            self.mesh = None
+            self.coords = [{}]
+            self.device = device or R.Device(local_rank)
+            self.ex = Executable(target, func, device=self.device, devices=[0], gemm_path=gemm_path)
+            self.hosted = [0]
+        elif mode == "local":
+            self.mesh = module.mesh
+            self.coords = self.mesh.coords()
+            self.device = device or R.Device(local_rank)
+            self.ex = Executable(module, func, device=self.device, gemm_path=gemm_path)
+            self.hosted = list(range(len(self.coords)))
+        else:
+            self.mesh = module.mesh
+            self.coords = self.mesh.coords()
+            if self.mesh.device_count != world:
+                raise ValueError(f"mesh has {self.mesh.device_count} devices, world size is {world}")
+            self.device = device or R.Device(local_rank)
+            self.ex = Executable(module, func, device=self.device, devices=[rank], comm_mode="nccl",
+                                 gemm_path=gemm_path,
+                                 comm_factory=lambda ex: make_nccl_comms(ex, rank, broadcast))
+            self.hosted = [rank]
+        self.rank = rank
+
+    # -- inputs -----------------------------------------------------------
+    def local_inputs(self, global_inputs: dict) -> list[dict]:
+        f = self.func
+        out = []
+        for d in self.hosted:
+            env = {}
+            for n, t in f.args:
+                a = np.asarray(global_inputs[n], dtype=np.float32)
+                if self.mesh is not None:
+                    a = a[_chunk_slices(a.shape, self.sharding.args[n], self.mesh, self.coords[d])]
+                if tuple(a.shape) != tuple(t.dims):
+                    raise ValueError(f"arg %{n}: sharded input is {a.shape}, local signature wants {t.dims}")
+                env[n] = a
+            out.append(env)
+        return out
+
+    def load(self, global_inputs: dict):
+        self.ex.upload_args(self.local_inputs(global_inputs))
+        self.device.sync()
+
+    def arg_addr(self, name: str, p: int = 0) -> int:
+        return self.ex.addr(p, name)
+
+    # -- execution --------------------------------------------------------
+    def run(self):
+        self.ex.plan.run()
+
+    def capture(self):
+        self.ex.plan.capture()
+
+    def step(self):
+        self.ex.plan.replay()
+
+    def sync(self):
+        self.device.sync()
+
+    def launch_count(self) -> int:
+        return self.ex.plan.launch_count()
+
+    def results(self):
+        return self.ex.download_results()
+
+    def result_addr(self, j: int, p: int = 0) -> int:
+        return self.ex.addr(p, self.ex.comp.result_bufs[j])
+
+    def global_results(self, tol=1e-5):
+        res = self.results()
+        if self.mesh is None:
+            return [r[0] for r in res]
+        return [unshard(res[j], self.sharding.results[j], self.mesh, self.coords, tol, f"result {j}")
+                for j in range(len(res))]
+
+    def close(self):
+        self.ex.close()
