@@ -59,11 +59,13 @@ enum spx_opcode {
   SPX_OP_IMUL = 10  /* t = imm[i] * a          */
 };
 
-/* operand encoding: 0..SPX_MAX_IN-1 = input view j; 32+i = result of insn i */
-#define SPX_REG_T 32
+/* Register machine: SPX_NREG value slots; input view j is preloaded into slot
+ * j, instruction i computes op(slot a, slot b [, imm[i]]) into slot dst.  The
+ * host allocates slots by liveness (paper_2401_11202_b200/plan.py). */
+#define SPX_NREG 12
 
 typedef struct {
-  int32_t op, a, b, pad; /* b also indexes imm[] for *I / IMM forms */
+  int32_t op, a, b, dst;
 } spx_insn;
 
 typedef struct {
@@ -79,7 +81,7 @@ typedef struct {
   int64_t numel;
   spx_view in[SPX_MAX_IN];
   int64_t out_off[SPX_MAX_OUT];   /* outputs are contiguous row-major          */
-  int32_t out_reg[SPX_MAX_OUT];   /* which register each output stores         */
+  int32_t out_reg[SPX_MAX_OUT];   /* which slot each output stores            */
   spx_insn prog[SPX_MAX_PROG];
   float imm[SPX_MAX_PROG];
 } spx_ew_params;
@@ -89,7 +91,9 @@ typedef struct {
   spx_ew_params x;                /* the reduced operand as an expression over
                                      the INPUT shape (out_reg[0] = value)      */
   int32_t monoid;                 /* 0 sum, 1 max                              */
-  int32_t n_kept, n_red, pad;
+  int32_t n_kept, n_red;          /* x.dims = kept (n_kept dims) ++ reduced      */
+  int32_t mode;                   /* 0 ROW / 1 COL (2-D, x.vec = float4 along the
+                                     fast dim), 2 GEN (any rank)               */
   int64_t kept_dims[SPX_MAX_RANK], kept_stride[SPX_MAX_RANK]; /* in input index space */
   int64_t red_dims[SPX_MAX_RANK], red_stride[SPX_MAX_RANK];
   int64_t n_out, n_red_elems;

@@ -237,8 +237,8 @@ class Executable:
             p.out_off[o] = self.off[name]
             p.out_reg[o] = prog.out_regs[names.index(name)]
         p.n_prog = len(prog.insns)
-        for i, (op, a, b, imm) in enumerate(prog.insns):
-            p.prog[i].op, p.prog[i].a, p.prog[i].b = op, a, b
+        for i, (op, a, b, dst, imm) in enumerate(prog.insns):
+            p.prog[i].op, p.prog[i].a, p.prog[i].b, p.prog[i].dst = op, a, b, dst
             p.imm[i] = imm
         p.vec = vec
         return p
@@ -263,41 +263,60 @@ class Executable:
         in_dims = list(k.data["in_dims"]) or [1]
         red = sorted(k.data["red"])
         kept = [d for d in range(len(in_dims)) if d not in red]
-        perm = kept + red
         root = k.data["root"]
         prog = Program.build({k.outs[0]: root})
+        views = []
+        for l in prog.leaves:
+            st = list(l.strides) if len(l.strides) == len(in_dims) else [0] * len(in_dims)
+            views.append(st)
+        cst = list(_contig(in_dims))
+        # collapse kept dims and reduced dims separately (views + the logical layout)
+        kd, kv = _collapse([in_dims[d] for d in kept], [[v[d] for d in kept] for v in views + [cst]]) \
+            if kept else ([], [[] for _ in views + [cst]])
+        rd, rv = _collapse([in_dims[d] for d in red], [[v[d] for d in red] for v in views + [cst]])
         p = R.ReduceParams()
         x = p.x
         x.base, x.dev_stride, x.ndev = self.base, self.dev_stride, self.ndev
-        x.rank = len(perm)
-        for i, d in enumerate(perm):
-            x.dims[i] = in_dims[d]
+        dims = list(kd) + list(rd)
+        x.rank = len(dims)
+        for i, dd in enumerate(dims):
+            x.dims[i] = dd
         x.numel = _prod(in_dims)
         x.n_in = len(prog.leaves)
         for j, l in enumerate(prog.leaves):
             x.inp[j].off = self.off[l.buf] + l.off
-            st = list(l.strides) if len(l.strides) == len(in_dims) else [0] * len(in_dims)
-            for i, d in enumerate(perm):
-                x.inp[j].stride[i] = st[d]
+            for i, st in enumerate(list(kv[j]) + list(rv[j])):
+                x.inp[j].stride[i] = st
         x.n_out = 1
         x.out_reg[0] = prog.out_regs[0]
         x.n_prog = len(prog.insns)
-        for i, (op, a, b, imm) in enumerate(prog.insns):
-            x.prog[i].op, x.prog[i].a, x.prog[i].b = op, a, b
+        for i, (op, a, b, dst, imm) in enumerate(prog.insns):
+            x.prog[i].op, x.prog[i].a, x.prog[i].b, x.prog[i].dst = op, a, b, dst
             x.imm[i] = imm
         p.monoid = 0 if k.data["monoid"] == "sum" else 1
-        p.n_kept, p.n_red = len(kept), len(red)
-        cst = _contig(in_dims)
-        for i, d in enumerate(kept):
-            p.kept_dims[i] = in_dims[d]
-            p.kept_stride[i] = cst[d]
-        for i, d in enumerate(red):
-            p.red_dims[i] = in_dims[d]
-            p.red_stride[i] = cst[d]
+        p.n_kept, p.n_red = len(kd), len(rd)
         p.n_out = _prod(in_dims[d] for d in kept)
         p.n_red_elems = _prod(in_dims[d] for d in red)
         p.out_off = self.off[k.outs[0]]
         p.scratch_off = self.scratch_off
+        # thread mapping: innermost logical dim reduced -> ROW, kept -> COL
+        two_d = len(kd) <= 1 and len(rd) == 1
+        innermost_kept = bool(kept) and kept[-1] == len(in_dims) - 1
+        if not two_d:
+            p.mode = 2
+            x.vec = 0
+        elif innermost_kept:
+            p.mode = 1
+            so = [kv[j][0] if kd else 0 for j in range(len(prog.leaves))]
+            x.vec = int(p.n_out % 4 == 0 and all(s_ in (0, 1) for s_ in so) and
+                        all((x.inp[j].off % 4 == 0) and (rv[j][0] % 4 == 0) for j in range(len(prog.leaves))
+                            if so[j] == 1))
+        else:
+            p.mode = 0
+            sr = [rv[j][0] for j in range(len(prog.leaves))]
+            x.vec = int(p.n_red_elems % 4 == 0 and all(s_ in (0, 1) for s_ in sr) and
+                        all((x.inp[j].off % 4 == 0) and (not kd or kv[j][0] % 4 == 0)
+                            for j in range(len(prog.leaves)) if sr[j] == 1))
         self._records.append((R.K_REDUCE, p))
 
     def _emit_gemm(self, k):

@@ -485,55 +485,90 @@ def _fits(exprs) -> bool:
 
 
 class Program:
-    """Expression DAG -> SSA bytecode (spx_insn)."""
+    """Expression DAG -> register-machine bytecode (spx_insn).
+
+    Leaves (input views) are preloaded into slots 0..n_in-1; every operation
+    writes a slot chosen by a liveness-based allocator over SPX_NREG slots, so
+    long chains run in a fixed small register file (interp.cuh)."""
 
     def __init__(self):
         self.leaves: list[Leaf] = []
-        self.insns: list[tuple] = []   # (op, a, b, imm)
+        self.insns: list[tuple] = []   # (op, a_slot, b_slot, dst_slot, imm)
         self.out_regs: list[int] = []
 
     @staticmethod
     def build(exprs) -> "Program":
         p = Program()
         memo = {}
+        ssa = []          # (op, a, b, imm) with a/b = ("in", j) | ("t", i)
 
-        def leaf_reg(l):
+        def leaf(l):
             if l not in p.leaves:
                 p.leaves.append(l)
-            return p.leaves.index(l)
+            return ("in", p.leaves.index(l))
 
-        def emit(op, a=0, b=0, imm=0.0):
-            p.insns.append((op, a, b, float(imm)))
-            return R.REG_T + len(p.insns) - 1
+        def emit(op, a=None, b=None, imm=0.0):
+            ssa.append((op, a, b, float(imm)))
+            return ("t", len(ssa) - 1)
 
-        def reg(x):
+        def val(x):
             if isinstance(x, Leaf):
-                return leaf_reg(x)
-            if isinstance(x, np.float32) or isinstance(x, float):
-                return emit(R.OP["IMM"], 0, 0, x)
+                return leaf(x)
+            if isinstance(x, (np.float32, float)):
+                return emit(R.OP["IMM"], None, None, x)
             if x.uid in memo:
                 return memo[x.uid]
             if x.op in ("add", "mul"):
                 a, b = x.kids
                 ca, cb = isinstance(a, (np.float32, float)), isinstance(b, (np.float32, float))
                 if cb and not ca:
-                    r = emit(R.OP["ADDI" if x.op == "add" else "MULI"], reg(a), 0, b)
+                    r = emit(R.OP["ADDI" if x.op == "add" else "MULI"], val(a), None, b)
                 elif ca and not cb:
-                    r = emit(R.OP["IADD" if x.op == "add" else "IMUL"], reg(b), 0, a)
+                    r = emit(R.OP["IADD" if x.op == "add" else "IMUL"], val(b), None, a)
                 else:
-                    ra, rb = reg(a), reg(b)
-                    r = emit(R.OP["ADD" if x.op == "add" else "MUL"], ra, rb)
+                    va, vb = val(a), val(b)
+                    r = emit(R.OP["ADD" if x.op == "add" else "MUL"], va, vb)
             elif x.op == "neg":
-                r = emit(R.OP["NEG"], reg(x.kids[0]))
+                r = emit(R.OP["NEG"], val(x.kids[0]))
             elif x.op == "exp":
-                r = emit(R.OP["EXP"], reg(x.kids[0]))
+                r = emit(R.OP["EXP"], val(x.kids[0]))
             else:
                 raise ValueError(x.op)
             memo[x.uid] = r
             return r
 
-        for e in exprs.values() if isinstance(exprs, dict) else exprs:
-            p.out_regs.append(reg(e))
-        if len(p.insns) > R.MAX_PROG or len(p.leaves) > R.MAX_IN:
+        outs = [val(e) for e in (exprs.values() if isinstance(exprs, dict) else exprs)]
+        n_in = len(p.leaves)
+        if n_in > R.MAX_IN or len(ssa) > R.MAX_PROG:
             raise ValueError("expression too large")
+        # liveness: last instruction index reading each value; outputs live to the end
+        last = {}
+        for i, (op, a, b, _) in enumerate(ssa):
+            for v in (a, b):
+                if v is not None:
+                    last[v] = i
+        for v in outs:
+            last[v] = len(ssa)
+        slot = {("in", j): j for j in range(n_in)}
+        free = [k for k in range(n_in, R.NREG)]
+        for j in range(n_in):                      # inputs dead from the start
+            if ("in", j) not in last:
+                free.append(j)
+        for i, (op, a, b, imm) in enumerate(ssa):
+            for v in (a, b):                       # operands whose last use is here
+                if v is not None and last.get(v) == i and slot[v] not in free:
+                    free.append(slot[v])
+            if ("t", i) not in last:               # dead result (cannot happen for roots)
+                last[("t", i)] = i
+            if not free:
+                raise ValueError("expression needs more than SPX_NREG live values")
+            free.sort()
+            d = free.pop(0)
+            slot[("t", i)] = d
+            if last[("t", i)] == i:
+                free.append(d)
+            sa = slot[a] if a is not None else 0
+            sb = slot[b] if b is not None else 0
+            p.insns.append((op, sa, sb, d, imm))
+        p.out_regs = [slot[v] for v in outs]
         return p

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libspindle_b200.so")
 
 MAX_RANK, MAX_IN, MAX_OUT, MAX_PROG = 6, 8, 4, 28
-REG_T = 32
+NREG = 12
 
 OP = dict(MOV=0, ADD=1, MUL=2, NEG=3, EXP=4, MAX=5, IMM=6, ADDI=7, MULI=8, IADD=9, IMUL=10)
 K_EW, K_REDUCE, K_GEMM, K_GATHER, K_CREDUCE, K_NCCL = 1, 2, 3, 4, 5, 6
@@ -25,7 +25,7 @@ I64R = C.c_int64 * MAX_RANK
 
 
 class Insn(C.Structure):
-    _fields_ = [("op", C.c_int32), ("a", C.c_int32), ("b", C.c_int32), ("pad", C.c_int32)]
+    _fields_ = [("op", C.c_int32), ("a", C.c_int32), ("b", C.c_int32), ("dst", C.c_int32)]
 
 
 class View(C.Structure):
@@ -44,7 +44,7 @@ class EwParams(C.Structure):
 
 class ReduceParams(C.Structure):
     _fields_ = [("x", EwParams), ("monoid", C.c_int32), ("n_kept", C.c_int32),
-                ("n_red", C.c_int32), ("pad", C.c_int32),
+                ("n_red", C.c_int32), ("mode", C.c_int32),
                 ("kept_dims", I64R), ("kept_stride", I64R),
                 ("red_dims", I64R), ("red_stride", I64R),
                 ("n_out", C.c_int64), ("n_red_elems", C.c_int64),

@@ -44,7 +44,6 @@ class Sim:
         regs = {}
         for j, a in enumerate(ins):
             regs[j] = a
-        shape = ins[0].shape if ins else None
         with np.errstate(all="ignore"):
             for i in range(x.n_prog):
                 ins_ = x.prog[i]
@@ -75,7 +74,8 @@ class Sim:
                     v = np.multiply(imm, A)
                 else:
                     raise AssertionError(op)
-                regs[R.REG_T + i] = np.asarray(v, dtype=np.float32)
+                assert 0 <= ins_.dst < R.NREG
+                regs[ins_.dst] = np.asarray(v, dtype=np.float32)
         return regs
 
     def run_ew(self, x: R.EwParams):
@@ -210,3 +210,71 @@ def sim_dense(module, inputs):
     sim.upload([{n: np.asarray(inputs[n]) for n in f.arg_names()}])
     sim.run()
     return [r[0] for r in sim.results()], ex
+
+
+def sim_nccl(module, spec, inputs, tol=1e-5):
+    """The one-process-per-GPU (NCCL) lowering, simulated: one dry Executable
+    per rank, records executed in lockstep, NCCL records combined across the
+    ranks of each communicator group (rank order = group order)."""
+    from paper_2401_11202_b200.evaluator import _chunk_slices, unshard
+    from paper_2401_11202_b200.executable import Executable
+    from paper_2401_11202_b200.session import comm_plan
+    f = module.func("main")
+    mesh = module.mesh
+    coords = mesh.coords()
+    world = len(coords)
+    exs, sims = [], []
+    probe = Executable(module, devices=[0], comm_mode="nccl", dry=True,
+                       comm_factory=lambda ex: {k: i for i, k in enumerate(ex.comm_keys())})
+    plan = comm_plan(probe)
+    for r in range(world):
+        ex = Executable(module, devices=[r], comm_mode="nccl", dry=True,
+                        comm_factory=lambda ex: {k: i for i, k in enumerate(ex.comm_keys())})
+        exs.append(ex)
+        s = Sim(ex)
+        a = {n: np.asarray(inputs[n])[_chunk_slices(np.shape(inputs[n]), spec.args[n], mesh, coords[r])]
+             for n in f.arg_names()}
+        s.upload([a])
+        sims.append(s)
+    nrec = len(exs[0].records())
+    assert all(len(e.records()) == nrec for e in exs)
+    for i in range(nrec):
+        kind = exs[0].records()[i][0]
+        if kind != R.K_NCCL:
+            for s, e in zip(sims, exs):
+                k, p = e.records()[i]
+                {R.K_EW: s.run_ew, R.K_REDUCE: s.run_reduce, R.K_GEMM: s.run_gemm,
+                 R.K_GATHER: s.run_gather, R.K_CREDUCE: s.run_creduce}[k](p)
+            continue
+        p0 = exs[0].records()[i][1]
+        key, groups = plan[p0.comm]
+        for grp in groups:
+            ps = [exs[r].records()[i][1] for r in grp]
+            cnt = ps[0].count
+            sends = [sims[r].arena[sims[r].idx(p.send):sims[r].idx(p.send) + (cnt * len(grp)
+                     if p.kind in (R.NCCL_REDUCESCATTER, R.NCCL_ALLTOALL) else cnt)].copy()
+                     for r, p in zip(grp, ps)]
+            outs = []
+            if p0.kind == R.NCCL_ALLREDUCE:
+                acc = sends[0]
+                for x in sends[1:]:
+                    acc = np.add(acc, x) if p0.monoid == 0 else np.maximum(acc, x)
+                outs = [acc] * len(grp)
+            elif p0.kind == R.NCCL_ALLGATHER:
+                outs = [np.concatenate(sends)] * len(grp)
+            elif p0.kind == R.NCCL_REDUCESCATTER:
+                acc = sends[0]
+                for x in sends[1:]:
+                    acc = np.add(acc, x) if p0.monoid == 0 else np.maximum(acc, x)
+                outs = [acc[j * cnt:(j + 1) * cnt] for j in range(len(grp))]
+            else:  # all-to-all: rank j receives piece j of every sender, in sender order
+                outs = [np.concatenate([sends[s][j * cnt:(j + 1) * cnt] for s in range(len(grp))])
+                        for j in range(len(grp))]
+            for r, p, o in zip(grp, ps, outs):
+                d0 = sims[r].idx(p.recv)
+                sims[r].arena[d0:d0 + o.size] = o
+    res = [s.results() for s in sims]           # [rank][result][device0]
+    out = []
+    for j in range(len(f.results)):
+        out.append(unshard([res[r][j][0] for r in range(world)], spec.results[j], mesh, coords, tol, f"result {j}"))
+    return out, exs
