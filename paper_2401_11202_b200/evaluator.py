@@ -21,11 +21,19 @@ from .executable import Executable
 from .plan import UnsupportedProgram
 
 
-class DivergenceError(Exception):
+try:  # when the reference package is importable, our errors ARE its errors too
+    from spindle.spmd_interp import DivergenceError as _RefDivergence  # type: ignore
+    from spindle.interp import EvalError as _RefEvalError  # type: ignore
+except Exception:  # pragma: no cover - the GPU box has no reference
+    _RefDivergence = Exception
+    _RefEvalError = Exception
+
+
+class DivergenceError(_RefDivergence):
     """Device replicas disagree on a value that must be replicated (spmd_interp.py:21-22)."""
 
 
-class EvalError(Exception):
+class EvalError(_RefEvalError):
     """interp.py:16-17"""
 
 
