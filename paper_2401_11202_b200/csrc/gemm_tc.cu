@@ -1,24 +1,33 @@
 // tcgen05 / TMEM / TMA GEMM for the reference's fp32 `matmul`
 // (interp.py:43-44: numpy `@` on float32 arrays -> sgemm).
 //
-// fp32 parity (<= 1e-5 max-normalised error, SPMD spec SPEC.md:92) on tensor
-// cores uses the 3xTF32 split: x = hi + lo with hi = x truncated to the tf32
-// grid (exact) and lo = x - hi (exact in fp32), and
-//     A.B ~= hi(A).hi(B) + hi(A).lo(B) + lo(A).hi(B)
-// accumulated in fp32 in TMEM; the dropped lo.lo term is ~2^-22 relative.
+// fp32 parity (<= 1e-5 max-normalised error) on tensor cores uses
+// the 3xTF32 split: x = hi + lo, hi = x truncated to the tf32 grid, lo = x - hi
+// (exact in fp32), and  A.B ~= hi(A).hi(B) + hi(A).lo(B) + lo(A).hi(B).
+// Measured on B200 (tools/tf32_conversion.py): kind::tf32 ignores the low 13
+// mantissa bits of an fp32 operand, i.e. it truncates -- so the raw TMA tile
+// already IS hi(x) and the split only writes lo(x).
 //
-// Structure (one 128 x BN output tile per CTA, 1 CTA per SM):
-//   warp 0      TMA producer: A and B k-slabs (32 fp32 = one 128B swizzle row)
-//               into a STAGES-deep ring; transposed operands are loaded as
-//               MN-major tiles, so `transpose` feeding a matmul never
-//               materialises (interp.py:51-52 folded into the descriptor)
-//   warps 2..5  split: hi in place, lo into a twin buffer (same swizzled
-//               layout -- the split is elementwise), fence.proxy.async, arrive
-//   warp 1      MMA issuer (one thread): 4 k-steps x 3 terms of
-//               tcgen05.mma.cta_group::1.kind::tf32 M=128 N=BN K=8 into TMEM,
-//               tcgen05.commit frees the smem stage
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
-// The batch dimension of the TMA tensor maps walks co-located mesh devices.
+// Tensor-core accumulation is not IEEE round-to-nearest: measured error grows
+// linearly with K (3e-5 at K=4096).  Each CTA therefore accumulates `promote`
+// k-blocks per TMEM chunk and folds finished chunks into fp32 registers
+// (__fadd_rn) while the tensor core fills the other chunk buffer; hi.hi and the
+// two correction terms go to separate accumulators (independent MMA chains --
+// one accumulator serialised the MMAs).  Error 7e-7..8e-7 at any K.
+//
+// Persistent kernel, one CTA per SM, 128 x 128 output tiles.  (A CTA-pair
+// variant with tcgen05.mma.cta_group::2 M=256 was measured slower on these
+// shapes -- the cross-CTA split/drain handshakes sat on the critical path --
+// and was dropped.)  Warp roles (10 warps):
+//   warp 0      TMA producer into a RSTAGES-deep raw ring (k-slab of 32 fp32)
+//   warp 1      TMEM alloc; MMA issuer: per k-step of 8
+//               hi.lo (A collector fill), hi.hi (collector reuse), lo.hi
+//   warps 2..5  split: lo = x - trunc_tf32(x) into a LSTAGES-deep lo ring
+//   warps 6..9  drain: TMEM -> registers fp32 promotion, epilogue stores
+// Transposed operands (a `transpose` feeding the matmul) are loaded MN-major
+// (SWIZZLE_128B_BASE32B, the only MN-major layout tf32 accepts), so the
+// transpose never materialises (interp.py:51-52 folded into the descriptor).
+// The third dimension of the TMA tensor maps walks co-located mesh devices.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdlib>
@@ -27,10 +36,10 @@
 
 namespace {
 
-constexpr int BM = 128;
+constexpr int BM = 128;             // rows per CTA
+constexpr int BN = 128;             // output columns per CTA (= per pair)
 constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
-constexpr int STAGES = 3;
-constexpr int NTHREADS = 320;   // TMA, MMA, 4 split warps, 4 drain warps
+constexpr int NTHREADS = 320;
 
 SPX_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -41,27 +50,48 @@ SPX_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Arrive on the barrier at the same offset in CTA `rank` of the cluster.
+SPX_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
 SPX_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Bounded wait: a protocol bug traps (error surfaces to the host) instead of
-// hanging the GPU.
+// Bounded wait: a protocol bug traps (the error surfaces to the host) instead
+// of hanging the GPU.  CLUSTER = acquire at cluster scope (peer arrivals).
+template <bool CLUSTER = false>
 SPX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;
   long long t0 = 0;
   for (int it = 0;; ++it) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
+    if (CLUSTER) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(a), "r"(parity)
+          : "memory");
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(a), "r"(parity)
+          : "memory");
+    }
     if (done) return;
     if (it == 64) t0 = clock64();
     if (it > 64 && (it & 1023) == 0 && clock64() - t0 > 20000000000LL) __trap();
   }
+}
+
+SPX_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 SPX_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
@@ -74,40 +104,46 @@ SPX_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c
 
 // UMMA shared-memory descriptor (sm_100 version 1).  Layout type 2 =
 // SWIZZLE_128B (16B atoms; K-major operands), 1 = SWIZZLE_128B_BASE32B (32B
-// atoms; the only MN-major layout tf32 operands support).
+// atoms; MN-major tf32 operands).
 SPX_DEV uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 
+// collector: 0 none, 1 fill A, 2 last use of A
+template <int CG, int COLLECT>
 SPX_DEV void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+#define SPX_MMA(GRP, SUFFIX)                                                                   \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                               \
+               "tcgen05.mma.cta_group::" GRP ".kind::tf32" SUFFIX " [%0], %1, %2, %3, p;\n\t}" \
+               ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc))
+  if (CG == 1) {
+    if (COLLECT == 1) SPX_MMA("1", ".collector::a::fill");
+    else if (COLLECT == 2) SPX_MMA("1", ".collector::a::lastuse");
+    else SPX_MMA("1", "");
+  } else {
+    if (COLLECT == 1) SPX_MMA("2", ".collector::a::fill");
+    else if (COLLECT == 2) SPX_MMA("2", ".collector::a::lastuse");
+    else SPX_MMA("2", "");
+  }
+#undef SPX_MMA
 }
+
+// MMA completion -> barrier (CG=2: the barrier at the same offset in both CTAs).
+template <int CG>
 SPX_DEV void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+  if (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  }
 }
-
-struct TcArgs {
-  int M, N, K, a_mn_major, b_k_major, promote;  // promote: k-blocks per TMEM chunk
-  uint64_t c_base;     // device 0 address of C
-  int64_t dev_stride;  // bytes
-  int64_t ldc;
-};
-
-template <int BN>
-struct Smem {
-  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
-};
 
 SPX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -122,42 +158,75 @@ SPX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
 }
 
-// Tensor-core accumulation is not IEEE fp32 round-to-nearest: measured on
-// B200 its error grows linearly with K (3e-5 at K=4096).  The kernel
-// therefore accumulates `promote` k-blocks at a time in one of two TMEM
-// accumulators and folds each finished chunk into fp32 registers
-// (__fadd_rn) held by the drain warps, while the tensor core fills the other
-// accumulator -- error stays ~1e-6 independent of K.
-template <int BN>
+struct TcArgs {
+  int M, N, K, a_mn_major, b_k_major, promote;   // promote: k-blocks per TMEM chunk
+  int tiles_m, tiles_n, tiles;                   // persistent tile space (x ndev)
+  uint64_t c_base;     // device 0 address of C
+  int64_t dev_stride;  // bytes
+  int64_t ldc;
+};
+
+template <int RS_, int LS_>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;       // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;       // 16 KB
+  static constexpr int RAW = A_BYTES + B_BYTES;     // one TMA stage (= the hi operands)
+  // Raw ring (TMA destination) and lo ring (split output) are separate so the
+  // producer runs RSTAGES k-blocks ahead of the tensor core.
+  static constexpr int RSTAGES = RS_;
+  static constexpr int LSTAGES = LS_;
+  static constexpr int LO_OFF = RSTAGES * RAW;
+  static constexpr int BAR_OFF = LO_OFF + LSTAGES * RAW;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // barriers + alignment slack
+};
+
+SPX_DEV void tile_coords(const TcArgs& a, int t, int& m0, int& n0, int& dev) {
+  const int per_dev = a.tiles_m * a.tiles_n;
+  dev = t / per_dev;
+  const int r = t - dev * per_dev;
+  const int n_blk = r / a.tiles_m;            // M fastest: concurrent CTAs share B panels
+  m0 = (r - n_blk * a.tiles_m) * BM;
+  n0 = n_blk * BN;
+}
+
+// Persistent: one CTA per SM walks tiles t = blockIdx.x, += gridDim.x.  The
+// k-block stream and the TMEM chunk stream run continuously across tiles, so
+// there is no per-tile pipeline fill, TMEM allocation or barrier set-up, and
+// a tile's epilogue stores overlap the next tile's main loop.
+template <int RS_, int LS_>
 __global__ void __launch_bounds__(NTHREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ TcArgs args) {
-  using S = Smem<BN>;
+  using S = Cfg<RS_, LS_>;
+  constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-  uint64_t* split = full + STAGES;
-  uint64_t* empty = split + STAGES;
-  uint64_t* tfull = empty + STAGES;     // [2] chunk accumulated (MMA commit)
-  uint64_t* tempty = tfull + 2;         // [2] chunk drained (128 drain threads)
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* lo_full = raw_empty + RS;   // split done
+  uint64_t* lo_empty = lo_full + LS;
+  uint64_t* tfull = lo_empty + LS;      // [2] chunk accumulated (MMA commit)
+  uint64_t* tempty = tfull + 2;         // [2] chunk drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, dev = blockIdx.z;
   const int nk = (args.K + BK - 1) / BK;
   const int P = args.promote;
   const int nchunks = (nk + P - 1) / P;
 
-  auto a_hi = [&](int s) { return smem + s * S::STAGE; };
-  auto a_lo = [&](int s) { return smem + s * S::STAGE + S::A_BYTES; };
-  auto b_hi = [&](int s) { return smem + s * S::STAGE + 2 * S::A_BYTES; };
-  auto b_lo = [&](int s) { return smem + s * S::STAGE + 2 * S::A_BYTES + S::B_BYTES; };
+  auto a_hi = [&](int s) { return smem + s * S::RAW; };
+  auto b_hi = [&](int s) { return smem + s * S::RAW + S::A_BYTES; };
+  auto a_lo = [&](int s) { return smem + S::LO_OFF + s * S::RAW; };
+  auto b_lo = [&](int s) { return smem + S::LO_OFF + s * S::RAW + S::A_BYTES; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&split[s], 128);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 1);
+    }
+    for (int s = 0; s < LS; ++s) {
+      mbar_init(&lo_full[s], 128);
+      mbar_init(&lo_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -168,8 +237,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -180,24 +248,30 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(S::A_BYTES + S::B_BYTES);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t round = kb / STAGES;
-        mbar_wait(&empty[s], (round & 1) ^ 1);
-        mbar_expect_tx(&full[s], bytes);
-        const int k0 = kb * BK;
-        if (args.a_mn_major) {
+      const uint32_t bytes = (uint32_t)S::RAW;
+      int g = 0;                                  // global k-block counter
+      for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+        int m0, n0, dev;
+        tile_coords(args, t, m0, n0, dev);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % RS;
+          mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
+          mbar_expect_tx(&raw_full[s], bytes);
+          const int k0 = kb * BK;
+          if (args.a_mn_major) {
 #pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_3d(a_hi(s) + c * 4096, &tma_a, &full[s], m0 + 32 * c, k0, dev);
-        } else {
-          tma_load_3d(a_hi(s), &tma_a, &full[s], k0, m0, dev);
-        }
-        if (args.b_k_major) {
-          tma_load_3d(b_hi(s), &tma_b, &full[s], k0, n0, dev);
-        } else {
+            for (int c = 0; c < BM / 32; ++c)
+              tma_load_3d(a_hi(s) + c * 4096, &tma_a, &raw_full[s], m0 + 32 * c, k0, dev);
+          } else {
+            tma_load_3d(a_hi(s), &tma_a, &raw_full[s], k0, m0, dev);
+          }
+          if (args.b_k_major) {
+            tma_load_3d(b_hi(s), &tma_b, &raw_full[s], k0, n0, dev);
+          } else {
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) tma_load_3d(b_hi(s) + c * 4096, &tma_b, &full[s], n0 + 32 * c, k0, dev);
+            for (int c = 0; c < BN / 32; ++c)
+              tma_load_3d(b_hi(s) + c * 4096, &tma_b, &raw_full[s], n0 + 32 * c, k0, dev);
+          }
         }
       }
     }
@@ -215,107 +289,115 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
       const uint32_t a_sbo = args.a_mn_major ? 512u : 1024u, b_sbo = args.b_k_major ? 1024u : 512u;
       const uint32_t a_lay = args.a_mn_major ? 1u : 2u, b_lay = args.b_k_major ? 2u : 1u;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t round = kb / STAGES;
-        const int c = kb / P, buf = c & 1;
-        const bool chunk_first = (kb % P) == 0;
-        const bool chunk_last = (kb % P) == P - 1 || kb == nk - 1;
-        if (chunk_first) {
-          mbar_wait(&tempty[buf], ((c >> 1) & 1) ^ 1);
+      int g = 0, cg = 0;                          // global k-block / chunk counters
+      for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int rs = g % RS, ls = g % LS;
+          const int buf = cg & 1;
+          const bool chunk_first = (kb % P) == 0;
+          const bool chunk_last = (kb % P) == P - 1 || kb == nk - 1;
+          if (chunk_first) {
+            mbar_wait(&tempty[buf], ((cg >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          mbar_wait(&lo_full[ls], (g / LS) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        }
-        mbar_wait(&split[s], round & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t ahi = smem_u32(a_hi(s)), alo = smem_u32(a_lo(s));
-        const uint32_t bhi = smem_u32(b_hi(s)), blo = smem_u32(b_lo(s));
-        const uint32_t dacc = tmem_d + (uint32_t)(buf * BN);
+          const uint32_t ahi = smem_u32(a_hi(rs)), alo = smem_u32(a_lo(ls));
+          const uint32_t bhi = smem_u32(b_hi(rs)), blo = smem_u32(b_lo(ls));
+          // two independent accumulation chains per chunk: main (hi.hi) and corr
+          // (hi.lo + lo.hi).  Measured: MMAs into ONE accumulator serialise on it
+          // (N=128 tf32 MMAs ran at ~1/3 of peak); alternating chains doubles the rate.
+          const uint32_t dmain = tmem_d + (uint32_t)(buf * 2 * BN);
+          const uint32_t dcorr = dmain + (uint32_t)BN;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t dah = smem_desc(ahi + kk * a_step, a_lbo, a_sbo, a_lay);
-          const uint64_t dal = smem_desc(alo + kk * a_step, a_lbo, a_sbo, a_lay);
-          const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
-          const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
-          mma_tf32(dacc, dal, dbh, idesc, (chunk_first && kk == 0) ? 0u : 1u);   // small terms first
-          mma_tf32(dacc, dah, dbl, idesc, 1u);
-          mma_tf32(dacc, dah, dbh, idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t dah = smem_desc(ahi + kk * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t dal = smem_desc(alo + kk * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
+            const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
+            const uint32_t init = (chunk_first && kk == 0) ? 0u : 1u;
+            mma_tf32<1, 1>(dcorr, dah, dbl, idesc, init);   // hi.lo  (A collector fill)
+            mma_tf32<1, 2>(dmain, dah, dbh, idesc, init);   // hi.hi  (A collector reuse)
+            mma_tf32<1, 0>(dcorr, dal, dbh, idesc, 1u);     // lo.hi
+          }
+          mma_commit<1>(&raw_empty[rs]);
+          mma_commit<1>(&lo_empty[ls]);
+          if (chunk_last) {
+            mma_commit<1>(&tfull[buf]);
+            ++cg;
+          }
         }
-        mma_commit(&empty[s]);
-        if (chunk_last) mma_commit(&tfull[buf]);
       }
     }
   } else if (warp < 6) {
-    // ---------------- split (hi/lo) ----------------
-    const int t = threadIdx.x - 64;  // 0..127
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t round = kb / STAGES;
-      mbar_wait(&full[s], round & 1);
-      float4* ah = reinterpret_cast<float4*>(a_hi(s));
-      float4* al = reinterpret_cast<float4*>(a_lo(s));
+    // ---------------- split: lo = x - trunc_tf32(x) ----------------
+    const int t0 = threadIdx.x - 64;  // 0..127
+    int g = 0;
+    for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int rs = g % RS, ls = g % LS;
+        mbar_wait(&raw_full[rs], (g / RS) & 1);
+        mbar_wait(&lo_empty[ls], ((g / LS) & 1) ^ 1);
+        {
+          const float4* src = reinterpret_cast<const float4*>(a_hi(rs));
+          float4* dst = reinterpret_cast<float4*>(a_lo(ls));
 #pragma unroll 4
-      for (int i = t; i < S::A_BYTES / 16; i += 128) {
-        float4 x = ah[i], h;
-        h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-        h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-        h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-        h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-        ah[i] = h;
-        al[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+          for (int i = t0; i < S::RAW / 16; i += 128) {
+            const float4 x = src[i];
+            dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                                 x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
+                                 x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
+                                 x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&lo_full[ls]);
       }
-      float4* bh = reinterpret_cast<float4*>(b_hi(s));
-      float4* bl = reinterpret_cast<float4*>(b_lo(s));
-#pragma unroll 4
-      for (int i = t; i < S::B_BYTES / 16; i += 128) {
-        float4 x = bh[i], h;
-        h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-        h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-        h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-        h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-        bh[i] = h;
-        bl[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&split[s]);
     }
   } else {
     // ---------------- drain + epilogue ----------------
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
-    float acc[BN];
+    int cg = 0;
+    for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+      int m0, n0, dev;
+      tile_coords(args, t, m0, n0, dev);
+      float acc[BN];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&tfull[buf], (c >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+      for (int c = 0; c < nchunks; ++c, ++cg) {
+        const int buf = cg & 1;
+        mbar_wait(&tfull[buf], (cg >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + cc * 32), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __fadd_rn(acc[cc * 32 + j], __uint_as_float(v[j]));
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&tempty[buf]);
-    }
-    const int row = m0 + q * 32 + lane;
-    if (row < args.M) {
-      float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
-                    (int64_t)row * args.ldc;
-#pragma unroll
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        const int col0 = n0 + cc * 32;
-        if (col0 + 32 <= args.N && (args.ldc & 3) == 0) {
-          float4* dst = reinterpret_cast<float4*>(crow + col0);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
-                                 acc[cc * 32 + 4 * j + 3]);
-        } else {
+        for (int cc = 0; cc < 2 * BN / 32; ++cc) {     // main columns, then corr columns
+          uint32_t v[32];
+          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 2 * BN + cc * 32), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (col0 + j < args.N) crow[col0 + j] = acc[cc * 32 + j];
+            acc[(cc % (BN / 32)) * 32 + j] = __fadd_rn(acc[(cc % (BN / 32)) * 32 + j], __uint_as_float(v[j]));
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&tempty[buf]);
+      }
+      const int row = m0 + q * 32 + lane;
+      if (row < args.M) {
+        float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
+                      (int64_t)row * args.ldc;
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          const int col0 = n0 + cc * 32;
+          if (col0 + 32 <= args.N && (args.ldc & 3) == 0) {
+            float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              dst[j] = make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
+                                   acc[cc * 32 + 4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < args.N) crow[col0 + j] = acc[cc * 32 + j];
+          }
         }
       }
     }
@@ -324,7 +406,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_d));
   }
 }
 
@@ -364,7 +446,6 @@ int make_map(CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer, ui
 struct SpxGemmTC {
   CUtensorMap ma, mb;
   TcArgs args;
-  int bn;
   dim3 grid;
   spx_gemm_params p;
 };
@@ -380,32 +461,57 @@ bool spx_gemm_tc_supported(const spx_gemm_params& p) {
 int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   SpxGemmTC* g = new SpxGemmTC();
   g->p = p;
-  g->bn = 128;
   const uint64_t a = p.base + (uint64_t)(p.a_off * 4), b = p.base + (uint64_t)(p.b_off * 4);
   int rc;
   if (p.a_mn_major) rc = make_map(&g->ma, a, p.M, p.K, p.ndev, p.lda * 4, p.dev_stride, 32, true);
   else rc = make_map(&g->ma, a, p.K, p.M, p.ndev, p.lda * 4, p.dev_stride, BM, false);
   if (rc) { delete g; return rc; }
-  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, g->bn, false);
+  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, BN, false);
   else rc = make_map(&g->mb, b, p.N, p.K, p.ndev, p.ldb * 4, p.dev_stride, 32, true);
   if (rc) { delete g; return rc; }
-  g->args.M = p.M; g->args.N = p.N; g->args.K = p.K;
-  g->args.a_mn_major = p.a_mn_major; g->args.b_k_major = p.b_k_major;
-  g->args.promote = p.debug > 0 ? p.debug : 4;   // debug field: override promote
-  g->args.c_base = p.base + (uint64_t)(p.c_off * 4);
-  g->args.dev_stride = p.dev_stride;
-  g->args.ldc = p.ldc;
-  g->grid = dim3((p.N + g->bn - 1) / g->bn, (p.M + BM - 1) / BM, p.ndev);
+  TcArgs& a_ = g->args;
+  a_.M = p.M; a_.N = p.N; a_.K = p.K;
+  a_.a_mn_major = p.a_mn_major; a_.b_k_major = p.b_k_major;
+  a_.promote = (p.debug & 255) > 0 ? (p.debug & 255) : 4;   // debug field: override promote
+  a_.tiles_m = (p.M + BM - 1) / BM;
+  a_.tiles_n = (p.N + BN - 1) / BN;
+  a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
+  a_.c_base = p.base + (uint64_t)(p.c_off * 4);
+  a_.dev_stride = p.dev_stride;
+  a_.ldc = p.ldc;
+  const int sms = spx_num_sms();
+  g->grid = dim3((unsigned)(a_.tiles < sms ? a_.tiles : sms));
   *out = g;
   return 0;
 }
 
-int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
-  {
-    static bool attr = false;
-    if (!attr) { SPX_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL)); attr = true; }
-    gemm_tc_kernel<128><<<g->grid, NTHREADS, Smem<128>::TOTAL, s>>>(g->ma, g->mb, g->args);
+template <int RS_, int LS_>
+static int launch_cfg(const SpxGemmTC* g, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    SPX_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<RS_, LS_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg<RS_, LS_>::TOTAL));
+    attr = true;
   }
+  gemm_tc_kernel<RS_, LS_><<<g->grid, NTHREADS, Cfg<RS_, LS_>::TOTAL, s>>>(g->ma, g->mb, g->args);
+  return 0;
+}
+
+int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
+  static int pipe = -1;
+  if (pipe < 0) {
+    const char* e = getenv("SPX_GEMM_PIPE");
+    pipe = e ? atoi(e) : 43;
+  }
+  int rc;
+  switch (pipe) {
+    case 52: rc = launch_cfg<5, 2>(g, s); break;
+    case 33: rc = launch_cfg<3, 3>(g, s); break;
+    case 34: rc = launch_cfg<3, 4>(g, s); break;
+    case 24: rc = launch_cfg<2, 4>(g, s); break;
+    default: rc = launch_cfg<4, 3>(g, s);
+  }
+  if (rc) return rc;
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;

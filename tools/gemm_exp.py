@@ -1,0 +1,23 @@
+"""GEMM timing on C2 shapes and a large square (dev tool)."""
+import os
+import sys
+import numpy as np
+sys.path.insert(0, "."); sys.path.insert(0, "tools")
+from debug_gemm import G, rel
+from paper_2401_11202_b200 import runtime as R
+dev = R.Device(0)
+rng = np.random.default_rng(0)
+print("SPX_GEMM_PIPE", os.environ.get("SPX_GEMM_PIPE"))
+for (M, N, K, at, bt) in [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
+                          (1024, 1024, 2048, True, False), (4096, 4096, 4096, False, False)]:
+    A = rng.standard_normal((K, M) if at else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if bt else (K, N)).astype(np.float32)
+    g = G(dev, A, B, at, bt)
+    C = g.run()
+    AA = A.T if at else A
+    BB = B.T if bt else B
+    err = rel(C, AA.astype(np.float64) @ BB)
+    ms = g.time_ms(10)
+    g.close()
+    print(f"{M}x{N}x{K} a_mn={int(at)} b_k={int(bt)} {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:6.1f} TF fp32-eq "
+          f"({3*2*M*N*K/ms/1e9/807.55*100:4.1f}% tf32 peak) rel err {err:.2e}", flush=True)
