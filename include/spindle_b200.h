@@ -111,7 +111,9 @@ typedef struct {
   int32_t a_mn_major;             /* 0: A stored [M][K]; 1: A stored [K][M]    */
   int32_t b_k_major;              /* 0: B stored [K][N]; 1: B stored [N][K]    */
   int32_t path;                   /* 0 auto, 1 tcgen05 3xTF32, 2 SIMT fp32     */
-  int32_t debug;                  /* 0; diagnostics bits for the tcgen05 path  */
+  int32_t promote;                /* k-blocks per TMEM chunk (0 = default 4)     */
+  int32_t reserve_sms;            /* SMs left free for concurrent collectives    */
+  int32_t pad;
 } spx_gemm_params;
 
 /* ---- collectives over co-located virtual devices ------------------------- */
@@ -180,6 +182,11 @@ int spx_comm_destroy(int comm);
 /* plans: a sequence of records [kind, param struct] executed in order on a stream */
 int spx_plan_create(uint64_t* out_plan);
 int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t params_bytes);
+/* Scheduling (optional): run record `index` on stream `stream` (0 = the stream
+ * passed to run/capture, 1 = the plan's side stream, used for collectives so
+ * they overlap compute), after the records listed in `waits` (indices of
+ * earlier records on the other stream) have completed. */
+int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, int n_waits);
 int spx_plan_finalize(uint64_t plan);              /* builds TMA descriptors etc. */
 int spx_plan_run(uint64_t plan, uint64_t stream);  /* eager launch of every record */
 int spx_plan_capture(uint64_t plan, uint64_t stream);  /* record into a CUDA graph */

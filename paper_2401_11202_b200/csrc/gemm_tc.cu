@@ -472,14 +472,15 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   TcArgs& a_ = g->args;
   a_.M = p.M; a_.N = p.N; a_.K = p.K;
   a_.a_mn_major = p.a_mn_major; a_.b_k_major = p.b_k_major;
-  a_.promote = (p.debug & 255) > 0 ? (p.debug & 255) : 4;   // debug field: override promote
+  a_.promote = p.promote > 0 ? p.promote : 4;
   a_.tiles_m = (p.M + BM - 1) / BM;
   a_.tiles_n = (p.N + BN - 1) / BN;
   a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
   a_.c_base = p.base + (uint64_t)(p.c_off * 4);
   a_.dev_stride = p.dev_stride;
   a_.ldc = p.ldc;
-  const int sms = spx_num_sms();
+  int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
+  if (sms < 1) sms = 1;
   g->grid = dim3((unsigned)(a_.tiles < sms ? a_.tiles : sms));
   *out = g;
   return 0;

@@ -125,11 +125,18 @@ struct Record {
   int path;  // GEMM: 1 tcgen05, 2 simt
   std::vector<uint8_t> params;
   SpxGemmTC* tc = nullptr;
+  int stream = 0;               // 0 main, 1 side
+  std::vector<int> waits;       // records on the other stream to wait for
+  bool signal = false;          // a later record on the other stream waits for this one
+  cudaEvent_t done = nullptr;
 };
 
 struct Plan {
   std::vector<Record> recs;
   bool finalized = false;
+  bool two_streams = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
@@ -280,8 +287,55 @@ int spx_plan_finalize(uint64_t plan) {
     if (r.kind == SPX_K_GEMM && r.path == 1 && !r.tc) {
       if (spx_gemm_tc_prepare(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), &r.tc)) return -1;
     }
+    if (r.signal && !r.done) SPX_CUDA(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+  }
+  if (P->two_streams) {
+    int lo = 0, hi = 0;
+    SPX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SPX_CUDA(cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, hi));   // collectives first
+    SPX_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+    SPX_CUDA(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming));
   }
   P->finalized = true;
+  return 0;
+}
+
+// Issue every record: main-stream records on `s`, side-stream records on the
+// plan's side stream, cross-stream order through events (fork at the start,
+// join at the end, so the whole plan is one unit on `s` -- also under capture).
+static int issue_all(Plan* P, cudaStream_t s, int* nl) {
+  if (!P->two_streams) {
+    for (auto& r : P->recs)
+      if (run_record(r, s, nl)) return -1;
+    return 0;
+  }
+  SPX_CUDA(cudaEventRecord(P->fork, s));
+  SPX_CUDA(cudaStreamWaitEvent(P->side, P->fork, 0));
+  for (auto& r : P->recs) {
+    cudaStream_t rs = r.stream ? P->side : s;
+    for (int w : r.waits) SPX_CUDA(cudaStreamWaitEvent(rs, P->recs[w].done, 0));
+    if (run_record(r, rs, nl)) return -1;
+    if (r.signal) SPX_CUDA(cudaEventRecord(r.done, rs));
+  }
+  SPX_CUDA(cudaEventRecord(P->join, P->side));
+  SPX_CUDA(cudaStreamWaitEvent(s, P->join, 0));
+  return 0;
+}
+
+int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, int n_waits) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (P->finalized) return spx_set_error("plan already finalized");
+  if (index < 0 || index >= (int)P->recs.size()) return spx_set_error("record index out of range");
+  Record& r = P->recs[index];
+  r.stream = stream ? 1 : 0;
+  r.waits.clear();
+  for (int i = 0; i < n_waits; ++i) {
+    const int w = waits[i];
+    if (w < 0 || w >= index) return spx_set_error("record %d waits for %d: not an earlier record", index, w);
+    r.waits.push_back(w);
+    P->recs[w].signal = true;
+  }
+  if (r.stream) P->two_streams = true;
   return 0;
 }
 
@@ -290,8 +344,7 @@ int spx_plan_run(uint64_t plan, uint64_t stream) {
   if (!P->finalized && spx_plan_finalize(plan)) return -1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int nl = 0;
-  for (auto& r : P->recs)
-    if (run_record(r, s, &nl)) return -1;
+  if (issue_all(P, s, &nl)) return -1;
   P->launches = nl;
   return 0;
 }
@@ -304,13 +357,11 @@ int spx_plan_capture(uint64_t plan, uint64_t stream) {
   if (P->graph) { cudaGraphDestroy(P->graph); P->graph = nullptr; }
   SPX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int nl = 0;
-  for (auto& r : P->recs) {
-    if (run_record(r, s, &nl)) {
-      cudaGraph_t g;
-      cudaStreamEndCapture(s, &g);
-      if (g) cudaGraphDestroy(g);
-      return -1;
-    }
+  if (issue_all(P, s, &nl)) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    return -1;
   }
   SPX_CUDA(cudaStreamEndCapture(s, &P->graph));
   SPX_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
@@ -339,8 +390,13 @@ int spx_plan_destroy(uint64_t plan) {
   Plan* P = reinterpret_cast<Plan*>(plan);
   if (P->exec) cudaGraphExecDestroy(P->exec);
   if (P->graph) cudaGraphDestroy(P->graph);
-  for (auto& r : P->recs)
+  for (auto& r : P->recs) {
     if (r.tc) spx_gemm_tc_free(r.tc);
+    if (r.done) cudaEventDestroy(r.done);
+  }
+  if (P->side) cudaStreamDestroy(P->side);
+  if (P->fork) cudaEventDestroy(P->fork);
+  if (P->join) cudaEventDestroy(P->join);
   delete P;
   return 0;
 }

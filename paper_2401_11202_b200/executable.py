@@ -45,7 +45,8 @@ class Executable:
     DRY_TABLES = 1 << 44
 
     def __init__(self, module, func="main", device: R.Device | None = None, devices=None,
-                 comm_mode="local", comms=None, gemm_path=0, dry=False, comm_factory=None):
+                 comm_mode="local", comms=None, gemm_path=0, dry=False, comm_factory=None,
+                 overlap=None):
         """dry=True builds the records against fake addresses without a GPU
         (used by the CPU tests and the record simulator)."""
         self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode).compile()
@@ -54,19 +55,30 @@ class Executable:
         self.ndev = len(self.comp.devices)
         self.gemm_path = gemm_path
         self.comms = comms or {}
+        import os
+        if overlap is None:
+            overlap = comm_mode == "nccl" and os.environ.get("SPX_OVERLAP", "1") != "0"
+        self.overlap = overlap
+        self.reserve_sms = int(os.environ.get("SPX_RESERVE_SMS", "0")) if overlap else 0
         self._layout()
         self._alloc()
         if comm_mode == "nccl" and comm_factory is not None:
             self.comms = comm_factory(self)
         self._tables = []
         self._records = []
+        self._krange = []          # per compiler kernel: [first record, end record)
+
         self._emit()
         self._upload_tables()
+        # collectives on a side stream, overlapped with compute (NCCL mode)
+        self.sched = self._schedule() if self.overlap else []
         self.plan = None
         if not dry:
             self.plan = R.NativePlan(self.device)
             for kind, params in self._records:
                 self.plan.add(kind, params)
+            for idx, stream, waits in self.sched:
+                self.plan.set_sched(idx, stream, waits)
             self.plan.finalize()
 
     # ---------------------------------------------------------------- layout
@@ -87,6 +99,13 @@ class Executable:
             top += _align(c.buffers[a])
         base = top
         keep = set(c.result_bufs)
+        if self.overlap:
+            # buffers a side-stream collective touches are not recycled: reuse
+            # would add write-after-read edges that serialise the streams
+            for k in ks:
+                if k.kind == "coll" and k.data["kind"] != "all_slice":
+                    keep.update(k.ins)
+                    keep.update(k.outs)
         free: list[tuple[int, int]] = []   # (offset, size) holes above `base`
         hi = base
         order = sorted((first[b], b) for b in first if b not in off)
@@ -246,6 +265,13 @@ class Executable:
     def _emit(self):
         c = self.comp
         for k in c.kernels:
+            first = len(self._records)
+            self._emit_one(k)
+            self._krange.append((first, len(self._records)))
+
+    def _emit_one(self, k):
+        c = self.comp
+        if True:
             if k.kind == "ew":
                 self._records.append((R.K_EW, self._ew_params(k.data["exprs"], k.data["dims"],
                                                               k.data.get("outs_keep"))))
@@ -258,6 +284,58 @@ class Executable:
                     self._emit_coll_local(k)
                 else:
                     self._emit_coll_nccl(k)
+
+    def _schedule(self):
+        """Two-stream schedule: communicating collectives on stream 1, everything
+        else on stream 0; a record waits for the LATEST earlier record on the
+        other stream whose arena intervals conflict with it (RAW, WAR or WAW --
+        the liveness packing reuses memory, so WAR/WAW matter too)."""
+        c = self.comp
+        iv = {}
+
+        def ivals(names):
+            out = []
+            for b in names:
+                o = self.off[b]
+                out.append((o, o + _align(c.buffers[b])))
+            return out
+
+        kin, kout, kstream = [], [], []
+        for k in c.kernels:
+            comm = k.kind == "coll" and k.data["kind"] != "all_slice"
+            kstream.append(1 if comm else 0)
+            r = ivals(k.ins)
+            w = ivals(k.outs)
+            if k.kind == "reduce":
+                sc = (self.scratch_off, self.zero_off)
+                r.append(sc)
+                w.append(sc)
+            kin.append(r)
+            kout.append(w)
+
+        def hit(a, b):
+            return any(x0 < y1 and y0 < x1 for x0, x1 in a for y0, y1 in b)
+
+        sched = []
+        by_stream = {0: [], 1: []}
+        for i, k in enumerate(c.kernels):
+            st = kstream[i]
+            other = by_stream[1 - st]
+            wait = None
+            for j in reversed(other):
+                if hit(kin[i], kout[j]) or hit(kout[i], kin[j]) or hit(kout[i], kout[j]):
+                    wait = j
+                    break
+            first, end = self._krange[i]
+            if end > first:
+                waits = [self._krange[wait][1] - 1] if wait is not None and self._krange[wait][1] > self._krange[wait][0] else []
+                for r in range(first, end):
+                    if st or waits:
+                        sched.append((r, st, waits if r == first else []))
+            by_stream[st].append(i)
+        if not any(st for _, st, _ in sched):
+            return []
+        return sched
 
     def _emit_reduce(self, k):
         in_dims = list(k.data["in_dims"]) or [1]
@@ -333,6 +411,8 @@ class Executable:
         p.a_mn_major = 1 if at else 0
         p.b_k_major = 1 if bt else 0
         p.path = self.gemm_path
+        # with collectives overlapped on a side stream, leave SMs for NCCL's CTAs
+        p.reserve_sms = self.reserve_sms
         self._records.append((R.K_GEMM, p))
 
     # ---- in-GPU collectives (spmd_interp.py:74-123 as group kernels) ----

@@ -57,7 +57,8 @@ class GemmParams(C.Structure):
                 ("a_off", C.c_int64), ("b_off", C.c_int64), ("c_off", C.c_int64),
                 ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
                 ("a_mn_major", C.c_int32), ("b_k_major", C.c_int32),
-                ("path", C.c_int32), ("debug", C.c_int32)]
+                ("path", C.c_int32), ("promote", C.c_int32), ("reserve_sms", C.c_int32),
+                ("pad", C.c_int32)]
 
 
 class GatherParams(C.Structure):
@@ -89,7 +90,7 @@ EXPORTS = [
     "spx_plan_create", "spx_plan_add", "spx_plan_finalize", "spx_plan_run", "spx_plan_capture",
     "spx_plan_replay", "spx_plan_launch_count", "spx_plan_destroy", "spx_plan_record_info",
     "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
-    "spx_plan_profile", "spx_host_alloc", "spx_host_free",
+    "spx_plan_profile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
 ]
 
 _lib = None
@@ -133,6 +134,7 @@ def load(build_if_missing: bool = True):
         "spx_comm_init": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)],
         "spx_comm_destroy": [C.c_int], "spx_device_init": [C.c_int], "spx_params_size": [C.c_int],
         "spx_host_alloc": [C.c_uint64, C.POINTER(C.c_void_p)], "spx_host_free": [C.c_void_p],
+        "spx_plan_set_sched": [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int],
     }
     for name, args in sigs.items():
         getattr(lib, name).argtypes = args
@@ -240,6 +242,10 @@ class NativePlan:
         assert isinstance(params, PARAMS[kind])
         call(self.lib.spx_plan_add, self.h, kind, C.byref(params), C.sizeof(params))
         self.n_records += 1
+
+    def set_sched(self, index: int, stream: int, waits):
+        arr = (C.c_int * max(1, len(waits)))(*waits)
+        call(self.lib.spx_plan_set_sched, self.h, index, stream, arr, len(waits))
 
     def finalize(self):
         call(self.lib.spx_plan_finalize, self.h)

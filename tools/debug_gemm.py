@@ -30,7 +30,7 @@ class G:
         p.a_off, p.b_off, p.c_off = 0, pad(na), pad(na) + pad(nb)
         p.lda, p.ldb, p.ldc = A.shape[1], B.shape[1], N
         p.a_mn_major, p.b_k_major = int(at), int(bt)
-        p.path, p.debug = path, promote
+        p.path, p.promote = path, promote
         self.plan = R.NativePlan(dev)
         self.plan.add(R.K_GEMM, p)
         self.plan.finalize()
