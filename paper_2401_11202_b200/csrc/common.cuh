@@ -55,6 +55,8 @@ int spx_set_error(const char* fmt, ...);
 
 // Launch entry points (host) implemented per kernel family.
 int spx_launch_ew(const spx_ew_params& p, cudaStream_t s, int* nlaunch);
+int spx_ew_static_match(const spx_ew_params& p);     // catalog index or -1 (ew_static.cu)
+int spx_launch_ew_static(int id, const spx_ew_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_creduce(const spx_creduce_params& p, cudaStream_t s, int* nlaunch);

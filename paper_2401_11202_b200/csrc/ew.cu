@@ -10,42 +10,65 @@
 
 namespace {
 
-template <int NIN>
+// U float4 granules per thread per iteration (loads hoisted).  Index math is
+// 32-bit relative to per-input base pointers (numel < 2^31).  This generic
+// interpreter is the fallback; the model zoo's programs run as the
+// compile-time-specialised kernels of ew_static.cu.
+template <int NIN, int U>
 __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ spx_ew_params p) {
   const int d = blockIdx.y;
   const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
   float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
-  const int64_t nvec = p.numel >> 2;
+  const uint32_t nvec = (uint32_t)(p.numel >> 2);
   const bool two_d = p.rank == 2;
-  const int64_t cols = two_d ? p.dims[1] : p.numel;
-  const int64_t step = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += step) {
-    const int64_t e = v << 2;
-    int64_t r = 0, c = e;
-    if (two_d) {
-      r = e / cols;
-      c = e - r * cols;
-    }
-    RegFile<4> f;
+  const uint32_t cols = (uint32_t)(two_d ? p.dims[1] : p.numel);
+  const uint32_t step = gridDim.x * blockDim.x;
+  const float* in_base[NIN];
+  uint32_t s0[NIN];
+  bool s1[NIN];
 #pragma unroll
-    for (int j = 0; j < NIN; ++j) {
-      if (j >= p.n_in) break;
-      const int64_t s1 = p.in[j].stride[p.rank - 1];
-      const int64_t off = p.in[j].off + (two_d ? r * p.in[j].stride[0] : 0) + (s1 ? c : 0);
-      if (s1) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(fb + off));
-        f.r[j].v[0] = x.x; f.r[j].v[1] = x.y; f.r[j].v[2] = x.z; f.r[j].v[3] = x.w;
-      } else {
-        const float x = __ldg(fb + off);
-        f.r[j].v[0] = x; f.r[j].v[1] = x; f.r[j].v[2] = x; f.r[j].v[3] = x;
+  for (int j = 0; j < NIN; ++j) {
+    in_base[j] = fb + p.in[j].off;
+    s0[j] = two_d ? (uint32_t)p.in[j].stride[0] : 0u;
+    s1[j] = p.in[j].stride[p.rank - 1] != 0;
+  }
+  for (uint32_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += step * U) {
+    Vec<4> x[U][NIN];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * step;
+      if (v >= nvec) break;
+      const uint32_t e = v << 2;
+      const uint32_t r = two_d ? e / cols : 0u;
+      const uint32_t c = e - r * cols;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) {
+        if (j >= p.n_in) break;
+        const float* src = in_base[j] + (size_t)r * s0[j];
+        if (s1[j]) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(src + c));
+          x[u][j].v[0] = t.x; x[u][j].v[1] = t.y; x[u][j].v[2] = t.z; x[u][j].v[3] = t.w;
+        } else {
+          const float t = __ldg(src);
+          x[u][j].v[0] = t; x[u][j].v[1] = t; x[u][j].v[2] = t; x[u][j].v[3] = t;
+        }
       }
     }
-    run_program<4>(p.prog, p.imm, p.n_prog, f);
 #pragma unroll
-    for (int o = 0; o < SPX_MAX_OUT; ++o) {
-      if (o >= p.n_out) break;
-      const Vec<4> y = f.get(p.out_reg[o]);
-      *reinterpret_cast<float4*>(ob + p.out_off[o] + e) = make_float4(y.v[0], y.v[1], y.v[2], y.v[3]);
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * step;
+      if (v >= nvec) break;
+      RegFile<4> f;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) f.r[j] = x[u][j];
+      run_program<4>(p.prog, p.imm, p.n_prog, f);
+#pragma unroll
+      for (int o = 0; o < SPX_MAX_OUT; ++o) {
+        if (o >= p.n_out) break;
+        const Vec<4> y = f.get(p.out_reg[o]);
+        *reinterpret_cast<float4*>(ob + p.out_off[o] + ((size_t)v << 2)) =
+            make_float4(y.v[0], y.v[1], y.v[2], y.v[3]);
+      }
     }
   }
 }
@@ -97,16 +120,17 @@ int spx_launch_ew(const spx_ew_params& p, cudaStream_t s, int* nlaunch) {
   if (p.numel <= 0 || p.ndev <= 0) return 0;
   if (p.n_prog > SPX_MAX_PROG || p.n_in > SPX_MAX_IN || p.n_out > SPX_MAX_OUT)
     return spx_set_error("ew: program exceeds ABI limits");
-  const bool vec = p.vec && p.numel % 4 == 0 && p.rank <= 2;
+  const bool vec = p.vec && p.numel % 4 == 0 && p.rank <= 2 && p.numel < (int64_t(1) << 31);
   if (vec) {
-    dim3 grid(blocks_for(p.numel / 4), (unsigned)p.ndev);
+    const int64_t nv = p.numel / 4;
+    auto grid_u = [&](int u) { return dim3(blocks_for((nv + u - 1) / u), (unsigned)p.ndev); };
     switch (p.n_in) {
       case 0:
-      case 1: ew_vec_kernel<1><<<grid, 256, 0, s>>>(p); break;
-      case 2: ew_vec_kernel<2><<<grid, 256, 0, s>>>(p); break;
-      case 3: ew_vec_kernel<3><<<grid, 256, 0, s>>>(p); break;
-      case 4: ew_vec_kernel<4><<<grid, 256, 0, s>>>(p); break;
-      default: ew_vec_kernel<SPX_MAX_IN><<<grid, 256, 0, s>>>(p);
+      case 1: ew_vec_kernel<1, 1><<<grid_u(1), 256, 0, s>>>(p); break;
+      case 2: ew_vec_kernel<2, 1><<<grid_u(1), 256, 0, s>>>(p); break;
+      case 3: ew_vec_kernel<3, 1><<<grid_u(1), 256, 0, s>>>(p); break;
+      case 4: ew_vec_kernel<4, 1><<<grid_u(1), 256, 0, s>>>(p); break;
+      default: ew_vec_kernel<SPX_MAX_IN, 1><<<grid_u(1), 256, 0, s>>>(p);
     }
   } else {
     ew_gen_kernel<<<dim3(blocks_for(p.numel), (unsigned)p.ndev), 256, 0, s>>>(p);

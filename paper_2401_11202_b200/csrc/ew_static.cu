@@ -1,0 +1,161 @@
+// Compile-time-specialised fused elementwise kernels for the programs the
+// reference's model zoo actually produces (models.py:43-85: momentum update,
+// square activation and its gradient, residual add, scale, sub).  The plan
+// still emits the generic register-machine program (ew.cu); spx_plan_add
+// matches it against this catalog and, on a hit, launches straight-line code
+// with the same per-op IEEE rounding (bit-identical results) but no
+// interpretation overhead -- ncu showed the interpreter latency-bound at
+// 0.9-1.7 TB/s on exactly these programs.
+#include "interp.cuh"
+
+namespace {
+
+constexpr uint32_t ins(int op, int a, int b, int d) {
+  return (uint32_t)op | ((uint32_t)a << 8) | ((uint32_t)b << 16) | ((uint32_t)d << 24);
+}
+
+template <uint32_t I>
+SPX_DEV void step(Vec<4>* r, float c) {
+  constexpr int op = I & 255, a = (I >> 8) & 255, b = (I >> 16) & 255, d = (I >> 24) & 255;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float x = r[a].v[k], y = r[b].v[k];
+    float z;
+    if (op == SPX_OP_ADD) z = f_add(x, y);
+    else if (op == SPX_OP_MUL) z = f_mul(x, y);
+    else if (op == SPX_OP_NEG) z = -x;
+    else if (op == SPX_OP_EXP) z = expf(x);
+    else if (op == SPX_OP_MAX) z = f_max(x, y);
+    else if (op == SPX_OP_IMM) z = c;
+    else if (op == SPX_OP_ADDI) z = f_add(x, c);
+    else if (op == SPX_OP_MULI) z = f_mul(x, c);
+    else if (op == SPX_OP_IADD) z = f_add(c, x);
+    else if (op == SPX_OP_IMUL) z = f_mul(c, x);
+    else z = x;
+    r[d].v[k] = z;
+  }
+}
+
+template <uint32_t... I, int... Ix>
+SPX_DEV void run_static(Vec<4>* r, const float* imm, std::integer_sequence<int, Ix...>) {
+  (step<I>(r, imm[Ix]), ...);
+}
+
+// NIN inputs, NOUT outputs (slots O0, O1), program I...; 2 float4 granules per
+// thread per iteration with all loads hoisted.
+template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
+__global__ void __launch_bounds__(256) ew_static_kernel(const __grid_constant__ spx_ew_params p) {
+  constexpr int U = 2;
+  const int d = blockIdx.y;
+  const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
+  float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
+  const uint32_t nvec = (uint32_t)(p.numel >> 2);
+  const bool two_d = p.rank == 2;
+  const uint32_t cols = (uint32_t)(two_d ? p.dims[1] : p.numel);
+  const uint32_t step_ = gridDim.x * blockDim.x;
+  float* out0 = ob + p.out_off[0];
+  float* out1 = ob + p.out_off[NOUT > 1 ? 1 : 0];
+  for (uint32_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += step_ * U) {
+    Vec<4> r[U][SPX_NREG];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * step_;
+      if (v >= nvec) break;
+      const uint32_t e = v << 2;
+      const uint32_t row = two_d ? e / cols : 0u;
+      const uint32_t col = e - row * cols;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) {
+        const float* src = fb + p.in[j].off + (two_d ? (size_t)row * p.in[j].stride[0] : 0);
+        if (p.in[j].stride[p.rank - 1] != 0) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(src + col));
+          r[u][j].v[0] = t.x; r[u][j].v[1] = t.y; r[u][j].v[2] = t.z; r[u][j].v[3] = t.w;
+        } else {
+          const float t = __ldg(src);
+          r[u][j].v[0] = t; r[u][j].v[1] = t; r[u][j].v[2] = t; r[u][j].v[3] = t;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * step_;
+      if (v >= nvec) break;
+      run_static<I...>(r[u], p.imm, std::make_integer_sequence<int, (int)sizeof...(I)>{});
+      const size_t e = (size_t)v << 2;
+      *reinterpret_cast<float4*>(out0 + e) = make_float4(r[u][O0].v[0], r[u][O0].v[1], r[u][O0].v[2], r[u][O0].v[3]);
+      if (NOUT > 1)
+        *reinterpret_cast<float4*>(out1 + e) =
+            make_float4(r[u][O1].v[0], r[u][O1].v[1], r[u][O1].v[2], r[u][O1].v[3]);
+    }
+  }
+}
+
+struct Entry {
+  int n_in, n_out, out0, out1, n_prog;
+  uint32_t prog[8];
+  void (*launch)(const spx_ew_params&, dim3, cudaStream_t);
+};
+
+template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
+void launch_static(const spx_ew_params& p, dim3 g, cudaStream_t s) {
+  ew_static_kernel<NIN, NOUT, O0, O1, I...><<<g, 256, 0, s>>>(p);
+}
+
+#define OP(x) SPX_OP_##x
+// The catalog (program slots as allocated by plan.Program.build).
+#define E(NIN, NOUT, O0, O1, N, ...) \
+  {NIN, NOUT, O0, O1, N, {__VA_ARGS__}, launch_static<NIN, NOUT, O0, O1, __VA_ARGS__>}
+const Entry kCatalog[] = {
+    // momentum update  m' = c0*m + g ; p' = p + -(c2*m')        (models.py:79-85)
+    E(3, 2, 0, 1, 5, ins(OP(IMUL), 0, 0, 0), ins(OP(ADD), 0, 1, 0), ins(OP(IMUL), 0, 0, 1), ins(OP(NEG), 1, 0, 1),
+      ins(OP(ADD), 2, 1, 1)),
+    // square-activation gradient  dh * (c*z)                    (models.py:76-77)
+    E(2, 1, 0, 0, 2, ins(OP(IMUL), 1, 0, 1), ins(OP(MUL), 0, 1, 0)),
+    // residual / bias add
+    E(2, 1, 0, 0, 1, ins(OP(ADD), 0, 1, 0)),
+    // square activation  z * z                                   (models.py:73-74)
+    E(1, 1, 0, 0, 1, ins(OP(MUL), 0, 0, 0)),
+    // scale  c * x
+    E(1, 1, 0, 0, 1, ins(OP(IMUL), 0, 0, 0)),
+    // sub  a + -b  (+ c)
+    E(3, 1, 0, 0, 3, ins(OP(ADD), 0, 1, 0), ins(OP(NEG), 2, 0, 1), ins(OP(ADD), 0, 1, 0)),
+    E(2, 1, 0, 0, 2, ins(OP(NEG), 1, 0, 1), ins(OP(ADD), 0, 1, 0)),
+    // product
+    E(2, 1, 0, 0, 1, ins(OP(MUL), 0, 1, 0)),
+};
+#undef E
+#undef OP
+
+}  // namespace
+
+// Catalog index for a program, or -1.  Also requires the vector-path layout.
+int spx_ew_static_match(const spx_ew_params& p) {
+  if (!p.vec || p.numel % 4 || p.rank > 2 || p.numel >= (int64_t(1) << 31)) return -1;
+  for (int i = 0; i < (int)(sizeof(kCatalog) / sizeof(kCatalog[0])); ++i) {
+    const Entry& c = kCatalog[i];
+    if (c.n_in != p.n_in || c.n_out != p.n_out || c.n_prog != p.n_prog) continue;
+    if (p.out_reg[0] != c.out0 || (c.n_out > 1 && p.out_reg[1] != c.out1)) continue;
+    bool ok = true;
+    for (int k = 0; k < c.n_prog && ok; ++k) {
+      const spx_insn& q = p.prog[k];
+      const uint32_t want = c.prog[k];
+      const int op = want & 255, a = (want >> 8) & 255, b = (want >> 16) & 255, d = (want >> 24) & 255;
+      const bool unary = op == SPX_OP_NEG || op == SPX_OP_EXP || op == SPX_OP_IMM || op >= SPX_OP_ADDI;
+      ok = q.op == op && q.a == a && q.dst == d && (unary || q.b == b);
+    }
+    if (ok) return i;
+  }
+  return -1;
+}
+
+int spx_launch_ew_static(int id, const spx_ew_params& p, cudaStream_t s, int* nlaunch) {
+  const int64_t nv = p.numel / 4;
+  int64_t b = (nv / 2 + 255) / 256;
+  const int64_t cap = (int64_t)spx_num_sms() * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  kCatalog[id].launch(p, dim3((unsigned)b, (unsigned)p.ndev), s);
+  SPX_CHECK_LAUNCH();
+  if (nlaunch) ++*nlaunch;
+  return 0;
+}

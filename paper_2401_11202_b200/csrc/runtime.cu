@@ -144,7 +144,9 @@ struct Plan {
 
 static int run_record(Record& r, cudaStream_t s, int* nl) {
   switch (r.kind) {
-    case SPX_K_EW: return spx_launch_ew(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
+    case SPX_K_EW:
+      if (r.path > 0) return spx_launch_ew_static(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
+      return spx_launch_ew(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
     case SPX_K_REDUCE: return spx_launch_reduce(*reinterpret_cast<const spx_reduce_params*>(r.params.data()), s, nl);
     case SPX_K_GATHER: return spx_launch_gather(*reinterpret_cast<const spx_gather_params*>(r.params.data()), s, nl);
     case SPX_K_CREDUCE: return spx_launch_creduce(*reinterpret_cast<const spx_creduce_params*>(r.params.data()), s, nl);
@@ -271,6 +273,11 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
   r.kind = kind;
   r.path = 0;
   r.params.assign(static_cast<const uint8_t*>(params), static_cast<const uint8_t*>(params) + bytes);
+  if (kind == SPX_K_EW) {
+    const char* e = getenv("SPX_EW_STATIC");
+    if (!(e && e[0] == '0'))
+      r.path = 1 + spx_ew_static_match(*reinterpret_cast<const spx_ew_params*>(r.params.data()));
+  }
   if (kind == SPX_K_GEMM) {
     const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
     const bool tc_ok = spx_gemm_tc_supported(g);
