@@ -57,9 +57,10 @@ class Executable:
         self.comms = comms or {}
         import os
         if overlap is None:
-            overlap = comm_mode == "nccl" and os.environ.get("SPX_OVERLAP", "1") != "0"
-        self.overlap = overlap
-        self.reserve_sms = int(os.environ.get("SPX_RESERVE_SMS", "0")) if overlap else 0
+            overlap = os.environ.get("SPX_OVERLAP", "1") != "0"
+        self.side = self._side_kernels() if overlap else set()
+        self.overlap = bool(self.side)
+        self.reserve_sms = int(os.environ.get("SPX_RESERVE_SMS", "0")) if self.overlap else 0
         self._layout()
         self._alloc()
         if comm_mode == "nccl" and comm_factory is not None:
@@ -100,10 +101,10 @@ class Executable:
         base = top
         keep = set(c.result_bufs)
         if self.overlap:
-            # buffers a side-stream collective touches are not recycled: reuse
-            # would add write-after-read edges that serialise the streams
-            for k in ks:
-                if k.kind == "coll" and k.data["kind"] != "all_slice":
+            # buffers a side-stream kernel touches are not recycled: reuse would
+            # add write-after-read edges that serialise the two streams
+            for i, k in enumerate(ks):
+                if i in self.side:
                     keep.update(k.ins)
                     keep.update(k.outs)
         free: list[tuple[int, int]] = []   # (offset, size) holes above `base`
@@ -285,6 +286,37 @@ class Executable:
                 else:
                     self._emit_coll_nccl(k)
 
+    def _side_kernels(self) -> set:
+        """Kernels that run on the side stream, overlapped with the main chain:
+        * NCCL collectives (one mesh device per GPU);
+        * off-critical-path GEMMs: weight gradients whose results feed only the
+          parameter update (kernels writing function results) or a side-stream
+          collective -- e.g. act^T @ dh in matmul_grads (models.py:64-71).  A
+          small-tile dW GEMM then fills SMs the dX GEMM leaves idle."""
+        import os
+        c = self.comp
+        ks = c.kernels
+        results = set(c.result_bufs)
+        readers: dict = {}
+        for i, k in enumerate(ks):
+            for b in k.ins:
+                readers.setdefault(b, []).append(i)
+        side = set()
+        if c.comm_mode == "nccl":
+            side = {i for i, k in enumerate(ks) if k.kind == "coll" and k.data["kind"] != "all_slice"}
+        if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
+            def terminal(i):
+                k = ks[i]
+                return k.kind in ("ew", "reduce") and all(b in results for b in
+                                                          k.data.get("outs_keep", k.outs))
+            for i, k in enumerate(ks):
+                if k.kind != "gemm":
+                    continue
+                rd = [j for b in k.outs for j in readers.get(b, [])]
+                if rd and all(terminal(j) or j in side for j in rd):
+                    side.add(i)
+        return side
+
     def _schedule(self):
         """Two-stream schedule: communicating collectives on stream 1, everything
         else on stream 0; a record waits for the LATEST earlier record on the
@@ -301,9 +333,8 @@ class Executable:
             return out
 
         kin, kout, kstream = [], [], []
-        for k in c.kernels:
-            comm = k.kind == "coll" and k.data["kind"] != "all_slice"
-            kstream.append(1 if comm else 0)
+        for i, k in enumerate(c.kernels):
+            kstream.append(1 if i in self.side else 0)
             r = ivals(k.ins)
             w = ivals(k.outs)
             if k.kind == "reduce":
