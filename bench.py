@@ -50,12 +50,15 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpus):
+    def __init__(self, gpus, active=True):
         self.gpus = gpus
+        self.active = active
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
     def __enter__(self):
+        if not self.active:
+            return self
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         try:
             self.fh = open(self.path, "w")
@@ -228,7 +231,8 @@ def main():
     launches_per_step = sess.launch_count()
 
     e0, e1 = dev.event(), dev.event()
-    with ClockSampler([local] if world == 1 else list(range(world))) as clk:
+    # rank 0 samples every GPU of the job (nvidia-smi sees the whole node)
+    with ClockSampler([local] if world == 1 else list(range(world)), active=(rank == 0)) as clk:
         barrier(dist)
         sess.sync()
         dev.record(e0)

@@ -43,6 +43,16 @@ constexpr int NTHREADS = 320;
 
 SPX_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// One lane of a converged warp (elect.sync).  The whole warp runs the issue
+// loops with warp-uniform operands, so ptxas keeps descriptors in uniform
+// registers; issuing from `if (lane == 0)` instead made it wrap every
+// tcgen05.mma in a waterfall loop (R2UR / ELECT / VOTEU per instruction).
+SPX_DEV bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
+}
+
 SPX_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -236,8 +246,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   const uint32_t tmem_d = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
+    // ---------------- TMA producer (whole warp, one elected lane issues) ----------------
+    {
       const uint32_t bytes = (uint32_t)S::RAW;
       int g = 0;                                  // global k-block counter
       for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
@@ -246,6 +256,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % RS;
           mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
+          if (!elect_one()) {
+            __syncwarp();
+            continue;
+          }
           mbar_expect_tx(&raw_full[s], bytes);
           const int k0 = kb * BK;
           if (args.a_mn_major) {
@@ -262,12 +276,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             for (int c = 0; c < BN / 32; ++c)
               tma_load_3d(b_hi(s) + c * 4096, &tma_b, &raw_full[s], n0 + 32 * c, k0, dev);
           }
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+    {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)args.a_mn_major << 15) |
                              ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
@@ -306,16 +321,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
             const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
             const uint32_t init = (chunk_first && kk == 0) ? 0u : 1u;
-            mma_tf32<1, 1>(dcorr, dah, dbl, idesc, init);   // hi.lo  (A collector fill)
-            mma_tf32<1, 2>(dmain, dah, dbh, idesc, init);   // hi.hi  (A collector reuse)
-            mma_tf32<1, 0>(dcorr, dal, dbh, idesc, 1u);     // lo.hi
+            if (elect_one()) {
+              mma_tf32<1, 1>(dcorr, dah, dbl, idesc, init);   // hi.lo  (A collector fill)
+              mma_tf32<1, 2>(dmain, dah, dbh, idesc, init);   // hi.hi  (A collector reuse)
+              mma_tf32<1, 0>(dcorr, dal, dbh, idesc, 1u);     // lo.hi
+            }
+            __syncwarp();
           }
-          mma_commit<1>(&raw_empty[rs]);
-          mma_commit<1>(&lo_empty[ls]);
-          if (chunk_last) {
-            mma_commit<1>(&tfull[buf]);
-            ++cg;
+          if (elect_one()) {
+            mma_commit<1>(&raw_empty[rs]);
+            mma_commit<1>(&lo_empty[ls]);
+            if (chunk_last) mma_commit<1>(&tfull[buf]);
           }
+          __syncwarp();
+          if (chunk_last) ++cg;
         }
       }
     }
