@@ -93,7 +93,8 @@ typedef struct {
   int32_t monoid;                 /* 0 sum, 1 max                              */
   int32_t n_kept, n_red;          /* x.dims = kept (n_kept dims) ++ reduced      */
   int32_t mode;                   /* 0 ROW / 1 COL (2-D, x.vec = float4 along the
-                                     fast dim), 2 GEN (any rank)               */
+                                     fast dim), 2 GEN (any rank), 3 OUT (few
+                                     reduced elements; 4 outputs per thread)   */
   int64_t kept_dims[SPX_MAX_RANK], kept_stride[SPX_MAX_RANK]; /* in input index space */
   int64_t red_dims[SPX_MAX_RANK], red_stride[SPX_MAX_RANK];
   int64_t n_out, n_red_elems;
@@ -113,7 +114,7 @@ typedef struct {
   int32_t path;                   /* 0 auto, 1 tcgen05 3xTF32, 2 SIMT fp32     */
   int32_t promote;                /* k-blocks per TMEM chunk (0 = default 4)     */
   int32_t reserve_sms;            /* SMs left free for concurrent collectives    */
-  int32_t pad;
+  int32_t splits;                 /* split-K: >1 writes [splits][M][ldc] partials at c_off */
 } spx_gemm_params;
 
 /* ---- collectives over co-located virtual devices ------------------------- */

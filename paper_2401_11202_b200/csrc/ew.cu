@@ -20,17 +20,15 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ spx
   const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
   float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
   const uint32_t nvec = (uint32_t)(p.numel >> 2);
-  const bool two_d = p.rank == 2;
-  const uint32_t cols = (uint32_t)(two_d ? p.dims[1] : p.numel);
+  const int rk = p.rank;
+  const uint32_t cols = (uint32_t)p.dims[rk - 1];     // innermost extent (float4 along it)
   const uint32_t step = gridDim.x * blockDim.x;
   const float* in_base[NIN];
-  uint32_t s0[NIN];
   bool s1[NIN];
 #pragma unroll
   for (int j = 0; j < NIN; ++j) {
     in_base[j] = fb + p.in[j].off;
-    s0[j] = two_d ? (uint32_t)p.in[j].stride[0] : 0u;
-    s1[j] = p.in[j].stride[p.rank - 1] != 0;
+    s1[j] = p.in[j].stride[rk - 1] != 0;
   }
   for (uint32_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += step * U) {
     Vec<4> x[U][NIN];
@@ -39,12 +37,24 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ spx
       const uint32_t v = v0 + u * step;
       if (v >= nvec) break;
       const uint32_t e = v << 2;
-      const uint32_t r = two_d ? e / cols : 0u;
-      const uint32_t c = e - r * cols;
+      uint32_t q = rk > 1 ? e / cols : 0u;            // index over the outer dims
+      const uint32_t c = e - q * cols;
+      int64_t outer[NIN];
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) outer[j] = 0;
+#pragma unroll
+      for (int k = SPX_MAX_RANK - 2; k >= 0; --k) {   // decompose q over dims[0 .. rk-2]
+        if (k > rk - 2) continue;
+        const uint32_t dk = (uint32_t)p.dims[k];
+        const uint32_t ik = k == 0 ? q : q % dk;
+        q = k == 0 ? 0u : q / dk;
+#pragma unroll
+        for (int j = 0; j < NIN; ++j) outer[j] += (int64_t)ik * p.in[j].stride[k];
+      }
 #pragma unroll
       for (int j = 0; j < NIN; ++j) {
         if (j >= p.n_in) break;
-        const float* src = in_base[j] + (size_t)r * s0[j];
+        const float* src = in_base[j] + outer[j];
         if (s1[j]) {
           const float4 t = __ldg(reinterpret_cast<const float4*>(src + c));
           x[u][j].v[0] = t.x; x[u][j].v[1] = t.y; x[u][j].v[2] = t.z; x[u][j].v[3] = t.w;
@@ -120,7 +130,7 @@ int spx_launch_ew(const spx_ew_params& p, cudaStream_t s, int* nlaunch) {
   if (p.numel <= 0 || p.ndev <= 0) return 0;
   if (p.n_prog > SPX_MAX_PROG || p.n_in > SPX_MAX_IN || p.n_out > SPX_MAX_OUT)
     return spx_set_error("ew: program exceeds ABI limits");
-  const bool vec = p.vec && p.numel % 4 == 0 && p.rank <= 2 && p.numel < (int64_t(1) << 31);
+  const bool vec = p.vec && p.numel % 4 == 0 && p.numel < (int64_t(1) << 31);
   if (vec) {
     const int64_t nv = p.numel / 4;
     auto grid_u = [&](int u) { return dim3(blocks_for((nv + u - 1) / u), (unsigned)p.ndev); };

@@ -161,6 +161,7 @@ SPX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 struct TcArgs {
   int M, N, K, a_mn_major, b_k_major, promote;   // promote: k-blocks per TMEM chunk
   int tiles_m, tiles_n, tiles;                   // persistent tile space (x ndev)
+  int splits, units;                             // split-K: units = tiles x splits
   uint64_t c_base;     // device 0 address of C
   int64_t dev_stride;  // bytes
   int64_t ldc;
@@ -179,6 +180,14 @@ struct Cfg {
   static constexpr int BAR_OFF = LO_OFF + LSTAGES * RAW;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // barriers + alignment slack
 };
+
+// Work unit u -> (tile t, split s) and its k-block range [kb0, kb0 + nku).
+SPX_DEV void unit_range(const TcArgs& a, int nk, int u, int& t, int& s, int& kb0, int& nku) {
+  t = u / a.splits;
+  s = u - t * a.splits;
+  kb0 = (int)(((long long)nk * s) / a.splits);
+  nku = (int)(((long long)nk * (s + 1)) / a.splits) - kb0;
+}
 
 SPX_DEV void tile_coords(const TcArgs& a, int t, int& m0, int& n0, int& dev) {
   const int per_dev = a.tiles_m * a.tiles_n;
@@ -212,7 +221,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (args.K + BK - 1) / BK;
   const int P = args.promote;
-  const int nchunks = (nk + P - 1) / P;
 
   auto a_hi = [&](int s) { return smem + s * S::RAW; };
   auto b_hi = [&](int s) { return smem + s * S::RAW + S::A_BYTES; };
@@ -250,10 +258,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     {
       const uint32_t bytes = (uint32_t)S::RAW;
       int g = 0;                                  // global k-block counter
-      for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
-        int m0, n0, dev;
+      for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+        int t, sp, kb0, nku, m0, n0, dev;
+        unit_range(args, nk, u, t, sp, kb0, nku);
         tile_coords(args, t, m0, n0, dev);
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        for (int kb = 0; kb < nku; ++kb, ++g) {
           const int s = g % RS;
           mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
           if (!elect_one()) {
@@ -261,7 +270,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             continue;
           }
           mbar_expect_tx(&raw_full[s], bytes);
-          const int k0 = kb * BK;
+          const int k0 = (kb0 + kb) * BK;
           if (args.a_mn_major) {
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c)
@@ -295,12 +304,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       const uint32_t a_sbo = args.a_mn_major ? 512u : 1024u, b_sbo = args.b_k_major ? 1024u : 512u;
       const uint32_t a_lay = args.a_mn_major ? 1u : 2u, b_lay = args.b_k_major ? 2u : 1u;
       int g = 0, cg = 0;                          // global k-block / chunk counters
-      for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+      for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+        int t, sp, kb0, nku;
+        unit_range(args, nk, u, t, sp, kb0, nku);
+        for (int kb = 0; kb < nku; ++kb, ++g) {
           const int rs = g % RS, ls = g % LS;
           const int buf = cg & 1;
           const bool chunk_first = (kb % P) == 0;
-          const bool chunk_last = (kb % P) == P - 1 || kb == nk - 1;
+          const bool chunk_last = (kb % P) == P - 1 || kb == nku - 1;
           if (chunk_first) {
             mbar_wait(&tempty[buf], ((cg >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -342,8 +353,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     // ---------------- split: lo = x - trunc_tf32(x) ----------------
     const int t0 = threadIdx.x - 64;  // 0..127
     int g = 0;
-    for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb, ++g) {
+    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+      int t, sp, kb0, nku;
+      unit_range(args, nk, u, t, sp, kb0, nku);
+      for (int kb = 0; kb < nku; ++kb, ++g) {
         const int rs = g % RS, ls = g % LS;
         mbar_wait(&raw_full[rs], (g / RS) & 1);
         mbar_wait(&lo_empty[ls], ((g / LS) & 1) ^ 1);
@@ -367,9 +380,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     // ---------------- drain + epilogue ----------------
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     int cg = 0;
-    for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
-      int m0, n0, dev;
+    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+      int t, sp, kb0, nku, m0, n0, dev;
+      unit_range(args, nk, u, t, sp, kb0, nku);
       tile_coords(args, t, m0, n0, dev);
+      const int nchunks = (nku + P - 1) / P;
       float acc[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = 0.f;
@@ -391,8 +406,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       }
       const int row = m0 + q * 32 + lane;
       if (row < args.M) {
+        // split-K partials go to a [splits][M][ldc] workspace (summed by a reduce record)
         float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
-                      (int64_t)row * args.ldc;
+                      ((int64_t)sp * args.M + row) * args.ldc;
 #pragma unroll
         for (int cc = 0; cc < BN / 32; ++cc) {
           const int col0 = n0 + cc * 32;
@@ -485,12 +501,14 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   a_.tiles_m = (p.M + BM - 1) / BM;
   a_.tiles_n = (p.N + BN - 1) / BN;
   a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
+  a_.splits = p.splits > 1 ? p.splits : 1;
+  a_.units = a_.tiles * a_.splits;
   a_.c_base = p.base + (uint64_t)(p.c_off * 4);
   a_.dev_stride = p.dev_stride;
   a_.ldc = p.ldc;
   int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
   if (sms < 1) sms = 1;
-  g->grid = dim3((unsigned)(a_.tiles < sms ? a_.tiles : sms));
+  g->grid = dim3((unsigned)(a_.units < sms ? a_.units : sms));
   *out = g;
   return 0;
 }

@@ -154,6 +154,66 @@ __global__ void __launch_bounds__(256) reduce_gen(const __grid_constant__ spx_re
   if (lane == 0) *out_ptr(p, d, nchunks, c, o) = acc;
 }
 
+// OUT mapping (mode 3): many outputs, few reduced elements (pooling windows,
+// gradients of broadcasts): a thread owns 4 consecutive outputs along the
+// contiguous innermost kept dim and walks the whole reduced range.
+__global__ void __launch_bounds__(256) reduce_out(const __grid_constant__ spx_reduce_params p) {
+  const int d = blockIdx.y;
+  const float* fb = dev_ptr(p.x.base, p.x.dev_stride, d, 0);
+  float* out = dev_ptr(p.x.base, p.x.dev_stride, d, p.out_off);
+  const spx_ew_params& x = p.x;
+  const int nk = p.n_kept;
+  for (int64_t o4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o4 * 4 < p.n_out;
+       o4 += (int64_t)gridDim.x * blockDim.x) {
+    int64_t base[SPX_MAX_IN];
+#pragma unroll
+    for (int j = 0; j < SPX_MAX_IN; ++j) base[j] = x.in[j].off;
+    int64_t rem = o4 * 4;
+#pragma unroll
+    for (int k = SPX_MAX_RANK - 1; k >= 0; --k) {
+      if (k >= nk) continue;
+      const int64_t ik = k == 0 ? rem : rem % x.dims[k];
+      rem = k == 0 ? 0 : rem / x.dims[k];
+#pragma unroll
+      for (int j = 0; j < SPX_MAX_IN; ++j) base[j] += ik * x.in[j].stride[k];
+    }
+    Vec<4> acc;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc.v[q] = ident(p.monoid);
+    for (int64_t r = 0; r < p.n_red_elems; ++r) {
+      RegFile<4> f;
+      int64_t rr = r;
+      int64_t roff[SPX_MAX_IN];
+#pragma unroll
+      for (int j = 0; j < SPX_MAX_IN; ++j) roff[j] = base[j];
+#pragma unroll
+      for (int k = SPX_MAX_RANK - 1; k >= 0; --k) {
+        if (k < nk || k >= x.rank) continue;
+        const int64_t ik = k == nk ? rr : rr % x.dims[k];
+        rr = k == nk ? 0 : rr / x.dims[k];
+#pragma unroll
+        for (int j = 0; j < SPX_MAX_IN; ++j) roff[j] += ik * x.in[j].stride[k];
+      }
+#pragma unroll
+      for (int j = 0; j < SPX_MAX_IN; ++j) {
+        if (j >= x.n_in) break;
+        if (x.in[j].stride[nk - 1] == 1) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(fb + roff[j]));
+          f.r[j].v[0] = t.x; f.r[j].v[1] = t.y; f.r[j].v[2] = t.z; f.r[j].v[3] = t.w;
+        } else {
+          const float t = __ldg(fb + roff[j]);
+          f.r[j].v[0] = t; f.r[j].v[1] = t; f.r[j].v[2] = t; f.r[j].v[3] = t;
+        }
+      }
+      run_program<4>(x.prog, x.imm, x.n_prog, f);
+      const Vec<4> y = f.get(x.out_reg[0]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc.v[q] = fold(p.monoid, acc.v[q], y.v[q]);
+    }
+    *reinterpret_cast<float4*>(out + o4 * 4) = make_float4(acc.v[0], acc.v[1], acc.v[2], acc.v[3]);
+  }
+}
+
 __global__ void reduce_final(const __grid_constant__ spx_reduce_params p, int nchunks) {
   const int d = blockIdx.y;
   const float* part = dev_ptr(p.x.base, p.x.dev_stride, d, p.scratch_off);
@@ -172,6 +232,16 @@ __global__ void reduce_final(const __grid_constant__ spx_reduce_params p, int nc
 int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch) {
   if (p.n_out <= 0 || p.x.ndev <= 0) return 0;
   const int mode = p.mode;
+  if (mode == 3) {
+    int64_t b = (p.n_out / 4 + 255) / 256;
+    const int64_t cap = (int64_t)spx_num_sms() * 16;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    reduce_out<<<dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s>>>(p);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+    return 0;
+  }
   const int W = p.x.vec ? 4 : 1;
   int64_t per_block_out = mode == 1 ? 32 * W : 8;
   const int64_t out_blocks = (p.n_out + per_block_out - 1) / per_block_out;

@@ -411,7 +411,15 @@ class Executable:
         # thread mapping: innermost logical dim reduced -> ROW, kept -> COL
         two_d = len(kd) <= 1 and len(rd) == 1
         innermost_kept = bool(kept) and kept[-1] == len(in_dims) - 1
-        if not two_d:
+        nl = len(prog.leaves)
+        out_vec = (bool(kd) and p.n_out % 4 == 0 and kd[-1] % 4 == 0 and
+                   all(kv[j][-1] in (0, 1) for j in range(nl)) and
+                   all(x.inp[j].off % 4 == 0 and all(st % 4 == 0 for st in list(kv[j][:-1]) + list(rv[j]))
+                       for j in range(nl) if kv[j][-1] == 1))
+        if p.n_red_elems <= 64 and p.n_out >= 4096 and out_vec:
+            p.mode = 3
+            x.vec = 1
+        elif not two_d:
             p.mode = 2
             x.vec = 0
         elif innermost_kept:
@@ -442,6 +450,9 @@ class Executable:
         p.a_mn_major = 1 if at else 0
         p.b_k_major = 1 if bt else 0
         p.path = self.gemm_path
+        p.splits = d.get("splits", 1)
+        if p.splits > 1:
+            p.path = 1                       # split-K partials exist on the tcgen05 path only
         # with collectives overlapped on a side stream, leave SMs for NCCL's CTAs
         p.reserve_sms = self.reserve_sms
         self._records.append((R.K_GEMM, p))

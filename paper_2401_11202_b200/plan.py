@@ -329,10 +329,39 @@ class Compiler:
         out = self._new_buf(dims, "mm")
         M, K = a_dims
         N = b_dims[1]
-        k = Kernel("gemm", [out], {ab, bb}, op_index=i,
-                   data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt)))
-        self.kernels.append(k)
+        splits = self._splitk(M, N, K, aoff, lda, boff, ldb)
+        if splits == 1:
+            k = Kernel("gemm", [out], {ab, bb}, op_index=i,
+                       data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt), splits=1))
+            self.kernels.append(k)
+        else:
+            # split-K: partial products into a [splits, M, N] workspace, summed
+            # in a fixed order by a reduction (deterministic)
+            ws = self._new_buf((splits, M, N), "ws")
+            self.kernels.append(Kernel("gemm", [ws], {ab, bb}, op_index=i,
+                                       data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at),
+                                                 b=(bb, boff, ldb, bt), splits=splits)))
+            root = Leaf(ws, 0, _contig((splits, M, N)))
+            self.kernels.append(Kernel("reduce", [out], {ws}, op_index=i,
+                                       data=dict(root=root, in_dims=(splits, M, N), red=[0],
+                                                 monoid="sum")))
         self.desc[op.results[0]] = Desc("buf", dims, buf=out)
+
+    NUM_SMS = 148
+
+    def _splitk(self, M, N, K, aoff, lda, boff, ldb) -> int:
+        """Split K when the output has too few 128x128 tiles to fill the SMs
+        (weight gradients: K = batch or N*H*W) and the tcgen05 path applies."""
+        tc_ok = (M >= 64 and N >= 32 and K >= 32 and aoff % 4 == 0 and boff % 4 == 0
+                 and lda % 4 == 0 and ldb % 4 == 0)
+        if not tc_ok:
+            return 1
+        tiles = -(-M // 128) * -(-N // 128) * len(self.devices)
+        nk = -(-K // 32)
+        if tiles * 2 > self.NUM_SMS or nk < 16:
+            return 1
+        s = min(nk // 8, -(-self.NUM_SMS // tiles))
+        return max(1, s)
 
     # ----------------------------------------------------------------- reduce
     def _lower_reduce(self, i, op, dims):

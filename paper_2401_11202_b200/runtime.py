@@ -58,7 +58,7 @@ class GemmParams(C.Structure):
                 ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
                 ("a_mn_major", C.c_int32), ("b_k_major", C.c_int32),
                 ("path", C.c_int32), ("promote", C.c_int32), ("reserve_sms", C.c_int32),
-                ("pad", C.c_int32)]
+                ("splits", C.c_int32)]
 
 
 class GatherParams(C.Structure):

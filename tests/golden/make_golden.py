@@ -161,6 +161,11 @@ STEPS = [
      "B:2,M:2,E:2", ["bp", "mp", "z3"], [EMB], 0.1, [0, 1]),
     ("tf2_bpmpz2_B2M2", "transformer", dict(blocks=2, batch=32, d_model=32, d_ff=64), "B:2,M:2",
      ["bp", "mp", "z2"], [], 0.1, [0]),
+    # C4 U-Net analog (tools/unet_model.py): 1x1-conv encoder/decoder with pool,
+    # upsample and skip -- rank-6 reshape/reduce/broadcast in the local program
+    ("unet_bp_B2", "unet", dict(batch=4, height=4, width=4, c0=4, c1=8, c2=8), "B:2", ["bp"], [], 0.25, [0]),
+    ("unet_bpz2_B4", "unet", dict(batch=4, height=4, width=4, c0=4, c1=8, c2=8), "B:4", ["bp", "z2"], [],
+     0.25, [0, 1]),
 ]
 
 
@@ -264,11 +269,16 @@ def main():
             cases.append(case)
 
     # --- C: small training steps with the benchmark configs' structure -----
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(HERE)), "tools"))
+    from unet_model import unet_schedule, unet_train
     for name, model, params, mesh, stages, extra, scale, seeds in STEPS:
-        module = build_model(model, **params)
+        module = unet_train(**params) if model == "unet" else build_model(model, **params)
         module.mesh = Mesh.parse(mesh)
         p = Partitioner(module)
-        for t in cookbook_schedule(model, stages, module):
+        tactics = (unet_schedule(stages, module) if model == "unet"
+                   else cookbook_schedule(model, stages, module))
+        for t in tactics:
             p.apply(t)
         for ax, s in extra:
             p.apply(ManualPartition(ax, dict(s)))

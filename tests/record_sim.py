@@ -111,10 +111,16 @@ class Sim:
                 B = self.gather_view(p, g.b_off, (1, g.ldb), (g.K, g.N))
             else:
                 B = self.gather_view(p, g.b_off, (g.ldb, 1), (g.K, g.N))
-            C = (A.astype(np.float64) @ B.astype(np.float64)).astype(np.float32)
-            for m in range(g.M):
-                s = self.dev_base(p) + g.c_off + m * g.ldc
-                self.arena[s:s + g.N] = C[m]
+            S = max(1, g.splits)
+            for sp in range(S):
+                k0, k1 = (g.K * sp) // S, (g.K * (sp + 1)) // S
+                # partial k-ranges are whole 32-wide k-blocks in the kernel
+                nk = -(-g.K // 32)
+                k0, k1 = min(g.K, 32 * ((nk * sp) // S)), min(g.K, 32 * ((nk * (sp + 1)) // S))
+                C = (A[:, k0:k1].astype(np.float64) @ B[k0:k1].astype(np.float64)).astype(np.float32)
+                for m in range(g.M):
+                    s = self.dev_base(p) + g.c_off + (sp * g.M + m) * g.ldc
+                    self.arena[s:s + g.N] = C[m]
 
     def run_gather(self, g: R.GatherParams):
         dims = [g.dims[k] for k in range(g.rank)]

@@ -81,6 +81,7 @@ def _mm_module(M, K, N, at=False, bt=False):
 GEMM_SHAPES = [
     (128, 128, 128), (256, 512, 384), (1024, 1024, 1024), (2048, 1024, 4096),
     (1024, 2048, 1024), (192, 96, 160), (130, 70, 200), (1024, 128, 1024),
+    (128, 8192, 256), (256, 32768, 64),      # few tiles, long K: split-K partials + reduction
 ]
 
 

@@ -36,6 +36,7 @@ MLP_C1 = dict(hidden_layers=1, batch=256, width=1024)
 
 # name -> (model, params, mesh or None (dense only), cookbook stages, extra tactics)
 EMB = ("E", {"x": 1, "y": 1})   # EMB-analog: shard activations along d_model
+UNET_C4 = dict(batch=128, height=32, width=32, c0=64, c1=256, c2=512)
 
 CONFIGS = {
     # C1: 2-layer MLP (1 hidden layer = 2 linear layers) b=256 d=1024, BP on B:2
@@ -51,6 +52,11 @@ CONFIGS = {
     "c3_tf32_bpz3_B8": ("transformer", TF_C3, "B:8", ["bp", "z3"], []),
     "c3_tf32_bpz3_B4": ("transformer", TF_C3, "B:4", ["bp", "z3"], []),
     "c3_tf32_bpz3_B2": ("transformer", TF_C3, "B:2", ["bp", "z3"], []),
+    # C4: U-Net analog (tools/unet_model.py), BP+Z2 on B:8 (+ B:4, B:2)
+    "c4_unet_dense": ("unet", UNET_C4, None, [], []),
+    "c4_unet_bpz2_B8": ("unet", UNET_C4, "B:8", ["bp", "z2"], []),
+    "c4_unet_bpz2_B4": ("unet", UNET_C4, "B:4", ["bp", "z2"], []),
+    "c4_unet_bpz2_B2": ("unet", UNET_C4, "B:2", ["bp", "z2"], []),
     # C5: transformer 8 blocks d=1024, BP+MP+Z3+EMB on 2x2x2 (+ 2x2, 2)
     "c5_tf8_bpmpz3emb_B2M2E2": ("transformer", TF_C2, "B:2,M:2,E:2", ["bp", "mp", "z3"], [EMB]),
     "c5_tf8_bpmpz3_B2M2": ("transformer", TF_C2, "B:2,M:2", ["bp", "mp", "z3"], []),
@@ -67,7 +73,15 @@ def make(name: str):
     model, params, mesh, stages, extra = CONFIGS[name]
     d = os.path.join(OUT, name)
     os.makedirs(d, exist_ok=True)
-    module = build_model(model, **params)
+    if model == "unet":
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from unet_model import unet_schedule, unet_train
+        build = lambda: unet_train(**params)
+        schedule = lambda names, m: unet_schedule(names, m)
+    else:
+        build = lambda: build_model(model, **params)
+        schedule = lambda names, m: cookbook_schedule(model, names, m)
+    module = build()
     meta = {"name": name, "model": model, "params": params, "mesh": mesh,
             "schedule": stages + [f"manual@{ax}:{json.dumps(s)}" for ax, s in extra]}
     with open(os.path.join(d, "dense.ir"), "w") as fh:
@@ -76,7 +90,7 @@ def make(name: str):
         module.mesh = Mesh.parse(mesh)
         t0 = time.perf_counter()
         p = Partitioner(module)
-        for t in cookbook_schedule(model, stages, module):
+        for t in schedule(stages, module):
             p.apply(t)
         for ax, s in extra:
             p.apply(ManualPartition(ax, dict(s)))
@@ -90,7 +104,7 @@ def make(name: str):
         with open(os.path.join(d, "sharding.json"), "w") as fh:
             json.dump(ex["sharding"], fh)
     from spindle.sim import total_flops
-    meta["model_flops"] = total_flops(build_model(model, **params))
+    meta["model_flops"] = total_flops(build())
     with open(os.path.join(d, "meta.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
     print(f"{name}: done {meta.get('partition_s', 0):.1f}s counts={meta.get('counts')}",
