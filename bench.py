@@ -333,7 +333,7 @@ def main():
                                 "loss D2H each step, host sync per step"},
                 "gpu_launches": int(launches_per_step * args.steps),
                 "launches_per_step": int(launches_per_step),
-                "clocks": clk.summary(), "loss": loss,
+                "clocks": clk.summary(), "loss": loss, "loss_finite": bool(np.isfinite(loss)),
                 "collectives_per_step": counts,
                 "flops_per_device_step": sess.ex.comp.flops}
         print(json.dumps(line), flush=True)
