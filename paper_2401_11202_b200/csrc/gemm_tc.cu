@@ -435,6 +435,294 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Variant with the A operand in TENSOR MEMORY (tcgen05.mma ... [a_tmem] ...).
+// The split warps read each A row from the TMA'd smem tile (any layout, one
+// lane per row = one TMEM lane), write hi(A) and lo(A) into TMEM with
+// tcgen05.st, and only lo(B) goes back to smem: the tensor core then reads
+// just B from shared memory (3 x 4 KB per k-step instead of 5 x 4 KB), the
+// split writes half as many smem bytes.  Per 128x128x32 k-block the smem
+// traffic falls from ~176 KB to ~128 KB (the kernel above is smem-bound).
+// TMEM: [0,256) two chunk accumulators (one chain each), [256, 256+64*LS)
+// the A hi/lo stages.
+// ---------------------------------------------------------------------------
+SPX_DEV void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+SPX_DEV void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+template <int RS_, int LS_>
+struct CfgT {
+  static constexpr int A_BYTES = BM * BK * 4;       // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;       // 16 KB
+  static constexpr int RAW = A_BYTES + B_BYTES;
+  static constexpr int RSTAGES = RS_;
+  static constexpr int LSTAGES = LS_;
+  static constexpr int LO_OFF = RSTAGES * RAW;      // lo(B) ring
+  static constexpr int BAR_OFF = LO_OFF + LSTAGES * B_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int TMEM_A = 2 * BN;             // first A column
+};
+
+template <int RS_, int LS_>
+__global__ void __launch_bounds__(NTHREADS, 1)
+gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     const __grid_constant__ TcArgs args) {
+  using S = CfgT<RS_, LS_>;
+  constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* lo_full = raw_empty + RS;
+  uint64_t* lo_empty = lo_full + LS;
+  uint64_t* tfull = lo_empty + LS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (args.K + BK - 1) / BK;
+  const int P = args.promote;
+
+  auto a_raw = [&](int s) { return smem + s * S::RAW; };
+  auto b_hi = [&](int s) { return smem + s * S::RAW + S::A_BYTES; };
+  auto b_lo = [&](int s) { return smem + S::LO_OFF + s * S::B_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 1);
+    }
+    for (int s = 0; s < LS; ++s) {
+      mbar_init(&lo_full[s], 128);
+      mbar_init(&lo_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_d = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    int g = 0;
+    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+      int t, sp, kb0, nku, m0, n0, dev;
+      unit_range(args, nk, u, t, sp, kb0, nku);
+      tile_coords(args, t, m0, n0, dev);
+      for (int kb = 0; kb < nku; ++kb, ++g) {
+        const int s = g % RS;
+        mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(&raw_full[s], (uint32_t)S::RAW);
+          const int k0 = (kb0 + kb) * BK;
+          if (args.a_mn_major) {
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c)
+              tma_load_3d(a_raw(s) + c * 4096, &tma_a, &raw_full[s], m0 + 32 * c, k0, dev);
+          } else {
+            tma_load_3d(a_raw(s), &tma_a, &raw_full[s], k0, m0, dev);
+          }
+          if (args.b_k_major) {
+            tma_load_3d(b_hi(s), &tma_b, &raw_full[s], k0, n0, dev);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c)
+              tma_load_3d(b_hi(s) + c * 4096, &tma_b, &raw_full[s], n0 + 32 * c, k0, dev);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) |
+                           ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
+    const uint32_t b_sbo = args.b_k_major ? 1024u : 512u;
+    const uint32_t b_lay = args.b_k_major ? 2u : 1u;
+    int g = 0, cg = 0;
+    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+      int t, sp, kb0, nku;
+      unit_range(args, nk, u, t, sp, kb0, nku);
+      for (int kb = 0; kb < nku; ++kb, ++g) {
+        const int rs = g % RS, ls = g % LS;
+        const int buf = cg & 1;
+        const bool chunk_first = (kb % P) == 0;
+        const bool chunk_last = (kb % P) == P - 1 || kb == nku - 1;
+        if (chunk_first) {
+          mbar_wait(&tempty[buf], ((cg >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        mbar_wait(&lo_full[ls], (g / LS) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bhi = smem_u32(b_hi(rs)), blo = smem_u32(b_lo(ls));
+        const uint32_t dacc = tmem_d + (uint32_t)(buf * BN);
+        const uint32_t ahi = tmem_d + (uint32_t)(S::TMEM_A + ls * 64), alo = ahi + 32;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
+          const uint32_t init = (chunk_first && kk == 0) ? 0u : 1u;
+          if (elect_one()) {
+            mma_tf32_ts(dacc, ahi + kk * 8, dbl, idesc, init);   // hi.lo
+            mma_tf32_ts(dacc, alo + kk * 8, dbh, idesc, 1u);     // lo.hi
+            mma_tf32_ts(dacc, ahi + kk * 8, dbh, idesc, 1u);     // hi.hi
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          mma_commit<1>(&raw_empty[rs]);
+          mma_commit<1>(&lo_empty[ls]);
+          if (chunk_last) mma_commit<1>(&tfull[buf]);
+        }
+        __syncwarp();
+        if (chunk_last) ++cg;
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- split: A rows -> TMEM (hi, lo); lo(B) -> smem ----------------
+    const int q = warp & 3;                       // TMEM lane quadrant = A rows 32q..32q+31
+    const int row = q * 32 + lane;
+    const int t0 = threadIdx.x - 64;              // 0..127 for the B part
+    int g = 0;
+    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+      int t, sp, kb0, nku;
+      unit_range(args, nk, u, t, sp, kb0, nku);
+      for (int kb = 0; kb < nku; ++kb, ++g) {
+        const int rs = g % RS, ls = g % LS;
+        mbar_wait(&raw_full[rs], (g / RS) & 1);
+        mbar_wait(&lo_empty[ls], ((g / LS) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // A row `row`: 32 consecutive k values
+        uint32_t hi[32], lo[32];
+        const float* abase = reinterpret_cast<const float*>(a_raw(rs));
+        if (args.a_mn_major) {
+          // [mchunk][k][32 m], 32B-granule swizzle: granule g' = g ^ (k & 3)
+          const int mc = row >> 5, mm = row & 31;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const int gran = (mm >> 3) ^ (k & 3);
+            const float x = abase[mc * 1024 + k * 32 + gran * 8 + (mm & 7)];
+            hi[k] = __float_as_uint(x);
+          }
+        } else {
+          // [m][32 k], 16B-chunk swizzle: chunk c' = c ^ (m & 7)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 x = *reinterpret_cast<const float4*>(abase + row * 32 + ((c ^ (row & 7)) << 2));
+            hi[4 * c] = __float_as_uint(x.x); hi[4 * c + 1] = __float_as_uint(x.y);
+            hi[4 * c + 2] = __float_as_uint(x.z); hi[4 * c + 3] = __float_as_uint(x.w);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float x = __uint_as_float(hi[k]);
+          lo[k] = __float_as_uint(x - __uint_as_float(hi[k] & 0xFFFFE000u));
+        }
+        const uint32_t ta = tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(S::TMEM_A + ls * 64);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        // lo(B) into smem (same swizzled layout as the raw tile)
+        const float4* src = reinterpret_cast<const float4*>(b_hi(rs));
+        float4* dst = reinterpret_cast<float4*>(b_lo(ls));
+#pragma unroll 4
+        for (int i = t0; i < S::B_BYTES / 16; i += 128) {
+          const float4 x = src[i];
+          dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                               x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
+                               x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
+                               x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&lo_full[ls]);
+      }
+    }
+  } else {
+    // ---------------- drain + epilogue ----------------
+    const int q = warp & 3;
+    int cg = 0;
+    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+      int t, sp, kb0, nku, m0, n0, dev;
+      unit_range(args, nk, u, t, sp, kb0, nku);
+      tile_coords(args, t, m0, n0, dev);
+      const int nchunks = (nku + P - 1) / P;
+      float acc[BN];
+#pragma unroll
+      for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+      for (int c = 0; c < nchunks; ++c, ++cg) {
+        const int buf = cg & 1;
+        mbar_wait(&tfull[buf], (cg >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + cc * 32), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __fadd_rn(acc[cc * 32 + j], __uint_as_float(v[j]));
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&tempty[buf]);
+      }
+      const int row = m0 + q * 32 + lane;
+      if (row < args.M) {
+        float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
+                      ((int64_t)sp * args.M + row) * args.ldc;
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          const int col0 = n0 + cc * 32;
+          if (col0 + 32 <= args.N && (args.ldc & 3) == 0) {
+            float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              dst[j] = make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
+                                   acc[cc * 32 + 4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < args.N) crow[col0 + j] = acc[cc * 32 + j];
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_d));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -525,13 +813,34 @@ static int launch_cfg(const SpxGemmTC* g, cudaStream_t s) {
   return 0;
 }
 
+template <int RS_, int LS_>
+static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    SPX_CUDA(cudaFuncSetAttribute(gemm_tc_tmema_kernel<RS_, LS_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CfgT<RS_, LS_>::TOTAL));
+    attr = true;
+  }
+  gemm_tc_tmema_kernel<RS_, LS_><<<g->grid, NTHREADS, CfgT<RS_, LS_>::TOTAL, s>>>(g->ma, g->mb, g->args);
+  return 0;
+}
+
 int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
-  static int pipe = -1;
+  static int pipe = -1, tmema = -1;
   if (pipe < 0) {
     const char* e = getenv("SPX_GEMM_PIPE");
     pipe = e ? atoi(e) : 43;
+    const char* t = getenv("SPX_GEMM_TMEMA");
+    tmema = t ? atoi(t) : 1;
   }
   int rc;
+  if (tmema) {
+    rc = launch_tmema<5, 3>(g, s);
+    if (rc) return rc;
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+    return 0;
+  }
   switch (pipe) {
     case 52: rc = launch_cfg<5, 2>(g, s); break;
     case 33: rc = launch_cfg<3, 3>(g, s); break;
