@@ -785,7 +785,7 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   TcArgs& a_ = g->args;
   a_.M = p.M; a_.N = p.N; a_.K = p.K;
   a_.a_mn_major = p.a_mn_major; a_.b_k_major = p.b_k_major;
-  a_.promote = p.promote > 0 ? p.promote : 4;
+  { const char* e = getenv("SPX_GEMM_PROMOTE"); a_.promote = p.promote > 0 ? p.promote : (e ? atoi(e) : 4); }
   a_.tiles_m = (p.M + BM - 1) / BM;
   a_.tiles_n = (p.N + BN - 1) / BN;
   a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
@@ -835,7 +835,12 @@ int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
   }
   int rc;
   if (tmema) {
-    rc = launch_tmema<5, 3>(g, s);
+    switch (pipe) {
+      case 44: rc = launch_tmema<4, 4>(g, s); break;
+      case 62: rc = launch_tmema<6, 2>(g, s); break;
+      case 34: rc = launch_tmema<3, 4>(g, s); break;
+      default: rc = launch_tmema<5, 3>(g, s);
+    }
     if (rc) return rc;
     SPX_CHECK_LAUNCH();
     if (nlaunch) ++*nlaunch;
