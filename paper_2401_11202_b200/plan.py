@@ -360,7 +360,7 @@ class Compiler:
         nk = -(-K // 32)
         # only for very few tiles: moderate cases (e.g. 64 tiles of 1024x1024
         # weight gradients) run better unsplit, concurrently on the side stream
-        if tiles * 4 > self.NUM_SMS or nk < 16:
+        if tiles * 8 > self.NUM_SMS or nk < 16:
             return 1
         s = min(nk // 8, -(-self.NUM_SMS // tiles))
         return max(1, s)
