@@ -301,19 +301,29 @@ class Executable:
         for i, k in enumerate(ks):
             for b in k.ins:
                 readers.setdefault(b, []).append(i)
+        def terminal(i):
+            k = ks[i]
+            return k.kind in ("ew", "reduce") and all(b in results for b in
+                                                      k.data.get("outs_keep", k.outs))
+
+        def off_critical(i, side):
+            rd = [j for b in ks[i].outs for j in readers.get(b, [])]
+            return bool(rd) and all(terminal(j) or j in side for j in rd)
+
         side = set()
+        crit_coll = os.environ.get("SPX_SIDE_ALL_COLLECTIVES", "0") == "1"
         if c.comm_mode == "nccl":
-            side = {i for i, k in enumerate(ks) if k.kind == "coll" and k.data["kind"] != "all_slice"}
-        if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
-            def terminal(i):
+            # collectives feeding only the parameter update (gradient reductions)
+            # overlap on the side stream; activation collectives on the critical
+            # path stay on the main stream (a cross-stream hop only adds latency)
+            for i in reversed(range(len(ks))):
                 k = ks[i]
-                return k.kind in ("ew", "reduce") and all(b in results for b in
-                                                          k.data.get("outs_keep", k.outs))
-            for i, k in enumerate(ks):
-                if k.kind != "gemm":
-                    continue
-                rd = [j for b in k.outs for j in readers.get(b, [])]
-                if rd and all(terminal(j) or j in side for j in rd):
+                if k.kind == "coll" and k.data["kind"] != "all_slice":
+                    if crit_coll or off_critical(i, side):
+                        side.add(i)
+        if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
+            for i in reversed(range(len(ks))):
+                if ks[i].kind == "gemm" and off_critical(i, side):
                     side.add(i)
         return side
 
