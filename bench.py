@@ -290,7 +290,7 @@ def main():
     cls_ms = {}
     for (kind, p), t in zip(recs, rec_ms):
         name = {R.K_EW: "elementwise", R.K_REDUCE: "reduce", R.K_GEMM: "gemm", R.K_GATHER: "relayout",
-                R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl"}[kind]
+                R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl", R.K_PEER: "peer_allreduce"}[kind]
         cls_ms[name] = cls_ms.get(name, 0.0) + float(t)
         if kind == R.K_GEMM:
             gemm_flops += 2.0 * p.M * p.N * p.K * p.ndev

@@ -155,9 +155,20 @@ typedef struct {
   int64_t count;                   /* elements: per-rank send count (AG/A2A chunk), recv count (RS), total (AR) */
 } spx_nccl_params;
 
+/* ---- all-reduce over NVLink peer memory (CUDA IPC-mapped arenas) -------- */
+typedef struct {
+  int32_t kind, n, me, monoid;     /* kind 0 = all-reduce; n members; me = my index */
+  int64_t count;                   /* elements */
+  uint64_t src[8];                 /* members' input buffers, mapped into this process */
+  uint64_t dst;                    /* local output */
+  uint64_t flags[8];               /* members' flag regions (mapped); [slot][phase][8] u32 */
+  uint64_t counter;                /* local epoch counters, u32 per slot */
+  int32_t slot, pad;
+} spx_peer_params;
+
 /* ---- plan records --------------------------------------------------------- */
 enum spx_kind { SPX_K_EW = 1, SPX_K_REDUCE = 2, SPX_K_GEMM = 3, SPX_K_GATHER = 4,
-                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6 };
+                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6, SPX_K_PEER = 7 };
 
 /* library / device */
 const char* spx_last_error(void);
@@ -174,6 +185,11 @@ int spx_host_free(void* ptr);
 int spx_stream_create(uint64_t* out_stream);
 int spx_stream_sync(uint64_t stream);
 int spx_stream_destroy(uint64_t stream);
+
+/* CUDA IPC: map another process's arena (peer collectives) */
+int spx_ipc_get_handle(uint64_t ptr, uint8_t out_handle[64]);
+int spx_ipc_open(const uint8_t handle[64], uint64_t* out_ptr);
+int spx_ipc_close(uint64_t ptr);
 
 /* NCCL (dlopen'd; the same libnccl torch uses) */
 int spx_nccl_get_unique_id(uint8_t out_id[128]);

@@ -154,6 +154,7 @@ static int run_record(Record& r, cudaStream_t s, int* nl) {
       if (r.path == 1) return spx_gemm_tc_launch(r.tc, s, nl);
       return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
     case SPX_K_NCCL: return run_nccl(*reinterpret_cast<const spx_nccl_params*>(r.params.data()), s);
+    case SPX_K_PEER: return spx_launch_peer(*reinterpret_cast<const spx_peer_params*>(r.params.data()), s, nl);
   }
   return spx_set_error("unknown record kind %d", r.kind);
 }
@@ -166,6 +167,7 @@ static size_t params_size(int kind) {
     case SPX_K_GATHER: return sizeof(spx_gather_params);
     case SPX_K_CREDUCE: return sizeof(spx_creduce_params);
     case SPX_K_NCCL: return sizeof(spx_nccl_params);
+    case SPX_K_PEER: return sizeof(spx_peer_params);
   }
   return 0;
 }
@@ -231,6 +233,25 @@ int spx_stream_sync(uint64_t stream) {
 }
 int spx_stream_destroy(uint64_t stream) {
   SPX_CUDA(cudaStreamDestroy(reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int spx_ipc_get_handle(uint64_t ptr, uint8_t out_handle[64]) {
+  cudaIpcMemHandle_t h;
+  SPX_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(ptr)));
+  memcpy(out_handle, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+  return 0;
+}
+int spx_ipc_open(const uint8_t handle[64], uint64_t* out_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h) < 64 ? sizeof(h) : 64);
+  void* p = nullptr;
+  SPX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *out_ptr = reinterpret_cast<uint64_t>(p);
+  return 0;
+}
+int spx_ipc_close(uint64_t ptr) {
+  SPX_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<void*>(ptr)));
   return 0;
 }
 

@@ -61,6 +61,12 @@ class Executable:
         self.side = self._side_kernels() if overlap else set()
         self.overlap = bool(self.side)
         self.reserve_sms = int(os.environ.get("SPX_RESERVE_SMS", "0")) if self.overlap else 0
+        # NCCL mode: critical-path all-reduces as one-shot NVLink peer-memory
+        # reductions (csrc/peer.cu) once the factory maps the peers' arenas
+        self.wants_peer = comm_mode == "nccl" and os.environ.get("SPX_PEER", "1") != "0"
+        self.peer_max_bytes = int(os.environ.get("SPX_PEER_MAX_BYTES", str(64 << 20)))
+        self.peer_bases = None          # [arena base of rank r, mapped here]
+        self._peer_handles = []
         self._layout()
         self._alloc()
         if comm_mode == "nccl" and comm_factory is not None:
@@ -183,6 +189,12 @@ class Executable:
         self.stage_a = hi
         self.stage_b = hi + self.stage_elems
         hi += 2 * self.stage_elems
+        # peer collectives: flag words [comm key][phase][member] (written by the
+        # peers through their mapping of this arena) and local epoch counters
+        nkeys = len(self.comm_keys()) if c.comm_mode == "nccl" else 0
+        self.flag_off = hi
+        self.flag_elems = _align(nkeys * 16 + nkeys) if nkeys else 0
+        hi += self.flag_elems
         self.off = off
         self.slice_elems = _align(hi, 1 << 18)           # 1 MiB granularity per device
         self.peak_bytes = hi * 4
@@ -192,6 +204,8 @@ class Executable:
         self.base = self.DRY_BASE if self.dry else self.device.malloc(self.dev_stride * self.ndev)
         if self.zero_elems and not self.dry:
             self.device.memset(self.base + self.zero_off * 4, self.zero_elems * 4, 0)
+        if self.flag_elems and not self.dry:
+            self.device.memset(self.base + self.flag_off * 4, self.flag_elems * 4, 0)
 
     def addr(self, p: int, buf: str, extra: int = 0) -> int:
         return self.base + p * self.dev_stride + (self.off[buf] + extra) * 4
@@ -218,7 +232,7 @@ class Executable:
             self.device.sync()
         for kind, p in self._records:
             for fld in ("src_table", "base_off", "dst", "src", "members"):
-                if hasattr(p, fld) and getattr(p, fld) >= (1 << 62):
+                if hasattr(p, fld) and isinstance(getattr(p, fld), int) and getattr(p, fld) >= (1 << 62):
                     setattr(p, fld, addrs[getattr(p, fld) - (1 << 62)])
 
     def _tref(self, arr) -> int:
@@ -265,8 +279,9 @@ class Executable:
 
     def _emit(self):
         c = self.comp
-        for k in c.kernels:
+        for i, k in enumerate(c.kernels):
             first = len(self._records)
+            self._cur = i
             self._emit_one(k)
             self._krange.append((first, len(self._records)))
 
@@ -615,7 +630,20 @@ class Executable:
         n = len(grp)
         monoid = 0 if attrs.get("monoid", "sum") == "sum" else 1
         if kind == "all_reduce":
-            self._nccl(R.NCCL_ALLREDUCE, comm, src_a, out_a, _prod(in_dims), monoid)
+            count = _prod(in_dims)
+            if (self.peer_bases is not None and self._cur not in self.side and 1 < n <= 8
+                    and count * 4 <= self.peer_max_bytes):
+                slot = self.comm_keys().index(key)
+                p = R.PeerParams()
+                p.kind, p.n, p.me, p.monoid, p.count, p.slot = 0, n, grp.index(me), monoid, count, slot
+                for j, r in enumerate(grp):
+                    p.src[j] = self.peer_bases[r] + (src_a - self.base)
+                    p.flags[j] = self.peer_bases[r] + self.flag_off * 4
+                p.dst = out_a
+                p.counter = self.base + (self.flag_off + len(self.comm_keys()) * 16) * 4
+                self._records.append((R.K_PEER, p))
+                return
+            self._nccl(R.NCCL_ALLREDUCE, comm, src_a, out_a, count, monoid)
             return
         if kind == "all_gather":
             apd = attrs["axes_per_dim"]
@@ -700,5 +728,8 @@ class Executable:
         if self.dry:
             return
         self.plan.destroy()
+        for ptr in self._peer_handles:
+            R.call(R.load().spx_ipc_close, ptr)
+        self._peer_handles = []
         self.device.free(self.base)
         self.device.free(self.table_base)

@@ -80,7 +80,16 @@ class NcclParams(C.Structure):
                 ("send", C.c_uint64), ("recv", C.c_uint64), ("count", C.c_int64)]
 
 
-PARAMS = {K_EW: EwParams, K_REDUCE: ReduceParams, K_GEMM: GemmParams,
+class PeerParams(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("me", C.c_int32), ("monoid", C.c_int32),
+                ("count", C.c_int64), ("src", C.c_uint64 * 8), ("dst", C.c_uint64),
+                ("flags", C.c_uint64 * 8), ("counter", C.c_uint64), ("slot", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+K_PEER = 7
+
+PARAMS = {K_PEER: PeerParams, K_EW: EwParams, K_REDUCE: ReduceParams, K_GEMM: GemmParams,
           K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams}
 
 EXPORTS = [
@@ -91,6 +100,7 @@ EXPORTS = [
     "spx_plan_replay", "spx_plan_launch_count", "spx_plan_destroy", "spx_plan_record_info",
     "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
     "spx_plan_profile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
+    "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
 ]
 
 _lib = None
@@ -135,6 +145,8 @@ def load(build_if_missing: bool = True):
         "spx_comm_destroy": [C.c_int], "spx_device_init": [C.c_int], "spx_params_size": [C.c_int],
         "spx_host_alloc": [C.c_uint64, C.POINTER(C.c_void_p)], "spx_host_free": [C.c_void_p],
         "spx_plan_set_sched": [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int],
+        "spx_ipc_get_handle": [C.c_uint64, C.c_void_p], "spx_ipc_open": [C.c_void_p, C.POINTER(C.c_uint64)],
+        "spx_ipc_close": [C.c_uint64],
     }
     for name, args in sigs.items():
         getattr(lib, name).argtypes = args

@@ -34,17 +34,54 @@ def nccl_comm_init(uid: bytes, nranks: int, rank: int) -> int:
     return out.value
 
 
+def ipc_handle(ptr: int) -> bytes:
+    lib = R.load()
+    buf = (R.C.c_uint8 * 64)()
+    R.call(lib.spx_ipc_get_handle, ptr, R.C.cast(buf, R.C.c_void_p))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    lib = R.load()
+    buf = (R.C.c_uint8 * 64).from_buffer_copy(handle)
+    out = R.C.c_uint64()
+    R.call(lib.spx_ipc_open, R.C.cast(buf, R.C.c_void_p), R.C.byref(out))
+    return out.value
+
+
+def map_peer_arenas(ex: Executable, rank: int, allgather):
+    """Exchange CUDA IPC handles of every rank's arena (`allgather(obj) ->
+    [obj per rank]`) and map the peers' arenas into this process; enables the
+    peer-memory all-reduce records (csrc/peer.cu).  The arena's flag words are
+    zeroed (and synchronised) before any handle is published."""
+    ex.device.sync()
+    handles = allgather(ipc_handle(ex.base))
+    bases = []
+    for r, h in enumerate(handles):
+        if r == rank:
+            bases.append(ex.base)
+        else:
+            ptr = ipc_open(h)
+            ex._peer_handles.append(ptr)
+            bases.append(ptr)
+    ex.peer_bases = bases
+
+
 def comm_plan(ex: Executable):
     """[(axes key, groups)] in the shared deterministic order."""
     c = ex.comp
     return [(key, c._groups(list(key))) for key in ex.comm_keys()]
 
 
-def make_nccl_comms(ex: Executable, rank: int, broadcast, get_uid=nccl_uid, init=nccl_comm_init):
+def make_nccl_comms(ex: Executable, rank: int, broadcast, get_uid=nccl_uid, init=nccl_comm_init,
+                    allgather=None):
     """One communicator per axes key; NCCL rank = position in the group's
     device order (the reference's group order, spmd_interp.py:57-63).
-    `broadcast(obj) -> obj` shares rank 0's unique ids with every rank."""
+    `broadcast(obj) -> obj` shares rank 0's unique ids with every rank;
+    with `allgather`, the peers' arenas are also mapped (map_peer_arenas)."""
     plan = comm_plan(ex)
+    if allgather is not None and ex.wants_peer and plan:
+        map_peer_arenas(ex, rank, allgather)
     uids = None
     if rank == 0:
         uids = {(key, gi): get_uid() for key, groups in plan for gi in range(len(groups))}
@@ -57,6 +94,13 @@ def make_nccl_comms(ex: Executable, rank: int, broadcast, get_uid=nccl_uid, init
     return comms
 
 
+def torch_allgather(obj):
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
 def torch_broadcast(obj):
     import torch.distributed as dist
     box = [obj]
@@ -67,7 +111,7 @@ def torch_broadcast(obj):
 class Session:
     def __init__(self, module, sharding=None, *, mode="local", device: R.Device | None = None,
                  rank: int = 0, world: int = 1, local_rank: int = 0, gemm_path: int = 0,
-                 func: str = "main", broadcast=torch_broadcast):
+                 func: str = "main", broadcast=torch_broadcast, allgather=torch_allgather):
         self.module = module
         self.sharding = sharding
         self.mode = mode
@@ -93,7 +137,8 @@ class Session:
             self.device = device or R.Device(local_rank)
             self.ex = Executable(module, func, device=self.device, devices=[rank], comm_mode="nccl",
                                  gemm_path=gemm_path,
-                                 comm_factory=lambda ex: make_nccl_comms(ex, rank, broadcast))
+                                 comm_factory=lambda ex: make_nccl_comms(ex, rank, broadcast,
+                                                                         allgather=allgather))
             self.hosted = [rank]
         self.rank = rank
 

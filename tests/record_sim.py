@@ -218,7 +218,15 @@ def sim_dense(module, inputs):
     return [r[0] for r in sim.results()], ex
 
 
-def sim_nccl(module, spec, inputs, tol=1e-5):
+def _dry_comms(ex, peer):
+    if peer:
+        # every dry arena has base DRY_BASE: a peer address decodes to the same
+        # offset in that member's simulated arena
+        ex.peer_bases = [ex.base] * ex.comp.mesh.device_count
+    return {k: i for i, k in enumerate(ex.comm_keys())}
+
+
+def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
     """The one-process-per-GPU (NCCL) lowering, simulated: one dry Executable
     per rank, records executed in lockstep, NCCL records combined across the
     ranks of each communicator group (rank order = group order)."""
@@ -231,11 +239,11 @@ def sim_nccl(module, spec, inputs, tol=1e-5):
     world = len(coords)
     exs, sims = [], []
     probe = Executable(module, devices=[0], comm_mode="nccl", dry=True,
-                       comm_factory=lambda ex: {k: i for i, k in enumerate(ex.comm_keys())})
+                       comm_factory=lambda ex: _dry_comms(ex, False))
     plan = comm_plan(probe)
     for r in range(world):
         ex = Executable(module, devices=[r], comm_mode="nccl", dry=True,
-                        comm_factory=lambda ex: {k: i for i, k in enumerate(ex.comm_keys())})
+                        comm_factory=lambda ex: _dry_comms(ex, peer))
         exs.append(ex)
         s = Sim(ex)
         a = {n: np.asarray(inputs[n])[_chunk_slices(np.shape(inputs[n]), spec.args[n], mesh, coords[r])]
@@ -246,6 +254,24 @@ def sim_nccl(module, spec, inputs, tol=1e-5):
     assert all(len(e.records()) == nrec for e in exs)
     for i in range(nrec):
         kind = exs[0].records()[i][0]
+        if kind == R.K_PEER:
+            # each member reads every member's source (same arena offset) and
+            # folds in member order; all reads happen before any write
+            outs = []
+            for r in range(world):
+                p = exs[r].records()[i][1]
+                grp = plan[[k for k, _ in plan].index(exs[r].comm_keys()[p.slot])][1]
+                grp = next(g for g in grp if r in g)
+                assert grp.index(r) == p.me and len(grp) == p.n
+                acc = None
+                for j, m in enumerate(grp):
+                    o = sims[m].idx(p.src[j])
+                    x = sims[m].arena[o:o + p.count]
+                    acc = x.copy() if acc is None else (np.add(acc, x) if p.monoid == 0 else np.maximum(acc, x))
+                outs.append((r, sims[r].idx(p.dst), acc))
+            for r, d0, acc in outs:
+                sims[r].arena[d0:d0 + acc.size] = acc
+            continue
         if kind != R.K_NCCL:
             for s, e in zip(sims, exs):
                 k, p = e.records()[i]

@@ -16,8 +16,9 @@ from record_sim import sim_nccl
 CASES = [c for c in golden_cases() if "local_ir" in c]
 
 
+@pytest.mark.parametrize("peer", [False, True], ids=["nccl", "peer"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: c["key"])
-def test_nccl_mode_matches_reference(case):
+def test_nccl_mode_matches_reference(case, peer):
     m = parse_module(case["local_ir"])
     spec = ShardingSpec.from_json(case["sharding"])
     base = parse_module(case["dense_ir"]) if "dense_ir" in case else m
@@ -25,12 +26,35 @@ def test_nccl_mode_matches_reference(case):
     ins = case_inputs(case, base, s)
     if case.get("error") == "DivergenceError":
         with pytest.raises(DivergenceError):
-            sim_nccl(m, spec, ins)
+            sim_nccl(m, spec, ins, peer=peer)
         return
-    got, exs = sim_nccl(m, spec, ins)
+    got, exs = sim_nccl(m, spec, ins, peer=peer)
     assert exs[0].comp.counts == case["counts"]
     for g, w in zip(got, case_expected(case, s, "spmd")):
         assert relative_error(g, w) < TOL
+    if peer:
+        # the peer all-reduce folds in member order like the reference's
+        # _combine: bit-identical to the NCCL-semantics simulation
+        ref, _ = sim_nccl(m, spec, ins, peer=False)
+        for g, w in zip(got, ref):
+            np.testing.assert_array_equal(g, w)
+
+
+def test_peer_records_replace_critical_path_all_reduces():
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.executable import Executable
+    from record_sim import _dry_comms
+    case = next(c for c in CASES if c["key"] == "step_tf2_bpmp_B2M2")
+    m = parse_module(case["local_ir"])
+    ex = Executable(m, devices=[0], comm_mode="nccl", dry=True, comm_factory=lambda e: _dry_comms(e, True))
+    kinds = [k for k, _ in ex.records()]
+    assert R.K_PEER in kinds
+    nkeys = len(ex.comm_keys())
+    for k, p in ex.records():
+        if k == R.K_PEER:
+            assert p.n == 2 and 0 <= p.slot < nkeys and p.kind == 0
+            assert p.flags[0] == ex.base + ex.flag_off * 4
+            assert p.counter == ex.base + (ex.flag_off + 16 * nkeys) * 4
 
 
 def _worker(rank, world, port, q):

@@ -1,0 +1,18 @@
+"""One line per bench log: tag, n, config, samples/s, ms/step, e2e, per-class ms."""
+import json
+import sys
+
+for path in sys.argv[1:]:
+    line = None
+    for l in open(path):
+        l = l.strip()
+        if l.startswith("{") and '"metric"' in l:
+            line = json.loads(l)
+    if line is None:
+        print(path, "NO RESULT")
+        continue
+    r = line.get("roofline", {})
+    print(path.split("/")[-1], line["n_gpus"], line["config"].get("program"), round(line["value"]),
+          round(line["ms_per_step"], 3), "e2e", round(line.get("e2e", {}).get("value", 0)),
+          r.get("step_ms_by_class"), "frac", round(r.get("frac", 0) or 0, 3),
+          "clk", line.get("clocks", {}).get("sm_mhz"), line.get("clocks", {}).get("reasons"))
