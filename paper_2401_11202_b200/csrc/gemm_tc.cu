@@ -40,6 +40,7 @@ constexpr int BM = 128;             // rows per CTA
 constexpr int BN = 128;             // output columns per CTA (= per pair)
 constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
 constexpr int NTHREADS = 320;
+constexpr int NTHREADS_T = 512;   // TMEM-A kernel: 4 warpgroups
 
 SPX_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -63,35 +64,45 @@ SPX_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 SPX_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+template <bool CLUSTER>
+SPX_DEV bool mbar_try(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  if (CLUSTER) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+  return done != 0;
+}
 // Bounded wait: a protocol bug traps (the error surfaces to the host) instead
-// of hanging the GPU.  CLUSTER = acquire at cluster scope (peer arrivals).
+// of hanging the GPU.  The bound check sits behind a first try_wait so the fast path (the
+// phase already complete, or completing within one hardware-suspended
+// try_wait) is two instructions in the issuing warp's loop.
+template <bool CLUSTER>
+SPX_DEV void mbar_wait_slow(uint32_t a, uint32_t parity) {
+  const long long t0 = clock64();
+  for (int it = 1;; ++it) {
+    if (mbar_try<CLUSTER>(a, parity)) return;
+    if ((it & 1023) == 0 && clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+// CLUSTER = acquire at cluster scope (peer arrivals).
 template <bool CLUSTER = false>
 SPX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  uint32_t done = 0;
-  long long t0 = 0;
-  for (int it = 0;; ++it) {
-    if (CLUSTER) {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(a), "r"(parity)
-          : "memory");
-    } else {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(a), "r"(parity)
-          : "memory");
-    }
-    if (done) return;
-    if (it == 64) t0 = clock64();
-    if (it > 64 && (it & 1023) == 0 && clock64() - t0 > 20000000000LL) __trap();
-  }
+  if (!mbar_try<CLUSTER>(a, parity)) mbar_wait_slow<CLUSTER>(a, parity);
 }
 
 SPX_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
@@ -479,13 +490,15 @@ struct CfgT {
 };
 
 template <int RS_, int LS_>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS_T, 1)
 gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ TcArgs args) {
   using S = CfgT<RS_, LS_>;
   constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned base kept as __shared__ pointer arithmetic, so the split
+  // warps' accesses compile to LDS/STS rather than generic loads
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* raw_empty = raw_full + RS;
   uint64_t* lo_full = raw_empty + RS;
@@ -528,6 +541,16 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_d = *tmem_slot;
 
+  // Warpgroup roles (setmaxnreg moves registers to the drain warpgroup, whose
+  // fp32 promotion accumulators hold a 32 x 128 tile slice per warp):
+  //   WG0  warp 0 TMA producer, warp 1 MMA issuer, warps 2-3 idle   (56 regs)
+  //   WG1, WG2  split, alternating k-blocks (g & 1)                 (120 regs)
+  //   WG3  drain + epilogue                                         (216 regs)
+  // One split warpgroup per k-block left the tensor core waiting on the
+  // split ~1/3 of the time; two alternating groups give each 2 k-blocks of
+  // MMA time per k-block of split work.
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     int g = 0;
@@ -561,61 +584,70 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // One warp issues for the whole CTA, so its per-k-block instruction count
+    // bounds the tensor core: everything except the waits is precomputed or
+    // advanced incrementally (stage/phase counters, descriptors as base +
+    // offset -- the address field is the low 14 bits of the descriptor, and
+    // every smem address here is < 256 KB, so adding never carries out).
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) |
                            ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
     const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
     const uint32_t b_sbo = args.b_k_major ? 1024u : 512u;
     const uint32_t b_lay = args.b_k_major ? 2u : 1u;
-    int g = 0, cg = 0;
+    const uint64_t dbh0 = smem_desc(smem_u32(b_hi(0)), b_lbo, b_sbo, b_lay);
+    const uint64_t dbl0 = smem_desc(smem_u32(b_lo(0)), b_lbo, b_sbo, b_lay);
+    const uint64_t dkk = b_step >> 4;
+    int rs = 0, ls = 0, cg = 0;
+    uint32_t lph = 0;
     for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
       int t, sp, kb0, nku;
       unit_range(args, nk, u, t, sp, kb0, nku);
-      for (int kb = 0; kb < nku; ++kb, ++g) {
-        const int rs = g % RS, ls = g % LS;
+      int kin = 0;                                  // k-block index inside the chunk
+      for (int kb = 0; kb < nku; ++kb) {
         const int buf = cg & 1;
-        const bool chunk_first = (kb % P) == 0;
-        const bool chunk_last = (kb % P) == P - 1 || kb == nku - 1;
-        if (chunk_first) {
+        const bool chunk_last = kin == P - 1 || kb == nku - 1;
+        if (kin == 0) {
           mbar_wait(&tempty[buf], ((cg >> 1) & 1) ^ 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
-        mbar_wait(&lo_full[ls], (g / LS) & 1);
+        mbar_wait(&lo_full[ls], lph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t bhi = smem_u32(b_hi(rs)), blo = smem_u32(b_lo(ls));
+        const uint64_t dbh = dbh0 + (uint64_t)(rs * (S::RAW >> 4));
+        const uint64_t dbl = dbl0 + (uint64_t)(ls * (S::B_BYTES >> 4));
         const uint32_t dacc = tmem_d + (uint32_t)(buf * BN);
         const uint32_t ahi = tmem_d + (uint32_t)(S::TMEM_A + ls * 64), alo = ahi + 32;
-#pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
-          const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
-          const uint32_t init = (chunk_first && kk == 0) ? 0u : 1u;
-          if (elect_one()) {
-            mma_tf32_ts(dacc, ahi + kk * 8, dbl, idesc, init);   // hi.lo
-            mma_tf32_ts(dacc, alo + kk * 8, dbh, idesc, 1u);     // lo.hi
-            mma_tf32_ts(dacc, ahi + kk * 8, dbh, idesc, 1u);     // hi.hi
-          }
-          __syncwarp();
-        }
+        const uint32_t init = kin == 0 ? 0u : 1u;
         if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            mma_tf32_ts(dacc, ahi + kk * 8, dbl + kk * dkk, idesc, kk == 0 ? init : 1u);   // hi.lo
+            mma_tf32_ts(dacc, alo + kk * 8, dbh + kk * dkk, idesc, 1u);                    // lo.hi
+            mma_tf32_ts(dacc, ahi + kk * 8, dbh + kk * dkk, idesc, 1u);                    // hi.hi
+          }
           mma_commit<1>(&raw_empty[rs]);
           mma_commit<1>(&lo_empty[ls]);
           if (chunk_last) mma_commit<1>(&tfull[buf]);
         }
         __syncwarp();
-        if (chunk_last) ++cg;
+        if (++rs == RS) rs = 0;
+        if (++ls == LS) { ls = 0; lph ^= 1u; }
+        if (chunk_last) { kin = 0; ++cg; } else { ++kin; }
       }
     }
-  } else if (warp < 6) {
+  }
+  } else if (warp < 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
     // ---------------- split: A rows -> TMEM (hi, lo); lo(B) -> smem ----------------
     const int q = warp & 3;                       // TMEM lane quadrant = A rows 32q..32q+31
     const int row = q * 32 + lane;
-    const int t0 = threadIdx.x - 64;              // 0..127 for the B part
+    const int grp = (warp - 4) >> 2;              // k-blocks g with (g & 1) == grp
+    const int t0 = (threadIdx.x - 128) & 127;     // 0..127 for the B part
     int g = 0;
     for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
       int t, sp, kb0, nku;
       unit_range(args, nk, u, t, sp, kb0, nku);
       for (int kb = 0; kb < nku; ++kb, ++g) {
+        if ((g & 1) != grp) continue;
         const int rs = g % RS, ls = g % LS;
         mbar_wait(&raw_full[rs], (g / RS) & 1);
         mbar_wait(&lo_empty[ls], ((g / LS) & 1) ^ 1);
@@ -668,6 +700,7 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     }
   } else {
     // ---------------- drain + epilogue ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
     const int q = warp & 3;
     int cg = 0;
     for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
@@ -821,7 +854,7 @@ static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
                                   CfgT<RS_, LS_>::TOTAL));
     attr = true;
   }
-  gemm_tc_tmema_kernel<RS_, LS_><<<g->grid, NTHREADS, CfgT<RS_, LS_>::TOTAL, s>>>(g->ma, g->mb, g->args);
+  gemm_tc_tmema_kernel<RS_, LS_><<<g->grid, NTHREADS_T, CfgT<RS_, LS_>::TOTAL, s>>>(g->ma, g->mb, g->args);
   return 0;
 }
 

@@ -8,8 +8,11 @@ from paper_2401_11202_b200 import runtime as R
 dev = R.Device(0)
 rng = np.random.default_rng(0)
 print("SPX_GEMM_PIPE", os.environ.get("SPX_GEMM_PIPE"))
-for (M, N, K, at, bt) in [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
-                          (1024, 1024, 2048, True, False), (4096, 4096, 4096, False, False)]:
+SHAPES = [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
+          (1024, 1024, 2048, True, False), (4096, 4096, 4096, False, False)]
+if os.environ.get("SHAPES"):
+    SHAPES = [SHAPES[int(i)] for i in os.environ["SHAPES"].split(",")]
+for (M, N, K, at, bt) in SHAPES:
     A = rng.standard_normal((K, M) if at else (M, K)).astype(np.float32)
     B = rng.standard_normal((N, K) if bt else (K, N)).astype(np.float32)
     g = G(dev, A, B, at, bt)
