@@ -121,25 +121,6 @@ SPX_DEV uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t l
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 
-// collector: 0 none, 1 fill A, 2 last use of A
-template <int CG, int COLLECT>
-SPX_DEV void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-#define SPX_MMA(GRP, SUFFIX)                                                                   \
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                               \
-               "tcgen05.mma.cta_group::" GRP ".kind::tf32" SUFFIX " [%0], %1, %2, %3, p;\n\t}" \
-               ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc))
-  if (CG == 1) {
-    if (COLLECT == 1) SPX_MMA("1", ".collector::a::fill");
-    else if (COLLECT == 2) SPX_MMA("1", ".collector::a::lastuse");
-    else SPX_MMA("1", "");
-  } else {
-    if (COLLECT == 1) SPX_MMA("2", ".collector::a::fill");
-    else if (COLLECT == 2) SPX_MMA("2", ".collector::a::lastuse");
-    else SPX_MMA("2", "");
-  }
-#undef SPX_MMA
-}
-
 // MMA completion -> barrier (CG=2: the barrier at the same offset in both CTAs).
 template <int CG>
 SPX_DEV void mma_commit(uint64_t* bar) {
@@ -178,19 +159,6 @@ struct TcArgs {
   int64_t ldc;
 };
 
-template <int RS_, int LS_>
-struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 4;       // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;       // 16 KB
-  static constexpr int RAW = A_BYTES + B_BYTES;     // one TMA stage (= the hi operands)
-  // Raw ring (TMA destination) and lo ring (split output) are separate so the
-  // producer runs RSTAGES k-blocks ahead of the tensor core.
-  static constexpr int RSTAGES = RS_;
-  static constexpr int LSTAGES = LS_;
-  static constexpr int LO_OFF = RSTAGES * RAW;
-  static constexpr int BAR_OFF = LO_OFF + LSTAGES * RAW;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // barriers + alignment slack
-};
 
 // Work unit u -> (tile t, split s) and its k-block range [kb0, kb0 + nku).
 SPX_DEV void unit_range(const TcArgs& a, int nk, int u, int& t, int& s, int& kb0, int& nku) {
@@ -200,250 +168,13 @@ SPX_DEV void unit_range(const TcArgs& a, int nk, int u, int& t, int& s, int& kb0
   nku = (int)(((long long)nk * (s + 1)) / a.splits) - kb0;
 }
 
-SPX_DEV void tile_coords(const TcArgs& a, int t, int& m0, int& n0, int& dev) {
+SPX_DEV void tile_coords(const TcArgs& a, int t, int& m0, int& n0, int& dev, int bm = BM) {
   const int per_dev = a.tiles_m * a.tiles_n;
   dev = t / per_dev;
   const int r = t - dev * per_dev;
   const int n_blk = r / a.tiles_m;            // M fastest: concurrent CTAs share B panels
-  m0 = (r - n_blk * a.tiles_m) * BM;
+  m0 = (r - n_blk * a.tiles_m) * bm;
   n0 = n_blk * BN;
-}
-
-// Persistent: one CTA per SM walks tiles t = blockIdx.x, += gridDim.x.  The
-// k-block stream and the TMEM chunk stream run continuously across tiles, so
-// there is no per-tile pipeline fill, TMEM allocation or barrier set-up, and
-// a tile's epilogue stores overlap the next tile's main loop.
-template <int RS_, int LS_>
-__global__ void __launch_bounds__(NTHREADS, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-               const __grid_constant__ TcArgs args) {
-  using S = Cfg<RS_, LS_>;
-  constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-  uint64_t* raw_empty = raw_full + RS;
-  uint64_t* lo_full = raw_empty + RS;   // split done
-  uint64_t* lo_empty = lo_full + LS;
-  uint64_t* tfull = lo_empty + LS;      // [2] chunk accumulated (MMA commit)
-  uint64_t* tempty = tfull + 2;         // [2] chunk drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (args.K + BK - 1) / BK;
-  const int P = args.promote;
-
-  auto a_hi = [&](int s) { return smem + s * S::RAW; };
-  auto b_hi = [&](int s) { return smem + s * S::RAW + S::A_BYTES; };
-  auto a_lo = [&](int s) { return smem + S::LO_OFF + s * S::RAW; };
-  auto b_lo = [&](int s) { return smem + S::LO_OFF + s * S::RAW + S::A_BYTES; };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < RS; ++s) {
-      mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], 1);
-    }
-    for (int s = 0; s < LS; ++s) {
-      mbar_init(&lo_full[s], 128);
-      mbar_init(&lo_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_d = *tmem_slot;
-
-  if (warp == 0) {
-    // ---------------- TMA producer (whole warp, one elected lane issues) ----------------
-    {
-      const uint32_t bytes = (uint32_t)S::RAW;
-      int g = 0;                                  // global k-block counter
-      for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
-        int t, sp, kb0, nku, m0, n0, dev;
-        unit_range(args, nk, u, t, sp, kb0, nku);
-        tile_coords(args, t, m0, n0, dev);
-        for (int kb = 0; kb < nku; ++kb, ++g) {
-          const int s = g % RS;
-          mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
-          if (!elect_one()) {
-            __syncwarp();
-            continue;
-          }
-          mbar_expect_tx(&raw_full[s], bytes);
-          const int k0 = (kb0 + kb) * BK;
-          if (args.a_mn_major) {
-#pragma unroll
-            for (int c = 0; c < BM / 32; ++c)
-              tma_load_3d(a_hi(s) + c * 4096, &tma_a, &raw_full[s], m0 + 32 * c, k0, dev);
-          } else {
-            tma_load_3d(a_hi(s), &tma_a, &raw_full[s], k0, m0, dev);
-          }
-          if (args.b_k_major) {
-            tma_load_3d(b_hi(s), &tma_b, &raw_full[s], k0, n0, dev);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-              tma_load_3d(b_hi(s) + c * 4096, &tma_b, &raw_full[s], n0 + 32 * c, k0, dev);
-          }
-          __syncwarp();
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
-    {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)args.a_mn_major << 15) |
-                             ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(BM >> 4) << 24);
-      // K-major (SW128, 16B atoms): LBO unused, SBO = 8 rows x 128B; a k-step of
-      //   8 fp32 advances the start address by 32B inside the swizzle row.
-      // MN-major (SW128_BASE32B): LBO = stride of 32-element MN chunks (32 k-rows
-      //   x 128B), SBO = 4 k-rows x 128B; a k-step (8 rows) advances 1024B.
-      const uint32_t a_lbo = args.a_mn_major ? 4096u : 16u, a_step = args.a_mn_major ? 1024u : 32u;
-      const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
-      const uint32_t a_sbo = args.a_mn_major ? 512u : 1024u, b_sbo = args.b_k_major ? 1024u : 512u;
-      const uint32_t a_lay = args.a_mn_major ? 1u : 2u, b_lay = args.b_k_major ? 2u : 1u;
-      int g = 0, cg = 0;                          // global k-block / chunk counters
-      for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
-        int t, sp, kb0, nku;
-        unit_range(args, nk, u, t, sp, kb0, nku);
-        for (int kb = 0; kb < nku; ++kb, ++g) {
-          const int rs = g % RS, ls = g % LS;
-          const int buf = cg & 1;
-          const bool chunk_first = (kb % P) == 0;
-          const bool chunk_last = (kb % P) == P - 1 || kb == nku - 1;
-          if (chunk_first) {
-            mbar_wait(&tempty[buf], ((cg >> 1) & 1) ^ 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          }
-          mbar_wait(&lo_full[ls], (g / LS) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ahi = smem_u32(a_hi(rs)), alo = smem_u32(a_lo(ls));
-          const uint32_t bhi = smem_u32(b_hi(rs)), blo = smem_u32(b_lo(ls));
-          // two independent accumulation chains per chunk: main (hi.hi) and corr
-          // (hi.lo + lo.hi).  Measured: MMAs into ONE accumulator serialise on it
-          // (N=128 tf32 MMAs ran at ~1/3 of peak); alternating chains doubles the rate.
-          const uint32_t dmain = tmem_d + (uint32_t)(buf * 2 * BN);
-          const uint32_t dcorr = dmain + (uint32_t)BN;
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t dah = smem_desc(ahi + kk * a_step, a_lbo, a_sbo, a_lay);
-            const uint64_t dal = smem_desc(alo + kk * a_step, a_lbo, a_sbo, a_lay);
-            const uint64_t dbh = smem_desc(bhi + kk * b_step, b_lbo, b_sbo, b_lay);
-            const uint64_t dbl = smem_desc(blo + kk * b_step, b_lbo, b_sbo, b_lay);
-            const uint32_t init = (chunk_first && kk == 0) ? 0u : 1u;
-            if (elect_one()) {
-              mma_tf32<1, 1>(dcorr, dah, dbl, idesc, init);   // hi.lo  (A collector fill)
-              mma_tf32<1, 2>(dmain, dah, dbh, idesc, init);   // hi.hi  (A collector reuse)
-              mma_tf32<1, 0>(dcorr, dal, dbh, idesc, 1u);     // lo.hi
-            }
-            __syncwarp();
-          }
-          if (elect_one()) {
-            mma_commit<1>(&raw_empty[rs]);
-            mma_commit<1>(&lo_empty[ls]);
-            if (chunk_last) mma_commit<1>(&tfull[buf]);
-          }
-          __syncwarp();
-          if (chunk_last) ++cg;
-        }
-      }
-    }
-  } else if (warp < 6) {
-    // ---------------- split: lo = x - trunc_tf32(x) ----------------
-    const int t0 = threadIdx.x - 64;  // 0..127
-    int g = 0;
-    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
-      int t, sp, kb0, nku;
-      unit_range(args, nk, u, t, sp, kb0, nku);
-      for (int kb = 0; kb < nku; ++kb, ++g) {
-        const int rs = g % RS, ls = g % LS;
-        mbar_wait(&raw_full[rs], (g / RS) & 1);
-        mbar_wait(&lo_empty[ls], ((g / LS) & 1) ^ 1);
-        {
-          const float4* src = reinterpret_cast<const float4*>(a_hi(rs));
-          float4* dst = reinterpret_cast<float4*>(a_lo(ls));
-#pragma unroll 4
-          for (int i = t0; i < S::RAW / 16; i += 128) {
-            const float4 x = src[i];
-            dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
-                                 x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
-                                 x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
-                                 x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&lo_full[ls]);
-      }
-    }
-  } else {
-    // ---------------- drain + epilogue ----------------
-    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
-    int cg = 0;
-    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
-      int t, sp, kb0, nku, m0, n0, dev;
-      unit_range(args, nk, u, t, sp, kb0, nku);
-      tile_coords(args, t, m0, n0, dev);
-      const int nchunks = (nku + P - 1) / P;
-      float acc[BN];
-#pragma unroll
-      for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-      for (int c = 0; c < nchunks; ++c, ++cg) {
-        const int buf = cg & 1;
-        mbar_wait(&tfull[buf], (cg >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-        for (int cc = 0; cc < 2 * BN / 32; ++cc) {     // main columns, then corr columns
-          uint32_t v[32];
-          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 2 * BN + cc * 32), v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            acc[(cc % (BN / 32)) * 32 + j] = __fadd_rn(acc[(cc % (BN / 32)) * 32 + j], __uint_as_float(v[j]));
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&tempty[buf]);
-      }
-      const int row = m0 + q * 32 + lane;
-      if (row < args.M) {
-        // split-K partials go to a [splits][M][ldc] workspace (summed by a reduce record)
-        float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
-                      ((int64_t)sp * args.M + row) * args.ldc;
-#pragma unroll
-        for (int cc = 0; cc < BN / 32; ++cc) {
-          const int col0 = n0 + cc * 32;
-          if (col0 + 32 <= args.N && (args.ldc & 3) == 0) {
-            float4* dst = reinterpret_cast<float4*>(crow + col0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              dst[j] = make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
-                                   acc[cc * 32 + 4 * j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < args.N) crow[col0 + j] = acc[cc * 32 + j];
-          }
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_d));
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -469,17 +200,26 @@ SPX_DEV void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
       : "memory");
 }
 
+template <int CG>
 SPX_DEV void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+  if (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
 
-template <int RS_, int LS_>
+template <int RS_, int LS_, int CG_ = 1>
 struct CfgT {
+  static constexpr int CG = CG_;                    // CTAs per tile (tcgen05 cta_group)
+  static constexpr int BNH = BN / CG;               // B rows (output columns) this CTA holds
   static constexpr int A_BYTES = BM * BK * 4;       // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;       // 16 KB
+  static constexpr int B_BYTES = BNH * BK * 4;      // 16 KB (8 KB per CTA of a pair)
   static constexpr int RAW = A_BYTES + B_BYTES;
   static constexpr int RSTAGES = RS_;
   static constexpr int LSTAGES = LS_;
@@ -489,11 +229,11 @@ struct CfgT {
   static constexpr int TMEM_A = 2 * BN;             // first A column
 };
 
-template <int RS_, int LS_>
+template <int RS_, int LS_, int CG>
 __global__ void __launch_bounds__(NTHREADS_T, 1)
 gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ TcArgs args) {
-  using S = CfgT<RS_, LS_>;
+  using S = CfgT<RS_, LS_, CG>;
   constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned base kept as __shared__ pointer arithmetic, so the split
@@ -509,6 +249,26 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (args.K + BK - 1) / BK;
+  // CG == 2: a cluster of two CTAs computes one 256 x 128 tile with
+  // tcgen05.mma.cta_group::2 issued by rank 0.  Each CTA holds its own 128 A
+  // rows (TMEM) and half of the B tile (64 output columns, smem), and drains
+  // its own 128 x 128 accumulator.  Per SM this halves the tensor core's B
+  // reads from shared memory and a quarter of the L2->SM traffic.
+  uint32_t crank = 0;
+  if (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int pair0 = blockIdx.x / CG, npairs = gridDim.x / CG;
+  // arrive on rank 0's copy of a barrier (the MMA issuer's)
+  auto arrive_leader = [&](uint64_t* bar) {
+    if (CG == 1) {
+      mbar_arrive(bar);
+    } else {
+      uint32_t r;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(bar)));
+      // default semantics (as CUTLASS's ClusterBarrier::arrive): an explicit
+      // .release.cluster costs ~1000 cycles of the issuing warp
+      asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+    }
+  };
   const int P = args.promote;
 
   auto a_raw = [&](int s) { return smem + s * S::RAW; };
@@ -521,43 +281,51 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
       mbar_init(&raw_empty[s], 1);
     }
     for (int s = 0; s < LS; ++s) {
-      mbar_init(&lo_full[s], 128);
+      mbar_init(&lo_full[s], 4 * CG);             // one elected lane per split warp
       mbar_init(&lo_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 4 * CG);              // one elected lane per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CG == 1) __syncthreads();
+  else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_d = *tmem_slot;
 
   // Warpgroup roles (setmaxnreg moves registers to the drain warpgroup, whose
   // fp32 promotion accumulators hold a 32 x 128 tile slice per warp):
-  //   WG0  warp 0 TMA producer, warp 1 MMA issuer, warps 2-3 idle   (56 regs)
-  //   WG1, WG2  split, alternating k-blocks (g & 1)                 (120 regs)
-  //   WG3  drain + epilogue                                         (216 regs)
+  //   WG0  warp 0 TMA producer, warp 1 MMA issuer, warps 2-3 idle   (64 regs)
+  //   WG1, WG2  split, alternating k-blocks (g & 1)                 (112 regs)
+  //   WG3  drain + epilogue                                         (224 regs)
   // One split warpgroup per k-block left the tensor core waiting on the
   // split ~1/3 of the time; two alternating groups give each 2 k-blocks of
   // MMA time per k-block of split work.
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     int g = 0;
-    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+    for (int u = pair0; u < args.units; u += npairs) {
       int t, sp, kb0, nku, m0, n0, dev;
       unit_range(args, nk, u, t, sp, kb0, nku);
-      tile_coords(args, t, m0, n0, dev);
+      tile_coords(args, t, m0, n0, dev, BM * CG);
+      m0 += (int)crank * BM;
+      const int nb0 = n0 + (int)crank * S::BNH;
       for (int kb = 0; kb < nku; ++kb, ++g) {
         const int s = g % RS;
         mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
@@ -572,17 +340,17 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
             tma_load_3d(a_raw(s), &tma_a, &raw_full[s], k0, m0, dev);
           }
           if (args.b_k_major) {
-            tma_load_3d(b_hi(s), &tma_b, &raw_full[s], k0, n0, dev);
+            tma_load_3d(b_hi(s), &tma_b, &raw_full[s], k0, nb0, dev);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-              tma_load_3d(b_hi(s) + c * 4096, &tma_b, &raw_full[s], n0 + 32 * c, k0, dev);
+            for (int c = 0; c < S::BNH / 32; ++c)
+              tma_load_3d(b_hi(s) + c * 4096, &tma_b, &raw_full[s], nb0 + 32 * c, k0, dev);
           }
         }
         __syncwarp();
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && crank == 0) {
     // ---------------- MMA issuer ----------------
     // One warp issues for the whole CTA, so its per-k-block instruction count
     // bounds the tensor core: everything except the waits is precomputed or
@@ -591,7 +359,7 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     // every smem address here is < 256 KB, so adding never carries out).
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) |
                            ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)((BM * CG) >> 4) << 24);
     const uint32_t b_lbo = args.b_k_major ? 16u : 4096u, b_step = args.b_k_major ? 32u : 1024u;
     const uint32_t b_sbo = args.b_k_major ? 1024u : 512u;
     const uint32_t b_lay = args.b_k_major ? 2u : 1u;
@@ -600,7 +368,7 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     const uint64_t dkk = b_step >> 4;
     int rs = 0, ls = 0, cg = 0;
     uint32_t lph = 0;
-    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+    for (int u = pair0; u < args.units; u += npairs) {
       int t, sp, kb0, nku;
       unit_range(args, nk, u, t, sp, kb0, nku);
       int kin = 0;                                  // k-block index inside the chunk
@@ -608,9 +376,9 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
         const int buf = cg & 1;
         const bool chunk_last = kin == P - 1 || kb == nku - 1;
         if (kin == 0) {
-          mbar_wait(&tempty[buf], ((cg >> 1) & 1) ^ 1);
+          mbar_wait<CG == 2>(&tempty[buf], ((cg >> 1) & 1) ^ 1);
         }
-        mbar_wait(&lo_full[ls], lph);
+        mbar_wait<CG == 2>(&lo_full[ls], lph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint64_t dbh = dbh0 + (uint64_t)(rs * (S::RAW >> 4));
         const uint64_t dbl = dbl0 + (uint64_t)(ls * (S::B_BYTES >> 4));
@@ -620,13 +388,13 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            mma_tf32_ts(dacc, ahi + kk * 8, dbl + kk * dkk, idesc, kk == 0 ? init : 1u);   // hi.lo
-            mma_tf32_ts(dacc, alo + kk * 8, dbh + kk * dkk, idesc, 1u);                    // lo.hi
-            mma_tf32_ts(dacc, ahi + kk * 8, dbh + kk * dkk, idesc, 1u);                    // hi.hi
+            mma_tf32_ts<CG>(dacc, ahi + kk * 8, dbl + kk * dkk, idesc, kk == 0 ? init : 1u);   // hi.lo
+            mma_tf32_ts<CG>(dacc, alo + kk * 8, dbh + kk * dkk, idesc, 1u);                    // lo.hi
+            mma_tf32_ts<CG>(dacc, ahi + kk * 8, dbh + kk * dkk, idesc, 1u);                    // hi.hi
           }
-          mma_commit<1>(&raw_empty[rs]);
-          mma_commit<1>(&lo_empty[ls]);
-          if (chunk_last) mma_commit<1>(&tfull[buf]);
+          mma_commit<CG>(&raw_empty[rs]);                 // CG == 2: both CTAs' barriers
+          mma_commit<CG>(&lo_empty[ls]);
+          if (chunk_last) mma_commit<CG>(&tfull[buf]);
         }
         __syncwarp();
         if (++rs == RS) rs = 0;
@@ -636,14 +404,14 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     }
   }
   } else if (warp < 12) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 112;");
     // ---------------- split: A rows -> TMEM (hi, lo); lo(B) -> smem ----------------
     const int q = warp & 3;                       // TMEM lane quadrant = A rows 32q..32q+31
     const int row = q * 32 + lane;
     const int grp = (warp - 4) >> 2;              // k-blocks g with (g & 1) == grp
     const int t0 = (threadIdx.x - 128) & 127;     // 0..127 for the B part
     int g = 0;
-    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+    for (int u = pair0; u < args.units; u += npairs) {
       int t, sp, kb0, nku;
       unit_range(args, nk, u, t, sp, kb0, nku);
       for (int kb = 0; kb < nku; ++kb, ++g) {
@@ -695,18 +463,20 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&lo_full[ls]);
+        __syncwarp();
+        if (lane == 0) arrive_leader(&lo_full[ls]);
       }
     }
   } else {
     // ---------------- drain + epilogue ----------------
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     const int q = warp & 3;
     int cg = 0;
-    for (int u = blockIdx.x; u < args.units; u += gridDim.x) {
+    for (int u = pair0; u < args.units; u += npairs) {
       int t, sp, kb0, nku, m0, n0, dev;
       unit_range(args, nk, u, t, sp, kb0, nku);
-      tile_coords(args, t, m0, n0, dev);
+      tile_coords(args, t, m0, n0, dev, BM * CG);
+      m0 += (int)crank * BM;
       const int nchunks = (nku + P - 1) / P;
       float acc[BN];
 #pragma unroll
@@ -724,7 +494,8 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
           for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __fadd_rn(acc[cc * 32 + j], __uint_as_float(v[j]));
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&tempty[buf]);
+        __syncwarp();
+        if (lane == 0) arrive_leader(&tempty[buf]);
       }
       const int row = m0 + q * 32 + lane;
       if (row < args.M) {
@@ -749,10 +520,14 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  // CG == 2: neither CTA leaves while its peer may still arrive on its barriers
+  // or the pair's MMAs may still read its shared memory / TMEM
+  if (CG == 1) __syncthreads();
+  else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_d));
+    if (CG == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_d));
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_d));
   }
 }
 
@@ -793,6 +568,7 @@ struct SpxGemmTC {
   CUtensorMap ma, mb;
   TcArgs args;
   dim3 grid;
+  int cg;              // CTAs per tile (1, or 2 = cluster pair with cta_group::2 MMAs)
   spx_gemm_params p;
 };
 
@@ -807,19 +583,21 @@ bool spx_gemm_tc_supported(const spx_gemm_params& p) {
 int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   SpxGemmTC* g = new SpxGemmTC();
   g->p = p;
+  { const char* e = getenv("SPX_GEMM_CG"); g->cg = e ? atoi(e) : 2; }
+  if (g->cg != 1) g->cg = 2;
   const uint64_t a = p.base + (uint64_t)(p.a_off * 4), b = p.base + (uint64_t)(p.b_off * 4);
   int rc;
   if (p.a_mn_major) rc = make_map(&g->ma, a, p.M, p.K, p.ndev, p.lda * 4, p.dev_stride, 32, true);
   else rc = make_map(&g->ma, a, p.K, p.M, p.ndev, p.lda * 4, p.dev_stride, BM, false);
   if (rc) { delete g; return rc; }
-  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, BN, false);
+  if (p.b_k_major) rc = make_map(&g->mb, b, p.K, p.N, p.ndev, p.ldb * 4, p.dev_stride, BN / g->cg, false);
   else rc = make_map(&g->mb, b, p.N, p.K, p.ndev, p.ldb * 4, p.dev_stride, 32, true);
   if (rc) { delete g; return rc; }
   TcArgs& a_ = g->args;
   a_.M = p.M; a_.N = p.N; a_.K = p.K;
   a_.a_mn_major = p.a_mn_major; a_.b_k_major = p.b_k_major;
   { const char* e = getenv("SPX_GEMM_PROMOTE"); a_.promote = p.promote > 0 ? p.promote : (e ? atoi(e) : 4); }
-  a_.tiles_m = (p.M + BM - 1) / BM;
+  a_.tiles_m = (p.M + BM * g->cg - 1) / (BM * g->cg);
   a_.tiles_n = (p.N + BN - 1) / BN;
   a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
   a_.splits = p.splits > 1 ? p.splits : 1;
@@ -828,63 +606,60 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   a_.dev_stride = p.dev_stride;
   a_.ldc = p.ldc;
   int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
-  if (sms < 1) sms = 1;
-  g->grid = dim3((unsigned)(a_.units < sms ? a_.units : sms));
+  sms -= sms % g->cg;
+  if (sms < g->cg) sms = g->cg;
+  const int want = a_.units * g->cg;
+  g->grid = dim3((unsigned)(want < sms ? want : sms));
   *out = g;
   return 0;
 }
 
-template <int RS_, int LS_>
-static int launch_cfg(const SpxGemmTC* g, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    SPX_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<RS_, LS_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg<RS_, LS_>::TOTAL));
-    attr = true;
-  }
-  gemm_tc_kernel<RS_, LS_><<<g->grid, NTHREADS, Cfg<RS_, LS_>::TOTAL, s>>>(g->ma, g->mb, g->args);
-  return 0;
-}
-
-template <int RS_, int LS_>
+template <int RS_, int LS_, int CG>
 static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
   static bool attr = false;
+  auto kern = gemm_tc_tmema_kernel<RS_, LS_, CG>;
   if (!attr) {
-    SPX_CUDA(cudaFuncSetAttribute(gemm_tc_tmema_kernel<RS_, LS_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  CfgT<RS_, LS_>::TOTAL));
+    SPX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgT<RS_, LS_, CG>::TOTAL));
     attr = true;
   }
-  gemm_tc_tmema_kernel<RS_, LS_><<<g->grid, NTHREADS_T, CfgT<RS_, LS_>::TOTAL, s>>>(g->ma, g->mb, g->args);
+  if (CG == 1) {
+    kern<<<g->grid, NTHREADS_T, CfgT<RS_, LS_, CG>::TOTAL, s>>>(g->ma, g->mb, g->args);
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g->grid;
+  cfg.blockDim = dim3(NTHREADS_T);
+  cfg.dynamicSmemBytes = CfgT<RS_, LS_, CG>::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SPX_CUDA(cudaLaunchKernelEx(&cfg, kern, g->ma, g->mb, g->args));
   return 0;
 }
 
 int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
-  static int pipe = -1, tmema = -1;
+  static int pipe = -1;
   if (pipe < 0) {
     const char* e = getenv("SPX_GEMM_PIPE");
-    pipe = e ? atoi(e) : 43;
-    const char* t = getenv("SPX_GEMM_TMEMA");
-    tmema = t ? atoi(t) : 1;
+    pipe = e ? atoi(e) : 0;
   }
   int rc;
-  if (tmema) {
+  if (g->cg == 2) {
     switch (pipe) {
-      case 44: rc = launch_tmema<4, 4>(g, s); break;
-      case 62: rc = launch_tmema<6, 2>(g, s); break;
-      case 34: rc = launch_tmema<3, 4>(g, s); break;
-      default: rc = launch_tmema<5, 3>(g, s);
+      case 84: rc = launch_tmema<8, 4, 2>(g, s); break;
+      case 53: rc = launch_tmema<5, 3, 2>(g, s); break;
+      default: rc = launch_tmema<6, 4, 2>(g, s);
     }
-    if (rc) return rc;
-    SPX_CHECK_LAUNCH();
-    if (nlaunch) ++*nlaunch;
-    return 0;
-  }
-  switch (pipe) {
-    case 52: rc = launch_cfg<5, 2>(g, s); break;
-    case 33: rc = launch_cfg<3, 3>(g, s); break;
-    case 34: rc = launch_cfg<3, 4>(g, s); break;
-    case 24: rc = launch_cfg<2, 4>(g, s); break;
-    default: rc = launch_cfg<4, 3>(g, s);
+  } else {
+    switch (pipe) {
+      case 44: rc = launch_tmema<4, 4, 1>(g, s); break;
+      default: rc = launch_tmema<5, 3, 1>(g, s);
+    }
   }
   if (rc) return rc;
   SPX_CHECK_LAUNCH();
