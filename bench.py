@@ -31,6 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+TF32_MMA_PEAK = 1112.0   # TF/s, profiles/r01_mma_bench.txt
 METRIC = "Partitioned fwd+bwd samples/s at 1/2/4/8 B200; % of tensor-core/HBM roofline"
 
 
@@ -296,15 +297,19 @@ def main():
             gemm_flops += 2.0 * p.M * p.N * p.K * p.ndev
             gemm_ms += float(t)
     hbm, bf16, src = peaks()
-    tf32_peak = bf16 / 2.0
+    # tensor-core tf32 ceiling: measured tcgen05 kind::tf32 issue rate
+    # (tools/mma_bench.cu, profiles/r01_mma_bench.txt); 1/2 x the bf16 figure
+    # would be the datasheet ratio applied to the cuBLAS-measured bf16 number
+    tf32_peak = TF32_MMA_PEAK
     achieved = 3.0 * gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-    roofline = {"bound": "tensor", "kernel": "tcgen05 3xTF32 GEMM (gemm_tc_kernel)",
+    roofline = {"bound": "tensor", "kernel": "tcgen05 3xTF32 GEMM (gemm_tc_tmema_kernel, CTA pairs)",
                 "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
                 "traffic": None,
                 "note": (f"achieved = tensor-core TF32 work (3 MMAs per fp32 FLOP: hi.hi + hi.lo + lo.hi) "
                          f"/ GEMM time, summed over the {sum(1 for k, _ in recs if k == R.K_GEMM)} GEMM launches "
-                         f"of one step; peak = dense tf32 = 1/2 x {src} bf16 burst {bf16:.1f} TF/s "
-                         f"(B200 tf32:bf16 = 1.1:2.25). fp32-equivalent GEMM rate "
+                         f"of one step; peak = measured tcgen05 kind::tf32 rate {tf32_peak:.0f} TF/s "
+                         f"(tools/mma_bench.cu; {src} bf16 {bf16:.1f} TF/s / 2 = {bf16 / 2:.0f}). "
+                         f"fp32-equivalent GEMM rate "
                          f"{gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0:.1f} TFLOP/s"),
                 "step_ms_by_class": {k: round(v, 4) for k, v in sorted(cls_ms.items())},
                 "gemm_share_of_step": (gemm_ms / float(np.sum(rec_ms))) if np.sum(rec_ms) > 0 else None}
