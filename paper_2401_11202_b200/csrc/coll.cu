@@ -14,6 +14,7 @@
 namespace {
 
 __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ spx_gather_params p) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.y;
   const float* const* table = reinterpret_cast<const float* const*>(p.src_table);
   const int64_t* base = reinterpret_cast<const int64_t*>(p.base_off);
@@ -38,6 +39,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ spx
 // Contiguous-source fast path: rank-1 copy of a chunk (all_slice of a dim-0
 // chunk, dim-0 all_gather pieces) with float4 moves.
 __global__ void __launch_bounds__(256) creduce_kernel(const __grid_constant__ spx_creduce_params p) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.y;
   const float* const* src = reinterpret_cast<const float* const*>(p.src);
   const int32_t* mem = reinterpret_cast<const int32_t*>(p.members) + (int64_t)d * p.n_members;
@@ -74,7 +76,7 @@ static unsigned grid_for(int64_t n) {
 
 int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch) {
   if (p.numel <= 0) return 0;
-  gather_kernel<<<dim3(grid_for(p.numel), (unsigned)p.ndev), 256, 0, s>>>(p);
+  spx_launch(gather_kernel, dim3(grid_for(p.numel), (unsigned)p.ndev), 256, 0, s, p);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;
@@ -82,7 +84,7 @@ int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch) 
 
 int spx_launch_creduce(const spx_creduce_params& p, cudaStream_t s, int* nlaunch) {
   if (p.numel <= 0) return 0;
-  creduce_kernel<<<dim3(grid_for(p.numel), (unsigned)p.ndev), 256, 0, s>>>(p);
+  spx_launch(creduce_kernel, dim3(grid_for(p.numel), (unsigned)p.ndev), 256, 0, s, p);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;

@@ -8,6 +8,7 @@
 #error "spindle_b200 kernels target sm_100a (Blackwell) only"
 #endif
 
+#include <utility>
 #define SPX_DEV __device__ __forceinline__
 
 // Arena addressing: device d's copy of an element offset.
@@ -70,3 +71,29 @@ void spx_gemm_tc_free(SpxGemmTC* g);
 bool spx_gemm_tc_supported(const spx_gemm_params& p);
 
 int spx_num_sms();
+
+// Programmatic dependent launch: every kernel starts with SPX_PDL_ENTRY --
+// it lets the NEXT kernel in the stream be scheduled once all of this grid's
+// CTAs are running (its launch latency and prologue then overlap our tail),
+// and waits for the PREVIOUS grid's completion (and memory) before touching
+// global memory.  Kernels launched through spx_launch carry the attribute;
+// without it (SPX_PDL=0, or a non-PDL predecessor such as an NCCL kernel) the
+// wait returns immediately and ordering is plain stream order.
+#define SPX_PDL_ENTRY() asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
+bool spx_pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void spx_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = spx_pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}

@@ -16,6 +16,7 @@ namespace {
 // compile-time-specialised kernels of ew_static.cu.
 template <int NIN, int U>
 __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ spx_ew_params p) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.y;
   const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
   float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ spx
 }
 
 __global__ void __launch_bounds__(256) ew_gen_kernel(const __grid_constant__ spx_ew_params p) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.y;
   const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
   float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
@@ -136,14 +138,14 @@ int spx_launch_ew(const spx_ew_params& p, cudaStream_t s, int* nlaunch) {
     auto grid_u = [&](int u) { return dim3(blocks_for((nv + u - 1) / u), (unsigned)p.ndev); };
     switch (p.n_in) {
       case 0:
-      case 1: ew_vec_kernel<1, 1><<<grid_u(1), 256, 0, s>>>(p); break;
-      case 2: ew_vec_kernel<2, 1><<<grid_u(1), 256, 0, s>>>(p); break;
-      case 3: ew_vec_kernel<3, 1><<<grid_u(1), 256, 0, s>>>(p); break;
-      case 4: ew_vec_kernel<4, 1><<<grid_u(1), 256, 0, s>>>(p); break;
-      default: ew_vec_kernel<SPX_MAX_IN, 1><<<grid_u(1), 256, 0, s>>>(p);
+      case 1: spx_launch(ew_vec_kernel<1, 1>, grid_u(1), 256, 0, s, p); break;
+      case 2: spx_launch(ew_vec_kernel<2, 1>, grid_u(1), 256, 0, s, p); break;
+      case 3: spx_launch(ew_vec_kernel<3, 1>, grid_u(1), 256, 0, s, p); break;
+      case 4: spx_launch(ew_vec_kernel<4, 1>, grid_u(1), 256, 0, s, p); break;
+      default: spx_launch(ew_vec_kernel<SPX_MAX_IN, 1>, grid_u(1), 256, 0, s, p);
     }
   } else {
-    ew_gen_kernel<<<dim3(blocks_for(p.numel), (unsigned)p.ndev), 256, 0, s>>>(p);
+    spx_launch(ew_gen_kernel, dim3(blocks_for(p.numel), (unsigned)p.ndev), 256, 0, s, p);
   }
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;

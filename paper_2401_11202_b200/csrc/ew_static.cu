@@ -45,6 +45,7 @@ SPX_DEV void run_static(Vec<4>* r, const float* imm, std::integer_sequence<int, 
 // thread per iteration with all loads hoisted.
 template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
 __global__ void __launch_bounds__(256) ew_static_kernel(const __grid_constant__ spx_ew_params p) {
+  SPX_PDL_ENTRY();
   constexpr int U = 2;
   const int d = blockIdx.y;
   const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
@@ -98,7 +99,7 @@ struct Entry {
 
 template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
 void launch_static(const spx_ew_params& p, dim3 g, cudaStream_t s) {
-  ew_static_kernel<NIN, NOUT, O0, O1, I...><<<g, 256, 0, s>>>(p);
+  spx_launch(ew_static_kernel<NIN, NOUT, O0, O1, I...>, g, 256, 0, s, p);
 }
 
 #define OP(x) SPX_OP_##x

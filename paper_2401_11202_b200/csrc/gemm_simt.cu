@@ -10,6 +10,7 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16;
 
 __global__ void __launch_bounds__(256) sgemm_kernel(const __grid_constant__ spx_gemm_params p) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.z;
   const float* A = dev_ptr(p.base, p.dev_stride, d, p.a_off);
   const float* B = dev_ptr(p.base, p.dev_stride, d, p.b_off);
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(const __grid_constant__ spx_
 int spx_launch_gemm_simt(const spx_gemm_params& p, cudaStream_t s, int* nlaunch) {
   if (p.M <= 0 || p.N <= 0) return 0;
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.ndev);
-  sgemm_kernel<<<grid, 256, 0, s>>>(p);
+  spx_launch(sgemm_kernel, grid, 256, 0, s, p);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;

@@ -306,6 +306,7 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
   else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_d = *tmem_slot;
+  SPX_PDL_ENTRY();   // barrier init, TMEM alloc, descriptor prefetch overlap the previous kernel
 
   // Warpgroup roles (setmaxnreg moves registers to the drain warpgroup, whose
   // fp32 promotion accumulators hold a 32 x 128 tile slice per warp):
@@ -622,22 +623,27 @@ static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
     SPX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgT<RS_, LS_, CG>::TOTAL));
     attr = true;
   }
-  if (CG == 1) {
-    kern<<<g->grid, NTHREADS_T, CfgT<RS_, LS_, CG>::TOTAL, s>>>(g->ma, g->mb, g->args);
-    return 0;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g->grid;
   cfg.blockDim = dim3(NTHREADS_T);
   cfg.dynamicSmemBytes = CfgT<RS_, LS_, CG>::TOTAL;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CG;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (CG > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = CG;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (spx_pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   SPX_CUDA(cudaLaunchKernelEx(&cfg, kern, g->ma, g->mb, g->args));
   return 0;
 }

@@ -51,18 +51,24 @@ SPX_DEV void load2d(const spx_reduce_params& p, const float* fb, int64_t o, int6
   }
 }
 
-template <int W>
+// WPO warps per output: 1 (8 outputs per block) or 8 (few outputs, e.g. the
+// loss: the whole block walks one output's chunk, partials combined in smem
+// in warp order)
+template <int W, int WPO>
 __global__ void __launch_bounds__(256) reduce_row(const __grid_constant__ spx_reduce_params p, int64_t chunk,
                                                   int nchunks) {
+  SPX_PDL_ENTRY();
+  __shared__ float part[8];
   const int d = blockIdx.z;
   const float* fb = dev_ptr(p.x.base, p.x.dev_stride, d, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t o = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t o = (int64_t)blockIdx.x * (8 / WPO) + warp / WPO;
+  const int sub = warp % WPO;
   const int c = blockIdx.y;
   if (o >= p.n_out) return;
   const int64_t r0 = c * chunk, r1 = min(p.n_red_elems, r0 + chunk);
   float acc = ident(p.monoid);
-  for (int64_t r = r0 + (int64_t)lane * W; r < r1; r += 32 * W) {
+  for (int64_t r = r0 + (int64_t)(sub * 32 + lane) * W; r < r1; r += 32 * W * WPO) {
     RegFile<W> f;
     load2d<W, true>(p, fb, o, r, f);
     run_program<W>(p.x.prog, p.x.imm, p.x.n_prog, f);
@@ -72,12 +78,24 @@ __global__ void __launch_bounds__(256) reduce_row(const __grid_constant__ spx_re
   }
 #pragma unroll
   for (int m = 16; m > 0; m >>= 1) acc = fold(p.monoid, acc, __shfl_xor_sync(0xffffffffu, acc, m));
-  if (lane == 0) *out_ptr(p, d, nchunks, c, o) = acc;
+  if (WPO == 1) {
+    if (lane == 0) *out_ptr(p, d, nchunks, c, o) = acc;
+    return;
+  }
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = part[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = fold(p.monoid, v, part[w]);
+    *out_ptr(p, d, nchunks, c, o) = v;
+  }
 }
 
 template <int W>
 __global__ void __launch_bounds__(256) reduce_col(const __grid_constant__ spx_reduce_params p, int64_t chunk,
                                                   int nchunks) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.z;
   const float* fb = dev_ptr(p.x.base, p.x.dev_stride, d, 0);
   const int64_t o = ((int64_t)blockIdx.x * 32 + threadIdx.x) * W;
@@ -114,6 +132,7 @@ __global__ void __launch_bounds__(256) reduce_col(const __grid_constant__ spx_re
 // Generic: any rank; one warp per output, lanes walk r.
 __global__ void __launch_bounds__(256) reduce_gen(const __grid_constant__ spx_reduce_params p, int64_t chunk,
                                                   int nchunks) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.z;
   const float* fb = dev_ptr(p.x.base, p.x.dev_stride, d, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,6 +177,7 @@ __global__ void __launch_bounds__(256) reduce_gen(const __grid_constant__ spx_re
 // gradients of broadcasts): a thread owns 4 consecutive outputs along the
 // contiguous innermost kept dim and walks the whole reduced range.
 __global__ void __launch_bounds__(256) reduce_out(const __grid_constant__ spx_reduce_params p) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.y;
   const float* fb = dev_ptr(p.x.base, p.x.dev_stride, d, 0);
   float* out = dev_ptr(p.x.base, p.x.dev_stride, d, p.out_off);
@@ -214,7 +234,26 @@ __global__ void __launch_bounds__(256) reduce_out(const __grid_constant__ spx_re
   }
 }
 
+// few outputs, many chunks: a block per output, strided fold + fixed smem tree
+__global__ void __launch_bounds__(256) reduce_final_block(const __grid_constant__ spx_reduce_params p, int nchunks) {
+  SPX_PDL_ENTRY();
+  __shared__ float red[256];
+  const int d = blockIdx.y;
+  const int64_t o = blockIdx.x;
+  const float* part = dev_ptr(p.x.base, p.x.dev_stride, d, p.scratch_off);
+  float v = ident(p.monoid);
+  for (int c = threadIdx.x; c < nchunks; c += 256) v = fold(p.monoid, v, part[(int64_t)c * p.n_out + o]);
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fold(p.monoid, red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dev_ptr(p.x.base, p.x.dev_stride, d, p.out_off)[o] = red[0];
+}
+
 __global__ void reduce_final(const __grid_constant__ spx_reduce_params p, int nchunks) {
+  SPX_PDL_ENTRY();
   const int d = blockIdx.y;
   const float* part = dev_ptr(p.x.base, p.x.dev_stride, d, p.scratch_off);
   float* out = dev_ptr(p.x.base, p.x.dev_stride, d, p.out_off);
@@ -237,13 +276,14 @@ int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch) 
     const int64_t cap = (int64_t)spx_num_sms() * 16;
     if (b > cap) b = cap;
     if (b < 1) b = 1;
-    reduce_out<<<dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s>>>(p);
+    spx_launch(reduce_out, dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s, p);
     SPX_CHECK_LAUNCH();
     if (nlaunch) ++*nlaunch;
     return 0;
   }
   const int W = p.x.vec ? 4 : 1;
-  int64_t per_block_out = mode == 1 ? 32 * W : 8;
+  const bool few = mode == 0 && p.n_out < 64;        // ROW with a handful of outputs
+  int64_t per_block_out = mode == 1 ? 32 * W : (few ? 1 : 8);
   const int64_t out_blocks = (p.n_out + per_block_out - 1) / per_block_out;
   const int64_t target = (int64_t)spx_num_sms() * 4;
   int64_t nchunks = (target + out_blocks * p.x.ndev - 1) / (out_blocks * p.x.ndev);
@@ -259,20 +299,29 @@ int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch) 
   if (nchunks < 1) nchunks = 1;
   dim3 grid((unsigned)out_blocks, (unsigned)nchunks, (unsigned)p.x.ndev);
   if (mode == 0) {
-    if (W == 4) reduce_row<4><<<grid, 256, 0, s>>>(p, chunk, (int)nchunks);
-    else reduce_row<1><<<grid, 256, 0, s>>>(p, chunk, (int)nchunks);
+    if (few) {
+      if (W == 4) spx_launch(reduce_row<4, 8>, grid, 256, 0, s, p, chunk, (int)nchunks);
+      else spx_launch(reduce_row<1, 8>, grid, 256, 0, s, p, chunk, (int)nchunks);
+    } else {
+      if (W == 4) spx_launch(reduce_row<4, 1>, grid, 256, 0, s, p, chunk, (int)nchunks);
+      else spx_launch(reduce_row<1, 1>, grid, 256, 0, s, p, chunk, (int)nchunks);
+    }
   } else if (mode == 1) {
-    if (W == 4) reduce_col<4><<<grid, dim3(32, 8), 0, s>>>(p, chunk, (int)nchunks);
-    else reduce_col<1><<<grid, dim3(32, 8), 0, s>>>(p, chunk, (int)nchunks);
+    if (W == 4) spx_launch(reduce_col<4>, grid, dim3(32, 8), 0, s, p, chunk, (int)nchunks);
+    else spx_launch(reduce_col<1>, grid, dim3(32, 8), 0, s, p, chunk, (int)nchunks);
   } else {
-    reduce_gen<<<grid, 256, 0, s>>>(p, chunk, (int)nchunks);
+    spx_launch(reduce_gen, grid, 256, 0, s, p, chunk, (int)nchunks);
   }
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
-  if (nchunks > 1) {
+  if (nchunks > 1 && p.n_out < 64 && nchunks >= 64) {
+    spx_launch(reduce_final_block, dim3((unsigned)p.n_out, (unsigned)p.x.ndev), 256, 0, s, p, (int)nchunks);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+  } else if (nchunks > 1) {
     int64_t b = (p.n_out + 255) / 256;
     if (b > 1024) b = 1024;
-    reduce_final<<<dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s>>>(p, (int)nchunks);
+    spx_launch(reduce_final, dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s, p, (int)nchunks);
     SPX_CHECK_LAUNCH();
     if (nlaunch) ++*nlaunch;
   }

@@ -22,6 +22,14 @@ int spx_set_error(const char* fmt, ...) {
 
 static int g_num_sms = 148;
 int spx_num_sms() { return g_num_sms; }
+bool spx_pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SPX_PDL");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
 
 // ---------------------------------------------------------------------------
 // NCCL via dlopen (no link-time dependency; reuse the process's libnccl)
