@@ -356,13 +356,16 @@ class Compiler:
                  and lda % 4 == 0 and ldb % 4 == 0)
         if not tc_ok:
             return 1
-        tiles = -(-M // 128) * -(-N // 128) * len(self.devices)
+        # SM units: the tcgen05 kernel computes 256 x 128 tiles on CTA pairs
+        units = -(-M // 256) * 2 * -(-N // 128) * len(self.devices)
         nk = -(-K // 32)
-        # only for very few tiles: moderate cases (e.g. 64 tiles of 1024x1024
-        # weight gradients) run better unsplit, concurrently on the side stream
-        if tiles * 8 > self.NUM_SMS or nk < 16:
+        # split only when the tiles leave most SMs idle (F: SPX_SPLITK_F);
+        # moderately small GEMMs often run concurrently on the side stream
+        import os
+        f = int(os.environ.get("SPX_SPLITK_F", "8"))
+        if units * f > self.NUM_SMS or nk < 16:
             return 1
-        s = min(nk // 8, -(-self.NUM_SMS // tiles))
+        s = min(nk // 8, self.NUM_SMS // units)
         return max(1, s)
 
     # ----------------------------------------------------------------- reduce

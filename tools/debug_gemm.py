@@ -19,6 +19,8 @@ class G:
         N = B.shape[0] if bt else B.shape[1]
         self.M, self.N, self.K = M, N, K
         na, nb, nc = A.size, B.size, M * N
+        import os
+        nc = nc * max(1, int(os.environ.get("SPLITS", "1")))
         self.base = dev.malloc(4 * (pad(na) + pad(nb) + pad(nc)))
         dev.h2d(self.base, A.astype(np.float32))
         dev.h2d(self.base + 4 * pad(na), B.astype(np.float32))
@@ -31,6 +33,8 @@ class G:
         p.lda, p.ldb, p.ldc = A.shape[1], B.shape[1], N
         p.a_mn_major, p.b_k_major = int(at), int(bt)
         p.path, p.promote = path, promote
+        import os
+        p.splits = int(os.environ.get("SPLITS", "1"))
         self.plan = R.NativePlan(dev)
         self.plan.add(R.K_GEMM, p)
         self.plan.finalize()

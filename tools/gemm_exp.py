@@ -9,7 +9,8 @@ dev = R.Device(0)
 rng = np.random.default_rng(0)
 print("SPX_GEMM_PIPE", os.environ.get("SPX_GEMM_PIPE"))
 SHAPES = [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
-          (1024, 1024, 2048, True, False), (4096, 4096, 4096, False, False)]
+          (1024, 1024, 2048, True, False), (4096, 4096, 4096, False, False),
+          (1024, 2048, 1024, False, False), (1024, 1024, 1024, True, False), (2048, 1024, 1024, False, False)]
 if os.environ.get("SHAPES"):
     SHAPES = [SHAPES[int(i)] for i in os.environ["SHAPES"].split(",")]
 for (M, N, K, at, bt) in SHAPES:
