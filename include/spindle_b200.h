@@ -156,13 +156,16 @@ typedef struct {
 } spx_nccl_params;
 
 /* ---- all-reduce over NVLink peer memory (CUDA IPC-mapped arenas) -------- */
+/* Flag region of a member (uint32): [slot][phase 2][block SPX_PEER_MAX_BLOCKS][member 8];
+ * epoch counters (local): [slot][block]. */
+#define SPX_PEER_MAX_BLOCKS 512
 typedef struct {
   int32_t kind, n, me, monoid;     /* kind 0 = all-reduce; n members; me = my index */
   int64_t count;                   /* elements */
   uint64_t src[8];                 /* members' input buffers, mapped into this process */
   uint64_t dst;                    /* local output */
-  uint64_t flags[8];               /* members' flag regions (mapped); [slot][phase][8] u32 */
-  uint64_t counter;                /* local epoch counters, u32 per slot */
+  uint64_t flags[8];               /* members' flag regions (mapped), layout above */
+  uint64_t counter;                /* local epoch counters, u32 [slot][block] */
   int32_t slot, pad;
 } spx_peer_params;
 
@@ -200,9 +203,11 @@ int spx_comm_destroy(int comm);
 int spx_plan_create(uint64_t* out_plan);
 int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t params_bytes);
 /* Scheduling (optional): run record `index` on stream `stream` (0 = the stream
- * passed to run/capture, 1 = the plan's side stream, used for collectives so
- * they overlap compute), after the records listed in `waits` (indices of
- * earlier records on the other stream) have completed. */
+ * passed to run/capture; 1..3 = the plan's side streams: 1 off-critical compute
+ * such as weight-gradient GEMMs, 2 collectives (high priority), 3 parameter
+ * updates), after the records listed in `waits` (indices of earlier records on
+ * other streams) have completed.  Side streams fork from and join back into
+ * the run/capture stream, so a plan stays one unit on it. */
 int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, int n_waits);
 int spx_plan_finalize(uint64_t plan);              /* builds TMA descriptors etc. */
 int spx_plan_run(uint64_t plan, uint64_t stream);  /* eager launch of every record */

@@ -1,84 +1,133 @@
 // All-reduce over NVLink peer memory (one mesh device per process, arenas
 // mapped into every peer with CUDA IPC).  For the latency-bound collectives on
-// the critical path (the Megatron activation reductions: ~4 MB, 64 per C2
+// the critical path (the Megatron activation reductions: ~4 MB, 32-64 per C2
 // step) a one-shot all-reduce beats a ring: every rank reads the n-1 peer
 // inputs straight over NVLink and folds them IN MEMBER ORDER -- the left fold
 // of the reference's `_combine` (spmd_interp.py:66-71) -- so every replica
 // gets bit-identical values, identical to the reference evaluator's.
 //
-// One record = three launches on the stream:
-//   1. peer_barrier  (1 warp): epoch = ++counter[slot]; store epoch into every
-//      member's flag word for (slot, phase 0, me) with st.release.sys, spin
-//      (bounded, traps on timeout) until all members' words reach epoch --
-//      every member's input is complete;
-//   2. peer_sum: out[i] = src[0][i] + src[1][i] + ... (float4, grid-stride);
-//   3. peer_barrier phase 1: nobody proceeds (and may overwrite its input)
-//      until every member has finished reading.
+// One launch.  Block b of every member owns the same slice of the tensor and
+// synchronises only with block b of the other members, through per-block
+// flag words in every member's arena (written remotely):
+//   1. arrive: store epoch into flags[slot][0][b][me] of every member, wait
+//      until all members' block b arrived (their inputs are complete: the
+//      kernel runs after its producers in stream order);
+//   2. out[i] = src[0][i] + src[1][i] + ... for the block's slice (float4, all
+//      members' loads in flight before the fold);
+//   3. depart: store epoch into flags[slot][1][b][me] of every member, wait
+//      until all members' block b are done reading -- nobody leaves (and may
+//      overwrite its input) while a peer still reads it.
+// Epochs are per (slot, block) counters in the local arena, so graph replays
+// and eager runs keep counting without host involvement.
+#include <cstdlib>
 #include "common.cuh"
 
 namespace {
 
-SPX_DEV void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Flags are relaxed (volatile) system-scope accesses: a release/acquire pair
+// costs ~5 us per barrier across NVLink, and neither side needs one -- the
+// inputs were completed by earlier kernels (kernel boundaries make them
+// visible to peer reads), the depart flag is stored after __syncthreads, when
+// every load of the block has returned its value, and the kernel reads each
+// peer element exactly once (no stale L1 line can be hit).
+SPX_DEV void st_flag(uint32_t* p, uint32_t v) {
+  asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-SPX_DEV uint32_t ld_acquire_sys(const uint32_t* p) {
+SPX_DEV uint32_t ld_flag(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-// flag word address of (slot, phase, member) inside a rank's flag region
-SPX_DEV uint32_t* flag_at(uint64_t region, int slot, int phase, int member) {
-  return reinterpret_cast<uint32_t*>(region) + ((slot * 2 + phase) * 8 + member);
+// flag word of (slot, phase, block, member) inside a member's flag region
+SPX_DEV uint32_t* flag_at(uint64_t region, int slot, int phase, int block, int member) {
+  return reinterpret_cast<uint32_t*>(region) +
+         (((int64_t)(slot * 2 + phase) * SPX_PEER_MAX_BLOCKS + block) * 8 + member);
 }
 
-__global__ void peer_barrier(const __grid_constant__ spx_peer_params p, int phase) {
-  const int lane = threadIdx.x;
-  uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + p.slot;
-  uint32_t epoch = 0;
-  if (lane == 0) {
-    epoch = *counter + (phase == 0 ? 1u : 0u);
-    if (phase == 0) *counter = epoch;
-  }
-  epoch = __shfl_sync(0xffffffffu, epoch, 0);
-  __threadfence_system();
-  if (lane < p.n) st_release_sys(flag_at(p.flags[lane], p.slot, phase, p.me), epoch);
-  if (lane < p.n) {
-    const uint32_t* mine = flag_at(p.flags[p.me], p.slot, phase, lane);
-    long long t0 = clock64();
-    while (ld_acquire_sys(mine) < epoch) {
-      __nanosleep(64);
-      if (clock64() - t0 > 20000000000LL) __trap();     // ~10 s: a peer never arrived
-    }
-  }
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(256) peer_sum(const __grid_constant__ spx_peer_params p) {
-  const int64_t n4 = p.count >> 2;
-  float4* dst = reinterpret_cast<float4*>(p.dst);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    float4 acc = reinterpret_cast<const float4*>(p.src[0])[i];
-    for (int m = 1; m < p.n; ++m) {
-      const float4 v = reinterpret_cast<const float4*>(p.src[m])[i];
-      if (p.monoid == 0) {
-        acc.x = f_add(acc.x, v.x); acc.y = f_add(acc.y, v.y); acc.z = f_add(acc.z, v.z); acc.w = f_add(acc.w, v.w);
-      } else {
-        acc.x = f_max(acc.x, v.x); acc.y = f_max(acc.y, v.y); acc.z = f_max(acc.z, v.z); acc.w = f_max(acc.w, v.w);
+SPX_DEV void block_barrier(const spx_peer_params& p, int phase, uint32_t epoch) {
+  const int t = threadIdx.x;
+  if (t < p.n) {
+    st_flag(flag_at(p.flags[t], p.slot, phase, blockIdx.x, p.me), epoch);
+    const uint32_t* mine = flag_at(p.flags[p.me], p.slot, phase, blockIdx.x, t);
+    if (ld_flag(mine) < epoch) {
+      const long long t0 = clock64();
+      while (ld_flag(mine) < epoch) {
+        if (clock64() - t0 > 20000000000LL) __trap();     // ~10 s: a peer never arrived
       }
     }
-    dst[i] = acc;
   }
-  // tail (count % 4)
-  if (blockIdx.x == 0 && threadIdx.x < (p.count & 3)) {
+  __syncthreads();
+}
+
+SPX_DEV float4 fold4(int monoid, float4 a, float4 v) {
+  if (monoid == 0) {
+    a.x = f_add(a.x, v.x); a.y = f_add(a.y, v.y); a.z = f_add(a.z, v.z); a.w = f_add(a.w, v.w);
+  } else {
+    a.x = f_max(a.x, v.x); a.y = f_max(a.y, v.y); a.z = f_max(a.z, v.z); a.w = f_max(a.w, v.w);
+  }
+  return a;
+}
+
+constexpr int U = 4;   // float4 per thread per iteration (loads in flight per member)
+
+// N > 0: member count known at compile time (all loads issued before folding)
+template <int N>
+__global__ void __launch_bounds__(256) peer_allreduce(const __grid_constant__ spx_peer_params p, int64_t per_block,
+                                                      int dbg) {
+  SPX_PDL_ENTRY();
+  const int n = N > 0 ? N : p.n;
+  uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
+  const uint32_t epoch = *counter + 1u;
+  if (!(dbg & 1)) block_barrier(p, 0, epoch);
+  if (dbg & 4) per_block = 0;
+
+  const int64_t n4 = p.count >> 2;
+  const int64_t b0 = (int64_t)blockIdx.x * per_block, b1 = min(n4, b0 + per_block);
+  float4* dst = reinterpret_cast<float4*>(p.dst);
+  for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += 256 * U) {
+    float4 v[N > 0 ? N : 1][U];
+    if (N > 0) {
+#pragma unroll
+      for (int m = 0; m < (N > 0 ? N : 1); ++m)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * 256;
+          if (i < b1) v[m][u] = reinterpret_cast<const float4*>(p.src[m])[i];
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * 256;
+        if (i >= b1) continue;
+        float4 acc = v[0][u];
+#pragma unroll
+        for (int m = 1; m < (N > 0 ? N : 1); ++m) acc = fold4(p.monoid, acc, v[m][u]);
+        dst[i] = acc;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * 256;
+        if (i >= b1) continue;
+        float4 acc = reinterpret_cast<const float4*>(p.src[0])[i];
+        for (int m = 1; m < n; ++m) acc = fold4(p.monoid, acc, reinterpret_cast<const float4*>(p.src[m])[i]);
+        dst[i] = acc;
+      }
+    }
+  }
+  // tail (count % 4) in the last block
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < (p.count & 3)) {
     const int64_t i = n4 * 4 + threadIdx.x;
     float acc = reinterpret_cast<const float*>(p.src[0])[i];
-    for (int m = 1; m < p.n; ++m) {
-      const float v = reinterpret_cast<const float*>(p.src[m])[i];
-      acc = p.monoid == 0 ? f_add(acc, v) : f_max(acc, v);
+    for (int m = 1; m < n; ++m) {
+      const float x = reinterpret_cast<const float*>(p.src[m])[i];
+      acc = p.monoid == 0 ? f_add(acc, x) : f_max(acc, x);
     }
     reinterpret_cast<float*>(p.dst)[i] = acc;
   }
+  __syncthreads();
+  if (!(dbg & 2)) block_barrier(p, 1, epoch);
+  if (threadIdx.x == 0) *counter = epoch;
 }
 
 }  // namespace
@@ -88,16 +137,23 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if ((p.dst & 15) || p.kind != 0) return spx_set_error("peer collective: unsupported record");
   for (int m = 0; m < p.n; ++m)
     if (p.src[m] & 15) return spx_set_error("peer collective: unaligned source");
-  peer_barrier<<<1, 32, 0, s>>>(p, 0);
+  // blocks: ~8 float4 per thread, at most 2 per SM (co-resident with little
+  // else) and SPX_PEER_MAX_BLOCKS (flag space); identical on every member
+  const int64_t n4 = p.count >> 2;
+  int64_t blocks = (n4 + 256 * 8 - 1) / (256 * 8);
+  const int64_t cap = (int64_t)spx_num_sms() * 2 < SPX_PEER_MAX_BLOCKS ? (int64_t)spx_num_sms() * 2 : SPX_PEER_MAX_BLOCKS;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const int64_t per_block = (n4 + blocks - 1) / blocks;
+  static int dbg = -1;
+  if (dbg < 0) { const char* e = getenv("SPX_PEER_DBG"); dbg = e ? atoi(e) : 0; }
+  switch (p.n) {
+    case 2: spx_launch(peer_allreduce<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
+    case 4: spx_launch(peer_allreduce<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
+    case 8: spx_launch(peer_allreduce<8>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
+    default: spx_launch(peer_allreduce<0>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg);
+  }
   SPX_CHECK_LAUNCH();
-  int64_t b = (p.count / 4 + 255) / 256;
-  const int64_t cap = (int64_t)spx_num_sms() * 4;
-  if (b > cap) b = cap;
-  if (b < 1) b = 1;
-  peer_sum<<<(unsigned)b, 256, 0, s>>>(p);
-  SPX_CHECK_LAUNCH();
-  peer_barrier<<<1, 32, 0, s>>>(p, 1);
-  SPX_CHECK_LAUNCH();
-  if (nlaunch) *nlaunch += 3;
+  if (nlaunch) ++*nlaunch;
   return 0;
 }

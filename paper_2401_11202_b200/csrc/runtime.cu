@@ -133,18 +133,21 @@ struct Record {
   int path;  // GEMM: 1 tcgen05, 2 simt
   std::vector<uint8_t> params;
   SpxGemmTC* tc = nullptr;
-  int stream = 0;               // 0 main, 1 side
-  std::vector<int> waits;       // records on the other stream to wait for
-  bool signal = false;          // a later record on the other stream waits for this one
+  int stream = 0;               // 0 main, 1..SPX_SIDE_STREAMS side streams
+  std::vector<int> waits;       // records on other streams to wait for
+  bool signal = false;          // a later record on another stream waits for this one
   cudaEvent_t done = nullptr;
 };
+
+constexpr int SPX_SIDE_STREAMS = 3;   // 1 off-critical compute, 2 collectives, 3 parameter updates
 
 struct Plan {
   std::vector<Record> recs;
   bool finalized = false;
-  bool two_streams = false;
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  bool two_streams = false;              // any record off the main stream
+  bool used[SPX_SIDE_STREAMS + 1] = {};
+  cudaStream_t side[SPX_SIDE_STREAMS + 1] = {};
+  cudaEvent_t fork = nullptr, join[SPX_SIDE_STREAMS + 1] = {};
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
@@ -329,9 +332,13 @@ int spx_plan_finalize(uint64_t plan) {
   if (P->two_streams) {
     int lo = 0, hi = 0;
     SPX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    SPX_CUDA(cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, hi));   // collectives first
+    for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
+      if (!P->used[k]) continue;
+      // collectives (and the legacy single side stream) first
+      SPX_CUDA(cudaStreamCreateWithPriority(&P->side[k], cudaStreamNonBlocking, k == 2 || k == 1 ? hi : lo));
+      SPX_CUDA(cudaEventCreateWithFlags(&P->join[k], cudaEventDisableTiming));
+    }
     SPX_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
-    SPX_CUDA(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming));
   }
   P->finalized = true;
   return 0;
@@ -347,15 +354,19 @@ static int issue_all(Plan* P, cudaStream_t s, int* nl) {
     return 0;
   }
   SPX_CUDA(cudaEventRecord(P->fork, s));
-  SPX_CUDA(cudaStreamWaitEvent(P->side, P->fork, 0));
+  for (int k = 1; k <= SPX_SIDE_STREAMS; ++k)
+    if (P->used[k]) SPX_CUDA(cudaStreamWaitEvent(P->side[k], P->fork, 0));
   for (auto& r : P->recs) {
-    cudaStream_t rs = r.stream ? P->side : s;
+    cudaStream_t rs = r.stream ? P->side[r.stream] : s;
     for (int w : r.waits) SPX_CUDA(cudaStreamWaitEvent(rs, P->recs[w].done, 0));
     if (run_record(r, rs, nl)) return -1;
     if (r.signal) SPX_CUDA(cudaEventRecord(r.done, rs));
   }
-  SPX_CUDA(cudaEventRecord(P->join, P->side));
-  SPX_CUDA(cudaStreamWaitEvent(s, P->join, 0));
+  for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
+    if (!P->used[k]) continue;
+    SPX_CUDA(cudaEventRecord(P->join[k], P->side[k]));
+    SPX_CUDA(cudaStreamWaitEvent(s, P->join[k], 0));
+  }
   return 0;
 }
 
@@ -364,7 +375,8 @@ int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, i
   if (P->finalized) return spx_set_error("plan already finalized");
   if (index < 0 || index >= (int)P->recs.size()) return spx_set_error("record index out of range");
   Record& r = P->recs[index];
-  r.stream = stream ? 1 : 0;
+  if (stream < 0 || stream > SPX_SIDE_STREAMS) return spx_set_error("stream %d out of range", stream);
+  r.stream = stream;
   r.waits.clear();
   for (int i = 0; i < n_waits; ++i) {
     const int w = waits[i];
@@ -372,7 +384,10 @@ int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, i
     r.waits.push_back(w);
     P->recs[w].signal = true;
   }
-  if (r.stream) P->two_streams = true;
+  if (r.stream) {
+    P->two_streams = true;
+    P->used[r.stream] = true;
+  }
   return 0;
 }
 
@@ -431,9 +446,11 @@ int spx_plan_destroy(uint64_t plan) {
     if (r.tc) spx_gemm_tc_free(r.tc);
     if (r.done) cudaEventDestroy(r.done);
   }
-  if (P->side) cudaStreamDestroy(P->side);
+  for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
+    if (P->side[k]) cudaStreamDestroy(P->side[k]);
+    if (P->join[k]) cudaEventDestroy(P->join[k]);
+  }
   if (P->fork) cudaEventDestroy(P->fork);
-  if (P->join) cudaEventDestroy(P->join);
   delete P;
   return 0;
 }

@@ -58,7 +58,10 @@ class Executable:
         import os
         if overlap is None:
             overlap = os.environ.get("SPX_OVERLAP", "1") != "0"
-        self.side = self._side_kernels() if overlap else set()
+        if overlap:
+            self._hoist_terminal()
+        self.stream_of = self._streams() if overlap else {}
+        self.side = set(self.stream_of)
         self.overlap = bool(self.side)
         self.reserve_sms = int(os.environ.get("SPX_RESERVE_SMS", "0")) if self.overlap else 0
         # NCCL mode: critical-path all-reduces as one-shot NVLink peer-memory
@@ -193,7 +196,8 @@ class Executable:
         # peers through their mapping of this arena) and local epoch counters
         nkeys = len(self.comm_keys()) if c.comm_mode == "nccl" else 0
         self.flag_off = hi
-        self.flag_elems = _align(nkeys * 16 + nkeys) if nkeys else 0
+        self.counter_off = hi + nkeys * 2 * R.PEER_MAX_BLOCKS * 8
+        self.flag_elems = _align(nkeys * 2 * R.PEER_MAX_BLOCKS * 8 + nkeys * R.PEER_MAX_BLOCKS) if nkeys else 0
         hi += self.flag_elems
         self.off = off
         self.slice_elems = _align(hi, 1 << 18)           # 1 MiB granularity per device
@@ -301,52 +305,87 @@ class Executable:
                 else:
                     self._emit_coll_nccl(k)
 
-    def _side_kernels(self) -> set:
-        """Kernels that run on the side stream, overlapped with the main chain:
-        * NCCL collectives (one mesh device per GPU);
-        * off-critical-path GEMMs: weight gradients whose results feed only the
-          parameter update (kernels writing function results) or a side-stream
-          collective -- e.g. act^T @ dh in matmul_grads (models.py:64-71).  A
-          small-tile dW GEMM then fills SMs the dX GEMM leaves idle."""
+    # streams of a two-level schedule (runtime.cu: SPX_SIDE_STREAMS)
+    MAIN, COMPUTE, COMM, UPDATE = 0, 1, 2, 3
+
+    def _terminal(self, k) -> bool:
+        """A kernel whose outputs are only function results (parameter and
+        momentum updates, the loss) -- nothing downstream waits for it."""
+        results = set(self.comp.result_bufs)
+        return k.kind in ("ew", "reduce") and all(b in results for b in k.data.get("outs_keep", k.outs))
+
+    def _hoist_terminal(self):
+        """Move every terminal kernel to just after its last producer.  The
+        reference's training steps emit all parameter updates after the whole
+        backward pass, in forward order (models.py:152-220), so as written the
+        first update waits for the LAST weight gradient; hoisted, each update
+        runs (on its own stream) as soon as its gradient exists."""
+        ks = self.comp.kernels
+        readers = {b for k in ks for b in k.ins}
+        prod = {}
+        after: dict = {}
+        keep = []
+        for i, k in enumerate(ks):
+            if self._terminal(k) and not any(b in readers for b in k.outs):
+                dep = max((prod[b] for b in k.ins if b in prod), default=-1)
+                after.setdefault(dep, []).append(k)
+            else:
+                keep.append((i, k))
+            for b in k.outs:
+                prod[b] = i
+        order = list(after.get(-1, []))
+        for i, k in keep:
+            order.append(k)
+            order.extend(after.get(i, []))
+        assert len(order) == len(ks)
+        self.comp.kernels = order
+
+    def _streams(self) -> dict:
+        """Kernel index -> side stream for everything off the critical path:
+        * COMM: NCCL collectives whose results feed only the parameter update
+          (gradient reductions; SPX_SIDE_ALL_COLLECTIVES=1: every collective);
+        * COMPUTE: off-critical-path GEMMs -- weight gradients whose results
+          feed only the update or a side-stream collective (act^T @ dh in
+          matmul_grads, models.py:64-71); a small-tile dW GEMM then fills SMs
+          the dX GEMM leaves idle;
+        * UPDATE: terminal kernels (parameter/momentum updates, the loss).
+        Everything else stays in program order on the main stream."""
         import os
         c = self.comp
         ks = c.kernels
-        results = set(c.result_bufs)
         readers: dict = {}
         for i, k in enumerate(ks):
             for b in k.ins:
                 readers.setdefault(b, []).append(i)
-        def terminal(i):
-            k = ks[i]
-            return k.kind in ("ew", "reduce") and all(b in results for b in
-                                                      k.data.get("outs_keep", k.outs))
 
         def off_critical(i, side):
             rd = [j for b in ks[i].outs for j in readers.get(b, [])]
-            return bool(rd) and all(terminal(j) or j in side for j in rd)
+            return bool(rd) and all(self._terminal(ks[j]) or j in side for j in rd)
 
-        side = set()
+        side: dict = {}
         crit_coll = os.environ.get("SPX_SIDE_ALL_COLLECTIVES", "0") == "1"
         if c.comm_mode == "nccl":
-            # collectives feeding only the parameter update (gradient reductions)
-            # overlap on the side stream; activation collectives on the critical
-            # path stay on the main stream (a cross-stream hop only adds latency)
+            # activation collectives on the critical path stay on the main
+            # stream (a cross-stream hop only adds latency)
             for i in reversed(range(len(ks))):
                 k = ks[i]
                 if k.kind == "coll" and k.data["kind"] != "all_slice":
                     if crit_coll or off_critical(i, side):
-                        side.add(i)
+                        side[i] = self.COMM
         if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
             for i in reversed(range(len(ks))):
                 if ks[i].kind == "gemm" and off_critical(i, side):
-                    side.add(i)
+                    side[i] = self.COMPUTE
+        if os.environ.get("SPX_UPDATE_STREAM", "1") != "0" and side:
+            for i, k in enumerate(ks):
+                if self._terminal(k):
+                    side[i] = self.UPDATE
         return side
 
     def _schedule(self):
-        """Two-stream schedule: communicating collectives on stream 1, everything
-        else on stream 0; a record waits for the LATEST earlier record on the
-        other stream whose arena intervals conflict with it (RAW, WAR or WAW --
-        the liveness packing reuses memory, so WAR/WAW matter too)."""
+        """Multi-stream schedule: a record waits for the LATEST earlier record
+        on each other stream whose arena intervals conflict with it (RAW, WAR
+        or WAW -- the liveness packing reuses memory, so WAR/WAW matter too)."""
         c = self.comp
         iv = {}
 
@@ -359,7 +398,7 @@ class Executable:
 
         kin, kout, kstream = [], [], []
         for i, k in enumerate(c.kernels):
-            kstream.append(1 if i in self.side else 0)
+            kstream.append(self.stream_of.get(i, self.MAIN))
             r = ivals(k.ins)
             w = ivals(k.outs)
             if k.kind == "reduce":
@@ -373,22 +412,23 @@ class Executable:
             return any(x0 < y1 and y0 < x1 for x0, x1 in a for y0, y1 in b)
 
         sched = []
-        by_stream = {0: [], 1: []}
+        by_stream: dict = {}
         for i, k in enumerate(c.kernels):
             st = kstream[i]
-            other = by_stream[1 - st]
-            wait = None
-            for j in reversed(other):
-                if hit(kin[i], kout[j]) or hit(kout[i], kin[j]) or hit(kout[i], kout[j]):
-                    wait = j
-                    break
+            waits = []
+            for o, lst in by_stream.items():
+                if o == st:
+                    continue
+                for j in reversed(lst):
+                    if hit(kin[i], kout[j]) or hit(kout[i], kin[j]) or hit(kout[i], kout[j]):
+                        if self._krange[j][1] > self._krange[j][0]:
+                            waits.append(self._krange[j][1] - 1)
+                        break
             first, end = self._krange[i]
-            if end > first:
-                waits = [self._krange[wait][1] - 1] if wait is not None and self._krange[wait][1] > self._krange[wait][0] else []
-                for r in range(first, end):
-                    if st or waits:
-                        sched.append((r, st, waits if r == first else []))
-            by_stream[st].append(i)
+            for r in range(first, end):
+                if st or waits:
+                    sched.append((r, st, sorted(waits) if r == first else []))
+            by_stream.setdefault(st, []).append(i)
         if not any(st for _, st, _ in sched):
             return []
         return sched
@@ -640,7 +680,7 @@ class Executable:
                     p.src[j] = self.peer_bases[r] + (src_a - self.base)
                     p.flags[j] = self.peer_bases[r] + self.flag_off * 4
                 p.dst = out_a
-                p.counter = self.base + (self.flag_off + len(self.comm_keys()) * 16) * 4
+                p.counter = self.base + self.counter_off * 4
                 self._records.append((R.K_PEER, p))
                 return
             self._nccl(R.NCCL_ALLREDUCE, comm, src_a, out_a, count, monoid)
