@@ -364,13 +364,18 @@ class Executable:
 
         side: dict = {}
         crit_coll = os.environ.get("SPX_SIDE_ALL_COLLECTIVES", "0") == "1"
+        prefetch = os.environ.get("SPX_PREFETCH", "1") != "0"
+        args = set(c.arg_bufs)
         if c.comm_mode == "nccl":
             # activation collectives on the critical path stay on the main
-            # stream (a cross-stream hop only adds latency)
+            # stream (a cross-stream hop only adds latency); collectives of
+            # function arguments (ZeRO-3 parameter all-gathers) depend on no
+            # compute and are prefetched on the collective stream
             for i in reversed(range(len(ks))):
                 k = ks[i]
                 if k.kind == "coll" and k.data["kind"] != "all_slice":
-                    if crit_coll or off_critical(i, side):
+                    if (crit_coll or off_critical(i, side)
+                            or (prefetch and k.ins and all(b in args for b in k.ins))):
                         side[i] = self.COMM
         if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
             for i in reversed(range(len(ks))):

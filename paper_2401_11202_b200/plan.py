@@ -121,6 +121,7 @@ class Compiler:
         self.buffers: dict[str, int] = {}      # name -> numel
         self.bufdims: dict[str, tuple] = {}
         self.kernels: list[Kernel] = []
+        self._coll_cse: dict = {}
         self._uid = 0
         self._tmp = 0
         self.arg_bufs = []
@@ -420,8 +421,48 @@ class Compiler:
             if x.kind == "view" and all(x.strides[dd] == 0 for dd in sliced):
                 self.desc[r] = Desc("view", dims, buf=x.buf, off=x.off, strides=x.strides)
                 return
+        # identical collectives of the same (immutable) buffer -- e.g. the
+        # forward and backward ZeRO-3 all-gathers of a parameter -- compute
+        # identical values: reuse the first result (bit-exact data movement)
+        import json as _json
+        cse_key = None
+        if x.kind == "buf":
+            cse_key = (k, x.buf, _json.dumps(op.attrs, sort_keys=True), tuple(dims))
+            hit = self._coll_cse.get(cse_key)
+            if hit is not None:
+                self.desc[r] = Desc("buf", dims, buf=hit)
+                return
+        elif x.kind == "view" and k == "all_gather" and x.off == 0:
+            # all_gather of a transposed buffer (the backward pass's W^T) is the
+            # transposed view of the buffer's own all-gather, when that exists
+            bd = tuple(self.bufdims.get(x.buf, ()))
+            cs = _contig(bd)
+            perm = []
+            for j, st in enumerate(x.strides):
+                cand = [q for q in range(len(bd)) if cs[q] == st and bd[q] == in_dims[j] and q not in perm]
+                if not cand or (bd[cand[0]] == 1):
+                    perm = None
+                    break
+                perm.append(cand[0])
+            if perm is not None and len(perm) == len(bd) and sorted(perm) == list(range(len(bd))):
+                apd = op.attrs["axes_per_dim"]
+                apd_b = [None] * len(bd)
+                gd = [0] * len(bd)
+                for j, q in enumerate(perm):
+                    apd_b[q] = apd[j]
+                    gd[q] = dims[j]
+                attrs_b = dict(op.attrs)
+                attrs_b["axes_per_dim"] = apd_b
+                hit = self._coll_cse.get((k, x.buf, _json.dumps(attrs_b, sort_keys=True), tuple(gd)))
+                if hit is not None:
+                    gcs = _contig(gd)
+                    self.desc[r] = Desc("view", tuple(dims), buf=hit, off=0,
+                                        strides=tuple(gcs[q] for q in perm))
+                    return
         src = self.materialize(src_name)
         out = self._new_buf(dims, "c")
+        if cse_key is not None:
+            self._coll_cse[cse_key] = out
         kern = Kernel("coll", [out], {src}, op_index=i,
                       data=dict(kind=k, attrs=dict(op.attrs), in_dims=in_dims, out_dims=tuple(dims),
                                 src=src))
