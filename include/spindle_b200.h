@@ -115,7 +115,25 @@ typedef struct {
   int32_t promote;                /* k-blocks per TMEM chunk (0 = default 4)     */
   int32_t reserve_sms;            /* SMs left free for concurrent collectives    */
   int32_t splits;                 /* split-K: >1 writes [splits][M][ldc] partials at c_off */
+  /* Fused epilogue (tcgen05 path, splits == 1): the elementwise consumer of
+   * C = A.B computed on the accumulator rows before they leave the SM, with
+   * the same IEEE operations (and order) as the unfused kernel:
+   *   SPX_EPI_NONE      out0 = C (at c_off / ldc)
+   *   SPX_EPI_ADD       out0 = X0 + C                      (residual add)
+   *   SPX_EPI_SQUARE    out0 = C, out1 = C * C              (square activation)
+   *   SPX_EPI_MULSCALE  out0 = C * (X0 * imm0)              (its backward)
+   *   SPX_EPI_MOMENTUM  out0 = X0 * imm0 + C,               (momentum SGD:
+   *                     out1 = X1 + -(out0 * imm1)           m' then p')
+   * X / out views: element offset from the device base + row pitch; columns
+   * contiguous. */
+  int32_t epi, epi_pad;
+  int64_t epi_in_off[2], epi_in_ld[2];
+  int64_t epi_out_off[2], epi_out_ld[2];
+  float epi_imm[2];
 } spx_gemm_params;
+
+enum spx_epilogue { SPX_EPI_NONE = 0, SPX_EPI_ADD = 1, SPX_EPI_SQUARE = 2, SPX_EPI_MULSCALE = 3,
+                    SPX_EPI_MOMENTUM = 4 };
 
 /* ---- collectives over co-located virtual devices ------------------------- */
 /* gather-style (all_slice, all_gather, all_to_all, relayouts):

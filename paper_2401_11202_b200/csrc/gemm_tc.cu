@@ -157,8 +157,79 @@ struct TcArgs {
   uint64_t c_base;     // device 0 address of C
   int64_t dev_stride;  // bytes
   int64_t ldc;
+  // fused epilogue (spx_gemm_params.epi*): offsets in elements from base
+  uint64_t base;
+  int epi;
+  int64_t in_off[2], in_ld[2], out_off[2], out_ld[2];
+  float imm[2];
 };
 
+// One accumulator value through the fused epilogue (spindle_b200.h,
+// spx_epilogue) -- the same IEEE operations, in the same order, as the
+// elementwise kernel it replaces (ew.cu / interp.cuh).
+template <int EPI>
+SPX_DEV void epi_apply(float c, float x0, float x1, float k0, float k1, float& y0, float& y1) {
+  if (EPI == SPX_EPI_ADD) {
+    y0 = f_add(x0, c);
+  } else if (EPI == SPX_EPI_SQUARE) {
+    y0 = c;
+    y1 = f_mul(c, c);
+  } else if (EPI == SPX_EPI_MULSCALE) {
+    y0 = f_mul(c, f_mul(x0, k0));
+  } else if (EPI == SPX_EPI_MOMENTUM) {
+    y0 = f_add(f_mul(x0, k0), c);
+    y1 = f_add(x1, -f_mul(y0, k1));
+  }
+}
+
+// Epilogue of one drain warp: its 32 accumulator rows (lane = row, acc[] =
+// the BN columns) go through a padded 32 x 33 shared-memory tile per 32-column
+// chunk, so that afterwards lane = column and every global load/store of the
+// warp is one 128-byte row segment (row-per-lane stores hit 32 lines each).
+template <int EPI>
+SPX_DEV void epi_store_tile(const TcArgs& a, int dev, int sp, int row0, int n0, const float* acc, float* stg,
+                            int lane) {
+  constexpr int NIN = EPI == SPX_EPI_ADD || EPI == SPX_EPI_MULSCALE ? 1 : EPI == SPX_EPI_MOMENTUM ? 2 : 0;
+  constexpr int NOUT = EPI == SPX_EPI_SQUARE || EPI == SPX_EPI_MOMENTUM ? 2 : 1;
+  constexpr int EG = NIN >= 2 ? 8 : 16;   // rows per group: loads of a group in flight together
+  float* db = reinterpret_cast<float*>(a.base + (uint64_t)((int64_t)dev * a.dev_stride));
+  const int rows = min(32, a.M - row0);
+#pragma unroll
+  for (int cc = 0; cc < BN / 32; ++cc) {
+    const int col = n0 + cc * 32 + lane;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = acc[cc * 32 + j];
+    __syncwarp();
+    if (col >= a.N) continue;
+#pragma unroll 1
+    for (int r0 = 0; r0 < rows; r0 += EG) {
+      float c[EG], x0[EG], x1[EG];
+#pragma unroll
+      for (int r = 0; r < EG; ++r) {
+        const int64_t row = row0 + r0 + r;
+        c[r] = stg[(r0 + r) * 33 + lane];
+        if (r0 + r < rows) {
+          if (NIN >= 1) x0[r] = db[a.in_off[0] + row * a.in_ld[0] + col];
+          if (NIN >= 2) x1[r] = db[a.in_off[1] + row * a.in_ld[1] + col];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < EG; ++r) {
+        if (r0 + r >= rows) break;
+        const int64_t row = row0 + r0 + r;
+        if (EPI == SPX_EPI_NONE) {
+          reinterpret_cast<float*>(a.c_base + (uint64_t)((int64_t)dev * a.dev_stride))[((int64_t)sp * a.M + row) * a.ldc + col] = c[r];
+          continue;
+        }
+        float y0, y1 = 0.f;
+        epi_apply<EPI>(c[r], NIN >= 1 ? x0[r] : 0.f, NIN >= 2 ? x1[r] : 0.f, a.imm[0], a.imm[1], y0, y1);
+        db[a.out_off[0] + row * a.out_ld[0] + col] = y0;
+        if (NOUT == 2) db[a.out_off[1] + row * a.out_ld[1] + col] = y1;
+      }
+    }
+  }
+}
 
 // Work unit u -> (tile t, split s) and its k-block range [kb0, kb0 + nku).
 SPX_DEV void unit_range(const TcArgs& a, int nk, int u, int& t, int& s, int& kb0, int& nku) {
@@ -225,11 +296,13 @@ struct CfgT {
   static constexpr int LSTAGES = LS_;
   static constexpr int LO_OFF = RSTAGES * RAW;      // lo(B) ring
   static constexpr int BAR_OFF = LO_OFF + LSTAGES * B_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  // epilogue staging: one 32 x 33 fp32 transpose tile per drain warp
+  static constexpr int STG_OFF = BAR_OFF + 256;
+  static constexpr int TOTAL = STG_OFF + 4 * 32 * 33 * 4 + 1024;
   static constexpr int TMEM_A = 2 * BN;             // first A column
 };
 
-template <int RS_, int LS_, int CG>
+template <int RS_, int LS_, int CG, int EPI>
 __global__ void __launch_bounds__(NTHREADS_T, 1)
 gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ TcArgs args) {
@@ -310,14 +383,14 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
 
   // Warpgroup roles (setmaxnreg moves registers to the drain warpgroup, whose
   // fp32 promotion accumulators hold a 32 x 128 tile slice per warp):
-  //   WG0  warp 0 TMA producer, warp 1 MMA issuer, warps 2-3 idle   (64 regs)
-  //   WG1, WG2  split, alternating k-blocks (g & 1)                 (112 regs)
-  //   WG3  drain + epilogue                                         (224 regs)
+  //   WG0  warp 0 TMA producer, warp 1 MMA issuer, warps 2-3 idle   (56 regs)
+  //   WG1, WG2  split, alternating k-blocks (g & 1)                 (104 regs)
+  //   WG3  drain + epilogue                                         (240 regs)
   // One split warpgroup per k-block left the tensor core waiting on the
   // split ~1/3 of the time; two alternating groups give each 2 k-blocks of
   // MMA time per k-block of split work.
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     int g = 0;
@@ -470,7 +543,7 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     }
   } else {
     // ---------------- drain + epilogue ----------------
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     const int q = warp & 3;
     int cg = 0;
     for (int u = pair0; u < args.units; u += npairs) {
@@ -479,6 +552,20 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
       tile_coords(args, t, m0, n0, dev, BM * CG);
       m0 += (int)crank * BM;
       const int nchunks = (nku + P - 1) / P;
+      if (EPI == SPX_EPI_ADD || EPI == SPX_EPI_MULSCALE || EPI == SPX_EPI_MOMENTUM) {
+        // pull the epilogue's input rows into L2 while the tile accumulates
+        const int prow = m0 + q * 32 + lane;
+        if (prow < args.M) {
+          const char* db = reinterpret_cast<const char*>(args.base + (uint64_t)((int64_t)dev * args.dev_stride));
+#pragma unroll
+          for (int i = 0; i < (EPI == SPX_EPI_MOMENTUM ? 2 : 1); ++i) {
+            const char* rp = db + 4 * (args.in_off[i] + (int64_t)prow * args.in_ld[i] + n0);
+#pragma unroll
+            for (int l = 0; l < BN * 4 / 128; ++l)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + 128 * l));
+          }
+        }
+      }
       float acc[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = 0.f;
@@ -499,7 +586,40 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
         if (lane == 0) arrive_leader(&tempty[buf]);
       }
       const int row = m0 + q * 32 + lane;
-      if (row < args.M) {
+      if (EPI == SPX_EPI_SQUARE) {
+        // no inputs: row per lane, 16 B stores of C and C * C
+        if (row < args.M) {
+          float* db = reinterpret_cast<float*>(args.base + (uint64_t)((int64_t)dev * args.dev_stride));
+          float* o0 = db + args.out_off[0] + (int64_t)row * args.out_ld[0];
+          float* o1 = db + args.out_off[1] + (int64_t)row * args.out_ld[1];
+          const bool vec = ((args.out_off[0] | args.out_off[1] | args.out_ld[0] | args.out_ld[1] | n0) & 3) == 0;
+#pragma unroll
+          for (int cc = 0; cc < BN / 32; ++cc) {
+            const int col0 = n0 + cc * 32;
+            if (vec && col0 + 32 <= args.N) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float* ac = acc + cc * 32 + 4 * j;
+                *reinterpret_cast<float4*>(o0 + col0 + 4 * j) = make_float4(ac[0], ac[1], ac[2], ac[3]);
+                *reinterpret_cast<float4*>(o1 + col0 + 4 * j) =
+                    make_float4(f_mul(ac[0], ac[0]), f_mul(ac[1], ac[1]), f_mul(ac[2], ac[2]), f_mul(ac[3], ac[3]));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < args.N) {
+                  o0[col0 + j] = acc[cc * 32 + j];
+                  o1[col0 + j] = f_mul(acc[cc * 32 + j], acc[cc * 32 + j]);
+                }
+            }
+          }
+        }
+      } else if (EPI != SPX_EPI_NONE) {
+        // fused epilogue: loads of its inputs want coalesced rows (transpose)
+        float* stg = reinterpret_cast<float*>(smem + S::STG_OFF) + q * 32 * 33;
+        if (m0 + q * 32 < args.M) epi_store_tile<EPI>(args, dev, sp, m0 + q * 32, n0, acc, stg, lane);
+      } else if (row < args.M) {
+        // plain store: row per lane, 16 B per access (fire-and-forget)
         float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
                       ((int64_t)sp * args.M + row) * args.ldc;
 #pragma unroll
@@ -606,6 +726,19 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   a_.c_base = p.base + (uint64_t)(p.c_off * 4);
   a_.dev_stride = p.dev_stride;
   a_.ldc = p.ldc;
+  a_.base = p.base;
+  a_.epi = p.epi;
+  for (int i = 0; i < 2; ++i) {
+    a_.in_off[i] = p.epi_in_off[i];
+    a_.in_ld[i] = p.epi_in_ld[i];
+    a_.out_off[i] = p.epi_out_off[i];
+    a_.out_ld[i] = p.epi_out_ld[i];
+    a_.imm[i] = p.epi_imm[i];
+  }
+  if (p.epi != SPX_EPI_NONE && p.splits > 1) {
+    delete g;
+    return spx_set_error("gemm: fused epilogue with split-K");
+  }
   int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
   sms -= sms % g->cg;
   if (sms < g->cg) sms = g->cg;
@@ -615,10 +748,10 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   return 0;
 }
 
-template <int RS_, int LS_, int CG>
-static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
+template <int RS_, int LS_, int CG, int EPI>
+static int launch_tmema_e(const SpxGemmTC* g, cudaStream_t s) {
   static bool attr = false;
-  auto kern = gemm_tc_tmema_kernel<RS_, LS_, CG>;
+  auto kern = gemm_tc_tmema_kernel<RS_, LS_, CG, EPI>;
   if (!attr) {
     SPX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgT<RS_, LS_, CG>::TOTAL));
     attr = true;
@@ -648,6 +781,19 @@ static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
   return 0;
 }
 
+// one kernel instantiation per epilogue (a single kernel holding every
+// epilogue variant was measured slower: its code crowded the other roles)
+template <int RS_, int LS_, int CG>
+static int launch_tmema(const SpxGemmTC* g, cudaStream_t s) {
+  switch (g->args.epi) {
+    case SPX_EPI_ADD: return launch_tmema_e<RS_, LS_, CG, SPX_EPI_ADD>(g, s);
+    case SPX_EPI_SQUARE: return launch_tmema_e<RS_, LS_, CG, SPX_EPI_SQUARE>(g, s);
+    case SPX_EPI_MULSCALE: return launch_tmema_e<RS_, LS_, CG, SPX_EPI_MULSCALE>(g, s);
+    case SPX_EPI_MOMENTUM: return launch_tmema_e<RS_, LS_, CG, SPX_EPI_MOMENTUM>(g, s);
+    default: return launch_tmema_e<RS_, LS_, CG, SPX_EPI_NONE>(g, s);
+  }
+}
+
 int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
   static int pipe = -1;
   if (pipe < 0) {
@@ -657,7 +803,6 @@ int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
   int rc;
   if (g->cg == 2) {
     switch (pipe) {
-      case 84: rc = launch_tmema<8, 4, 2>(g, s); break;
       case 53: rc = launch_tmema<5, 3, 2>(g, s); break;
       default: rc = launch_tmema<6, 4, 2>(g, s);
     }

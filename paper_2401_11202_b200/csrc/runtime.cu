@@ -316,6 +316,7 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
     if (g.path == 1 && !tc_ok) return spx_set_error("gemm %dx%dx%d: tcgen05 path requested but operands unsupported", g.M, g.N, g.K);
     r.path = (g.path == 2 || (g.path == 0 && !tc_ok)) ? 2 : 1;
     if (g.splits > 1 && r.path != 1) return spx_set_error("gemm %dx%dx%d: split-K needs the tcgen05 path", g.M, g.N, g.K);
+    if (g.epi != SPX_EPI_NONE && r.path != 1) return spx_set_error("gemm %dx%dx%d: fused epilogue needs the tcgen05 path", g.M, g.N, g.K);
   }
   P->recs.push_back(std::move(r));
   return 0;

@@ -358,9 +358,13 @@ class Executable:
             for b in k.ins:
                 readers.setdefault(b, []).append(i)
 
+        results = set(c.result_bufs)
+
         def off_critical(i, side):
             rd = [j for b in ks[i].outs for j in readers.get(b, [])]
-            return bool(rd) and all(self._terminal(ks[j]) or j in side for j in rd)
+            if not rd:       # writes only results (a GEMM with a fused update)
+                return all(b in results for b in ks[i].outs)
+            return all(self._terminal(ks[j]) or j in side for j in rd)
 
         side: dict = {}
         crit_coll = os.environ.get("SPX_SIDE_ALL_COLLECTIVES", "0") == "1"
@@ -523,6 +527,18 @@ class Executable:
         p.splits = d.get("splits", 1)
         if p.splits > 1:
             p.path = 1                       # split-K partials exist on the tcgen05 path only
+        epi = d.get("epi")
+        if epi is not None:
+            p.path = 1                       # fused epilogues exist on the tcgen05 path only
+            p.epi = epi["kind"]
+            for j, x in enumerate(epi["xs"]):
+                p.epi_in_off[j] = self.off[x.buf] + x.off
+                p.epi_in_ld[j] = x.strides[0]
+            for j, o in enumerate(epi["outs"]):
+                p.epi_out_off[j] = self.off[o]
+                p.epi_out_ld[j] = d["N"]
+            p.epi_imm[0], p.epi_imm[1] = epi["imm"]
+            p.c_off = self.off[epi["outs"][0]]
         # with collectives overlapped on a side stream, leave SMs for NCCL's CTAs
         p.reserve_sms = self.reserve_sms
         self._records.append((R.K_GEMM, p))

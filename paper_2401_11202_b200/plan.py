@@ -221,6 +221,7 @@ class Compiler:
         for r in f.results:
             self.result_bufs.append(self.materialize(r))
         self._merge_ew()
+        self._fuse_epilogues()
         return self
 
     def _lower(self, i, op, uses):
@@ -333,7 +334,8 @@ class Compiler:
         splits = self._splitk(M, N, K, aoff, lda, boff, ldb)
         if splits == 1:
             k = Kernel("gemm", [out], {ab, bb}, op_index=i,
-                       data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt), splits=1))
+                       data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt), splits=1,
+                                 tc_ok=self._tc_ok(M, N, K, aoff, lda, boff, ldb)))
             self.kernels.append(k)
         else:
             # split-K: partial products into a [splits, M, N] workspace, summed
@@ -350,12 +352,16 @@ class Compiler:
 
     NUM_SMS = 148
 
+    @staticmethod
+    def _tc_ok(M, N, K, aoff, lda, boff, ldb) -> bool:
+        """The runtime's tcgen05 eligibility (gemm_tc.cu: spx_gemm_tc_supported)."""
+        return (M >= 64 and N >= 32 and K >= 32 and aoff % 4 == 0 and boff % 4 == 0
+                and lda % 4 == 0 and ldb % 4 == 0)
+
     def _splitk(self, M, N, K, aoff, lda, boff, ldb) -> int:
         """Split K when the output has too few 128x128 tiles to fill the SMs
         (weight gradients: K = batch or N*H*W) and the tcgen05 path applies."""
-        tc_ok = (M >= 64 and N >= 32 and K >= 32 and aoff % 4 == 0 and boff % 4 == 0
-                 and lda % 4 == 0 and ldb % 4 == 0)
-        if not tc_ok:
+        if not self._tc_ok(M, N, K, aoff, lda, boff, ldb):
             return 1
         # SM units: the tcgen05 kernel computes 256 x 128 tiles on CTA pairs
         units = -(-M // 256) * 2 * -(-N // 128) * len(self.devices)
@@ -469,6 +475,62 @@ class Compiler:
         self.kernels.append(kern)
         self.desc[r] = Desc("buf", dims, buf=out)
 
+    # ----------------------------------------------------- GEMM epilogues
+    def _fuse_epilogues(self):
+        """Fold the elementwise consumer of a GEMM output into the GEMM's
+        epilogue (residual add, square activation and its backward, the
+        momentum update of a weight gradient): the accumulator rows are
+        transformed before they leave the SM, so the product is never written
+        and re-read.  Off by default (SPX_EPILOGUE=1 enables): measured on the
+        C2 step, the separate elementwise kernels -- HBM-bound, overlapped with
+        the GEMMs by PDL and the side streams -- cost less than the epilogue's
+        extra work on the 4 drain warps (their input loads cannot reach HBM
+        bandwidth with so little memory-level parallelism per SM).  See
+        DESIGN.md, "GEMM epilogue fusion"."""
+        import os
+        if os.environ.get("SPX_EPILOGUE", "0") == "0":
+            return
+        kinds = {int(x) for x in os.environ.get("SPX_EPILOGUE_KINDS", "1,2,3,4").split(",") if x}
+        ks = self.kernels
+        readers: dict = {}
+        producer = {}
+        for idx, k in enumerate(ks):
+            for b in k.ins:
+                readers.setdefault(b, []).append(idx)
+            for b in k.outs:
+                producer[b] = idx
+        results = set(self.result_bufs)
+        for gi, G in enumerate(ks):
+            if G.kind != "gemm" or G.data.get("splits", 1) != 1 or not G.data.get("tc_ok"):
+                continue
+            C = G.outs[0]
+            M, N = G.data["M"], G.data["N"]
+            rd = sorted(r for r in readers.get(C, []) if ks[r].alive)
+            if not rd or ks[rd[0]].kind != "ew" or tuple(ks[rd[0]].data["dims"]) != (M, N):
+                continue
+            E = ks[rd[0]]
+            outs = list(E.data.get("outs_keep", E.outs))
+            m = _match_epilogue(E.data["exprs"], outs, C, M, N)
+            if m is None:
+                continue
+            epi, xs, imm, gouts = m
+            if epi not in kinds:
+                continue
+            keep_c = C in results or len(rd) > 1
+            if keep_c and epi != R.EPI_SQUARE:
+                continue
+            if any(producer.get(x.buf, -1) > gi for x in xs):
+                continue                   # an input is produced after the GEMM
+            G.data["epi"] = dict(kind=epi, xs=xs, imm=imm, outs=gouts)
+            G.outs = list(gouts)
+            G.ins = set(G.ins) | {x.buf for x in xs}
+            E.alive = False
+            for b in gouts:
+                producer[b] = gi
+            for x in xs:
+                readers.setdefault(x.buf, []).append(gi)
+        self.kernels = [k for k in ks if k.alive]
+
     # ------------------------------------------------------ multi-output merge
     def _merge_ew(self):
         """Merge an EW kernel into a later EW kernel that reads one of its outputs
@@ -535,6 +597,74 @@ class Compiler:
                 keep = X.outs[-1:]
             X.data["outs_keep"] = keep
         self.kernels = [kk for kk in ks if kk.alive]
+
+
+def _is_const(e):
+    return isinstance(e, (np.float32, float))
+
+
+def _match_epilogue(exprs: dict, outs: list, C: str, M: int, N: int):
+    """Recognise the elementwise consumer of a GEMM output C as one of the
+    fused epilogues (include/spindle_b200.h, spx_epilogue).  Returns
+    (epi, [input leaves], [imm], [output buffers]) or None.  Only exact
+    structural matches: the fused kernel performs the same IEEE operations
+    in the same association (add/mul operand order is immaterial -- IEEE
+    addition and multiplication are commutative)."""
+    def is_c(e):
+        return isinstance(e, Leaf) and e.buf == C and e.off == 0 and tuple(e.strides) == (N, 1)
+
+    def is_x(e):
+        return (isinstance(e, Leaf) and e.buf != C and len(e.strides) == 2 and e.strides[1] == 1
+                and e.off % 4 == 0 and e.strides[0] % 4 == 0)
+
+    def node(e, op):
+        return isinstance(e, Node) and e.op == op
+
+    def pair(e, op, f, g):
+        """e = op(a, b) with f(a) and g(b) in either order -> (a, b) or None."""
+        if not node(e, op) or len(e.kids) != 2:
+            return None
+        a, b = e.kids
+        if f(a) and g(b):
+            return a, b
+        if f(b) and g(a):
+            return b, a
+        return None
+
+    def scaled(e):
+        """e = x * k (either order) -> (x leaf, k) or None."""
+        m = pair(e, "mul", is_x, _is_const)
+        return (m[0], float(m[1])) if m else None
+
+    if len(outs) == 1:
+        e = exprs[outs[0]]
+        m = pair(e, "add", is_c, is_x)
+        if m:
+            return R.EPI_ADD, [m[1]], [0.0, 0.0], [outs[0]]
+        if node(e, "mul") and len(e.kids) == 2 and is_c(e.kids[0]) and is_c(e.kids[1]):
+            return R.EPI_SQUARE, [], [0.0, 0.0], [C, outs[0]]
+        m = pair(e, "mul", is_c, lambda q: scaled(q) is not None)
+        if m:
+            x, k = scaled(m[1])
+            return R.EPI_MULSCALE, [x], [k, 0.0], [outs[0]]
+        return None
+    if len(outs) == 2:
+        for mo, po in ((outs[0], outs[1]), (outs[1], outs[0])):
+            em, ep = exprs[mo], exprs[po]
+            m = pair(em, "add", lambda q: scaled(q) is not None, is_c)
+            if not m:
+                continue
+            mx, k0 = scaled(m[0])
+            # p' = P + -(m' * k1)
+            pp = pair(ep, "add", is_x, lambda q: node(q, "neg"))
+            if not pp:
+                continue
+            inner = pp[1].kids[0]
+            mm = pair(inner, "mul", lambda q: q is em or q == em, _is_const)
+            if not mm:
+                continue
+            return R.EPI_MOMENTUM, [mx, pp[0]], [k0, float(mm[1])], [mo, po]
+    return None
 
 
 def _substitute(e, sub, contig, memo):

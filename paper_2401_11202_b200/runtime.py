@@ -58,7 +58,14 @@ class GemmParams(C.Structure):
                 ("lda", C.c_int64), ("ldb", C.c_int64), ("ldc", C.c_int64),
                 ("a_mn_major", C.c_int32), ("b_k_major", C.c_int32),
                 ("path", C.c_int32), ("promote", C.c_int32), ("reserve_sms", C.c_int32),
-                ("splits", C.c_int32)]
+                ("splits", C.c_int32),
+                ("epi", C.c_int32), ("epi_pad", C.c_int32),
+                ("epi_in_off", C.c_int64 * 2), ("epi_in_ld", C.c_int64 * 2),
+                ("epi_out_off", C.c_int64 * 2), ("epi_out_ld", C.c_int64 * 2),
+                ("epi_imm", C.c_float * 2)]
+
+
+EPI_NONE, EPI_ADD, EPI_SQUARE, EPI_MULSCALE, EPI_MOMENTUM = 0, 1, 2, 3, 4
 
 
 class GatherParams(C.Structure):

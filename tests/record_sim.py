@@ -118,9 +118,36 @@ class Sim:
                 nk = -(-g.K // 32)
                 k0, k1 = min(g.K, 32 * ((nk * sp) // S)), min(g.K, 32 * ((nk * (sp + 1)) // S))
                 C = (A[:, k0:k1].astype(np.float64) @ B[k0:k1].astype(np.float64)).astype(np.float32)
+                if g.epi != R.EPI_NONE:
+                    self._epilogue(g, p, C)
+                    continue
                 for m in range(g.M):
                     s = self.dev_base(p) + g.c_off + (sp * g.M + m) * g.ldc
                     self.arena[s:s + g.N] = C[m]
+
+    def _epilogue(self, g, p, C):
+        """The fused GEMM epilogues (spindle_b200.h spx_epilogue), float32 ops."""
+        f32 = np.float32
+        X = [self.gather_view(p, g.epi_in_off[j], (g.epi_in_ld[j], 1), (g.M, g.N)) for j in range(2)
+             if g.epi_in_ld[j] > 0]
+        k0, k1 = f32(g.epi_imm[0]), f32(g.epi_imm[1])
+        with np.errstate(all="ignore"):
+            if g.epi == R.EPI_ADD:
+                Y = [X[0] + C]
+            elif g.epi == R.EPI_SQUARE:
+                Y = [C, C * C]
+            elif g.epi == R.EPI_MULSCALE:
+                Y = [C * (X[0] * k0)]
+            elif g.epi == R.EPI_MOMENTUM:
+                m = X[0] * k0 + C
+                Y = [m, X[1] + -(m * k1)]
+            else:
+                raise AssertionError(g.epi)
+        for j, y in enumerate(Y):
+            y = np.asarray(y, dtype=np.float32)
+            for r in range(g.M):
+                s = self.dev_base(p) + g.epi_out_off[j] + r * g.epi_out_ld[j]
+                self.arena[s:s + g.N] = y[r]
 
     def run_gather(self, g: R.GatherParams):
         dims = [g.dims[k] for k in range(g.rank)]

@@ -227,3 +227,31 @@ def test_elementwise_static_catalog_bitexact(static, monkeypatch):
     want = O.interpret(m, ins)
     for g, w in zip(got, want):
         np.testing.assert_array_equal(g, w)
+
+
+@pytest.mark.parametrize("epi", [1, 2, 3, 4])
+def test_gemm_fused_epilogue_bitexact(epi, monkeypatch):
+    """A GEMM with its elementwise consumer fused into the epilogue gives
+    bit-identical results to the GEMM followed by the separate elementwise
+    kernel (same accumulation, same IEEE ops), and matches the oracle."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_plan_cpu import EPILOGUE_PROGRAMS
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.executable import Executable
+    m = pkg.parse_module(EPILOGUE_PROGRAMS[epi])
+    monkeypatch.setenv("SPX_EPILOGUE", "1")
+    ex = Executable(m, devices=[0], dry=True)
+    assert [p.epi for k, p in ex.records() if k == R.K_GEMM] == [epi]
+    rng = np.random.default_rng(epi)
+    ins = {n: rng.standard_normal(t.dims).astype(np.float32) for n, t in m.func("main").args}
+    monkeypatch.setenv("SPX_EPILOGUE", "1")
+    fused = pkg.interpret(m, ins)
+    monkeypatch.setenv("SPX_EPILOGUE", "0")
+    plain = pkg.interpret(m, ins)
+    want = O.interpret(m, ins)
+    for f, p, w in zip(fused, plain, want):
+        np.testing.assert_array_equal(f, p)
+        assert np.all(np.isfinite(f)) and O.relative_error(f, w) < TOL

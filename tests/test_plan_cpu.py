@@ -101,3 +101,66 @@ def test_split_k_gemm_sim():
            "b": rng.standard_normal((4096, 256)).astype(np.float32)}
     got, _ = sim_dense(m, ins)
     assert relative_error(got[0], ins["a"].T.astype(np.float64) @ ins["b"]) < TOL
+
+
+EPILOGUE_PROGRAMS = {
+    # residual add: out = x + A.B
+    1: """func @main(%a: tensor<256x128xf32>, %b: tensor<128x256xf32>, %x: tensor<256x256xf32>) -> tensor<256x256xf32> {
+  %c = matmul %a, %b : tensor<256x256xf32>
+  %o = add %x, %c : tensor<256x256xf32>
+  return %o
+}
+""",
+    # square activation, product kept for a later reader
+    2: """func @main(%a: tensor<256x128xf32>, %b: tensor<128x256xf32>, %x: tensor<256x256xf32>) -> (tensor<256x256xf32>, tensor<256x256xf32>) {
+  %c = matmul %a, %b : tensor<256x256xf32>
+  %s = mul %c, %c : tensor<256x256xf32>
+  %u = mul %c, %x : tensor<256x256xf32>
+  return %s, %u
+}
+""",
+    # backward of the square: g = A.B * (x * 2)
+    3: """func @main(%a: tensor<256x128xf32>, %b: tensor<128x256xf32>, %x: tensor<256x256xf32>) -> tensor<256x256xf32> {
+  %c = matmul %a, %b : tensor<256x256xf32>
+  %k = constant 2.0 : tensor<256x256xf32>
+  %x2 = mul %x, %k : tensor<256x256xf32>
+  %o = mul %c, %x2 : tensor<256x256xf32>
+  return %o
+}
+""",
+    # momentum SGD on a weight gradient
+    4: """func @main(%a: tensor<128x256xf32>, %b: tensor<128x256xf32>, %m: tensor<256x256xf32>, %p: tensor<256x256xf32>) -> (tensor<256x256xf32>, tensor<256x256xf32>) {
+  %at = transpose %a {perm = [1, 0]} : tensor<256x128xf32>
+  %g = matmul %at, %b : tensor<256x256xf32>
+  %c1 = constant 0.9 : tensor<256x256xf32>
+  %v = mul %c1, %m : tensor<256x256xf32>
+  %nm = add %v, %g : tensor<256x256xf32>
+  %c2 = constant 0.01 : tensor<256x256xf32>
+  %w = mul %c2, %nm : tensor<256x256xf32>
+  %n = neg %w : tensor<256x256xf32>
+  %np = add %p, %n : tensor<256x256xf32>
+  return %np, %nm
+}
+""",
+}
+
+
+@pytest.mark.parametrize("epi", sorted(EPILOGUE_PROGRAMS))
+def test_gemm_epilogue_fusion_sim(epi, monkeypatch):
+    """Each fused epilogue is recognised (no separate elementwise kernel for
+    the GEMM's consumer) and the fused records reproduce the oracle."""
+    from oracle.spmd_oracle import interpret
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.executable import Executable
+    monkeypatch.setenv("SPX_EPILOGUE", "1")
+    m = parse_module(EPILOGUE_PROGRAMS[epi])
+    ex = Executable(m, devices=[0], dry=True)
+    gem = [p for k, p in ex.records() if k == R.K_GEMM]
+    assert len(gem) == 1 and gem[0].epi == epi
+    rng = np.random.default_rng(epi)
+    f = m.func("main")
+    ins = {n: rng.standard_normal(t.dims).astype(np.float32) for n, t in f.args}
+    got, _ = sim_dense(m, ins)
+    want = interpret(m, ins)
+    for g, w in zip(got, want):
+        assert relative_error(g, w) < TOL
