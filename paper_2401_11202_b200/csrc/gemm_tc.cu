@@ -159,6 +159,7 @@ struct TcArgs {
   int64_t ldc;
   // fused epilogue (spx_gemm_params.epi*): offsets in elements from base
   uint64_t base;
+  int tma_store;       // plain C stores through the tensor map (else row stores)
   int epi;
   int64_t in_off[2], in_ld[2], out_off[2], out_ld[2];
   float imm[2];
@@ -296,16 +297,18 @@ struct CfgT {
   static constexpr int LSTAGES = LS_;
   static constexpr int LO_OFF = RSTAGES * RAW;      // lo(B) ring
   static constexpr int BAR_OFF = LO_OFF + LSTAGES * B_BYTES;
-  // epilogue staging: one 32 x 33 fp32 transpose tile per drain warp
-  static constexpr int STG_OFF = BAR_OFF + 256;
-  static constexpr int TOTAL = STG_OFF + 4 * 32 * 33 * 4 + 1024;
+  // epilogue staging per drain warp: two 32 x 32 fp32 tiles (128B-swizzled
+  // TMA-store sources), or one 32 x 33 transpose tile for fused epilogues
+  static constexpr int STG_OFF = (BAR_OFF + 256 + 1023) / 1024 * 1024;
+  static constexpr int STG_WARP = 8192;
+  static constexpr int TOTAL = STG_OFF + 4 * STG_WARP + 1024;
   static constexpr int TMEM_A = 2 * BN;             // first A column
 };
 
 template <int RS_, int LS_, int CG, int EPI>
 __global__ void __launch_bounds__(NTHREADS_T, 1)
 gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                     const __grid_constant__ TcArgs args) {
+                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ TcArgs args) {
   using S = CfgT<RS_, LS_, CG>;
   constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -616,8 +619,45 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
         }
       } else if (EPI != SPX_EPI_NONE) {
         // fused epilogue: loads of its inputs want coalesced rows (transpose)
-        float* stg = reinterpret_cast<float*>(smem + S::STG_OFF) + q * 32 * 33;
+        float* stg = reinterpret_cast<float*>(smem + S::STG_OFF + q * S::STG_WARP);
         if (m0 + q * 32 < args.M) epi_store_tile<EPI>(args, dev, sp, m0 + q * 32, n0, acc, stg, lane);
+      } else if (args.tma_store) {
+        // plain store through TMA: each 32-row x 32-column slice goes to a
+        // 128B-swizzled staging tile (conflict-free float4 writes, lane = row)
+        // and leaves the SM as one bulk tensor store
+        uint8_t* stg = smem + S::STG_OFF + q * S::STG_WARP;
+        const int rowc = sp * args.M + m0 + q * 32;
+        const bool rows_in = m0 + q * 32 < args.M;
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          // every staged slice is stored and committed as one bulk group, so
+          // wait_group.read 1 below really frees the buffer of slice cc - 2
+          if (!rows_in || n0 + cc * 32 >= args.N) break;
+          uint8_t* t = stg + (cc & 1) * 4096;
+          if (cc >= 2) {
+            // the store issued from this buffer two slices ago must have read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(t + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
+                            acc[cc * 32 + 4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tma_c)),
+                "r"(n0 + cc * 32), "r"(rowc), "r"(dev), "r"(smem_u32(t))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        // staging is reused by the next tile: all of this tile's stores must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
       } else if (row < args.M) {
         // plain store: row per lane, 16 B per access (fire-and-forget)
         float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
@@ -640,6 +680,7 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
       }
     }
   }
+  if (warp >= 12 && args.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   // CG == 2: neither CTA leaves while its peer may still arrive on its barriers
   // or the pair's MMAs may still read its shared memory / TMEM
@@ -686,7 +727,7 @@ int make_map(CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer, ui
 }  // namespace
 
 struct SpxGemmTC {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   TcArgs args;
   dim3 grid;
   int cg;              // CTAs per tile (1, or 2 = cluster pair with cta_group::2 MMAs)
@@ -728,6 +769,23 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
   a_.ldc = p.ldc;
   a_.base = p.base;
   a_.epi = p.epi;
+  // TMA stores of C: 16B-aligned base and pitch; with split-K the partial
+  // slabs are stacked rows, so a 32-row box must not straddle two of them
+  a_.tma_store = 0;
+  {
+    const char* e = getenv("SPX_GEMM_TMA_STORE");
+    const bool want = !(e && e[0] == '0');
+    const bool ok = (a_.c_base & 15) == 0 && (p.ldc & 3) == 0 && (p.dev_stride & 15) == 0 &&
+                    (a_.splits == 1 || p.M % 32 == 0);
+    if (want && ok && p.epi == SPX_EPI_NONE) {
+      if (make_map(&g->mc, a_.c_base, p.N, (uint64_t)p.M * a_.splits, p.ndev, p.ldc * 4, p.dev_stride, 32, false)) {
+        delete g;
+        return -1;
+      }
+      a_.tma_store = 1;
+    }
+  }
+  if (!a_.tma_store) memset(&g->mc, 0, sizeof(g->mc));
   for (int i = 0; i < 2; ++i) {
     a_.in_off[i] = p.epi_in_off[i];
     a_.in_ld[i] = p.epi_in_ld[i];
@@ -777,7 +835,7 @@ static int launch_tmema_e(const SpxGemmTC* g, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  SPX_CUDA(cudaLaunchKernelEx(&cfg, kern, g->ma, g->mb, g->args));
+  SPX_CUDA(cudaLaunchKernelEx(&cfg, kern, g->ma, g->mb, g->mc, g->args));
   return 0;
 }
 
@@ -808,8 +866,7 @@ int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch) {
     }
   } else {
     switch (pipe) {
-      case 44: rc = launch_tmema<4, 4, 1>(g, s); break;
-      default: rc = launch_tmema<5, 3, 1>(g, s);
+      default: rc = launch_tmema<4, 4, 1>(g, s);
     }
   }
   if (rc) return rc;

@@ -10,7 +10,9 @@ rng = np.random.default_rng(0)
 print("SPX_GEMM_PIPE", os.environ.get("SPX_GEMM_PIPE"))
 SHAPES = [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
           (1024, 1024, 2048, True, False), (4096, 4096, 4096, False, False),
-          (1024, 2048, 1024, False, False), (1024, 1024, 1024, True, False), (2048, 1024, 1024, False, False)]
+          (1024, 2048, 1024, False, False), (1024, 1024, 1024, True, False), (2048, 1024, 1024, False, False),
+          (1024, 512, 1024, False, False), (1024, 1024, 512, False, False), (1024, 1024, 2048, False, False),
+          (1024, 256, 1024, False, False), (1024, 1024, 256, False, False)]
 if os.environ.get("SHAPES"):
     SHAPES = [SHAPES[int(i)] for i in os.environ["SHAPES"].split(",")]
 for (M, N, K, at, bt) in SHAPES:
