@@ -17,18 +17,27 @@ reference's own CLI dumps (`cli.py:79-91`):
 This is the "cached artefact format" of SURVEY.md §8(f) rank 2: partitioning
 deep models takes minutes to hours, evaluating them does not.
 
-usage: PYTHONPATH=/root/reference/pkg/src python tools/make_programs.py NAME [NAME...]
+Partitioning runs under `fast_partitioning()` (paper_2401_11202_b200/fastpart.py:
+indexed find_def/collect_uses, identical output); --slow uses the reference as is.
+
+usage: PYTHONPATH=/root/reference/pkg/src python tools/make_programs.py [--slow] NAME [NAME...]
        PYTHONPATH=/root/reference/pkg/src python tools/make_programs.py --list
 """
 from __future__ import annotations
 
+import contextlib
 import json
 import os
 import sys
 import time
 
-OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                   "paper_2401_11202_b200", "programs")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2401_11202_b200.fastpart import fast_partitioning  # noqa: E402
+
+SLOW = False
+
+OUT = os.environ.get("SPX_PROGRAMS_OUT") or os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2401_11202_b200", "programs")
 
 TF_C2 = dict(blocks=8, batch=2048, d_model=1024, d_ff=4096)
 TF_C3 = dict(blocks=32, batch=8192, d_model=2048, d_ff=8192)
@@ -90,12 +99,15 @@ def make(name: str):
         module.mesh = Mesh.parse(mesh)
         t0 = time.perf_counter()
         p = Partitioner(module)
-        for t in schedule(stages, module):
-            p.apply(t)
-        for ax, s in extra:
-            p.apply(ManualPartition(ax, dict(s)))
+        ctx = contextlib.nullcontext() if SLOW else fast_partitioning()
+        with ctx:
+            for t in schedule(stages, module):
+                p.apply(t)
+            for ax, s in extra:
+                p.apply(ManualPartition(ax, dict(s)))
         ex = p.export()
         meta["partition_s"] = time.perf_counter() - t0
+        meta["partitioner"] = "reference" if SLOW else "reference + fastpart index"
         meta["counts"] = ex["counts"]
         meta["cost"] = ex["cost"]
         meta["conflicts"] = sum(len(r["conflicts"]) for r in ex["reports"])
@@ -115,5 +127,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["--list"]:
         print("\n".join(CONFIGS))
         sys.exit(0)
-    for n in sys.argv[1:]:
+    names = sys.argv[1:]
+    if "--slow" in names:
+        SLOW = True
+        names.remove("--slow")
+    for n in names:
         make(n)
