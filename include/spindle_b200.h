@@ -200,6 +200,7 @@ int spx_malloc(uint64_t bytes, uint64_t* out_ptr);  /* arena (cudaMalloc) */
 int spx_free(uint64_t ptr);
 int spx_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream);
 int spx_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, uint64_t stream);
+int spx_memcpy_d2d(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream);
 int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream);
 int spx_host_alloc(uint64_t bytes, void** out_ptr); /* pinned host memory */
 int spx_host_free(void* ptr);
@@ -238,6 +239,7 @@ int spx_plan_record_info(uint64_t plan, int index, int* kind, int* path);
 /* timing helpers (CUDA events on the given stream) */
 int spx_event_create(uint64_t* out_event);
 int spx_event_record(uint64_t event, uint64_t stream);
+int spx_stream_wait_event(uint64_t stream, uint64_t event);   /* later work on `stream` waits */
 int spx_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms);
 int spx_event_destroy(uint64_t event);
 

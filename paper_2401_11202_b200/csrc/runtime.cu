@@ -220,6 +220,11 @@ int spx_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, uint64_t stream) {
                            reinterpret_cast<cudaStream_t>(stream)));
   return 0;
 }
+int spx_memcpy_d2d(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream) {
+  SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst), reinterpret_cast<const void*>(src), bytes,
+                           cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
 int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream) {
   SPX_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(dst), value, bytes, reinterpret_cast<cudaStream_t>(stream)));
   return 0;
@@ -464,6 +469,10 @@ int spx_event_create(uint64_t* out) {
 }
 int spx_event_record(uint64_t ev, uint64_t stream) {
   SPX_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+int spx_stream_wait_event(uint64_t stream, uint64_t ev) {
+  SPX_CUDA(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<cudaEvent_t>(ev), 0));
   return 0;
 }
 int spx_event_elapsed_ms(uint64_t a, uint64_t b, float* out) {

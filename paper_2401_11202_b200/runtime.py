@@ -107,6 +107,7 @@ EXPORTS = [
     "spx_plan_create", "spx_plan_add", "spx_plan_finalize", "spx_plan_run", "spx_plan_capture",
     "spx_plan_replay", "spx_plan_launch_count", "spx_plan_destroy", "spx_plan_record_info",
     "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
+    "spx_stream_wait_event", "spx_memcpy_d2d",
     "spx_plan_profile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
     "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
 ]
@@ -145,6 +146,8 @@ def load(build_if_missing: bool = True):
         "spx_plan_launch_count": [C.c_uint64], "spx_plan_destroy": [C.c_uint64],
         "spx_plan_record_info": [C.c_uint64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "spx_event_create": [u64p], "spx_event_record": [C.c_uint64, C.c_uint64],
+        "spx_stream_wait_event": [C.c_uint64, C.c_uint64],
+        "spx_memcpy_d2d": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64],
         "spx_event_elapsed_ms": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float)],
         "spx_event_destroy": [C.c_uint64],
         "spx_plan_profile": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float), C.c_int],
@@ -220,8 +223,23 @@ class Device:
         call(self.lib.spx_event_create, C.byref(e))
         return e.value
 
-    def record(self, ev: int):
-        call(self.lib.spx_event_record, ev, self.stream)
+    def record(self, ev: int, stream: int | None = None):
+        call(self.lib.spx_event_record, ev, self.stream if stream is None else stream)
+
+    def new_stream(self) -> int:
+        s = C.c_uint64()
+        call(self.lib.spx_stream_create, C.byref(s))
+        return s.value
+
+    def wait(self, ev: int, stream: int | None = None):
+        """Work issued later on `stream` (default: the device stream) waits for `ev`."""
+        call(self.lib.spx_stream_wait_event, self.stream if stream is None else stream, ev)
+
+    def h2d_async(self, dst: int, arr: np.ndarray, stream: int):
+        call(self.lib.spx_memcpy_h2d, dst, arr.ctypes.data, arr.nbytes, stream)
+
+    def d2d(self, dst: int, src: int, nbytes: int, stream: int | None = None):
+        call(self.lib.spx_memcpy_d2d, dst, src, nbytes, self.stream if stream is None else stream)
 
     def elapsed_ms(self, a: int, b: int) -> float:
         out = C.c_float()

@@ -172,7 +172,42 @@ class Session:
     def capture(self):
         self.ex.plan.capture()
 
+    # -- input pipeline -----------------------------------------------------
+    def feed(self, host: dict):
+        """Stage the NEXT step's inputs: `host[name]` are pinned host arrays of
+        local (already sharded) args; they go host->device on a copy stream
+        into one of two staging slots, overlapping the step that is running.
+        The next `step()` waits for the copy, moves the slot into the arg
+        buffers (device-to-device) and runs.  Hosted device 0 (nccl mode:
+        this rank's device)."""
+        dev = self.device
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = dev.new_stream()
+            self._stage = {}
+            self._ready = [dev.event(), dev.event()]
+            self._consumed = [dev.event(), dev.event()]
+            self._fed = 0
+            self._pending = []
+        slot = self._fed % 2
+        if self._fed >= 2:
+            # the slot's previous batch must have been moved into the args
+            dev.wait(self._consumed[slot], self._copy_stream)
+        for nm, arr in host.items():
+            if nm not in self._stage:
+                self._stage[nm] = (dev.malloc(arr.nbytes), dev.malloc(arr.nbytes), arr.nbytes)
+            dev.h2d_async(self._stage[nm][slot], arr, self._copy_stream)
+        dev.record(self._ready[slot], self._copy_stream)
+        self._pending.append((slot, list(host)))
+        self._fed += 1
+
     def step(self):
+        if getattr(self, "_pending", None):
+            slot, names = self._pending.pop(0)
+            dev = self.device
+            dev.wait(self._ready[slot])
+            for nm in names:
+                dev.d2d(self.arg_addr(nm), self._stage[nm][slot], self._stage[nm][2])
+            dev.record(self._consumed[slot])
         self.ex.plan.replay()
 
     def sync(self):

@@ -255,3 +255,42 @@ def test_gemm_fused_epilogue_bitexact(epi, monkeypatch):
     for f, p, w in zip(fused, plain, want):
         np.testing.assert_array_equal(f, p)
         assert np.all(np.isfinite(f)) and O.relative_error(f, w) < TOL
+
+
+def test_session_feed_pipeline():
+    """Session.feed stages the next batch on a copy stream; step() consumes it
+    in order -- results equal loading the same batch synchronously."""
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.session import Session
+    text = """func @main(%x: tensor<256x512xf32>, %w: tensor<512x256xf32>) -> tensor<256x256xf32> {
+  %c = matmul %x, %w : tensor<256x256xf32>
+  %o = add %c, %c : tensor<256x256xf32>
+  return %o
+}
+"""
+    m = pkg.parse_module(text)
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal((512, 256)).astype(np.float32)
+    xs = [rng.standard_normal((256, 512)).astype(np.float32) for _ in range(3)]
+    sess = Session(m)
+    sess.load({"x": xs[0], "w": w})
+    sess.capture()
+    dev = sess.device
+    pins = []
+    for x in xs:
+        p = dev.pinned(x.shape)
+        p[...] = x
+        pins.append(p)
+    sess.feed({"x": pins[0]})
+    got = []
+    for i in range(3):
+        if i + 1 < 3:
+            sess.feed({"x": pins[i + 1]})
+        sess.step()
+        sess.sync()
+        got.append(sess.results()[0][0].copy())
+    for x, g in zip(xs, got):
+        want = O.interpret(m, {"x": x, "w": w})[0]
+        assert O.relative_error(g, want) < TOL
+    sess.close()
