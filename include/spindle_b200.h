@@ -114,7 +114,8 @@ typedef struct {
   int32_t path;                   /* 0 auto, 1 tcgen05 3xTF32, 2 SIMT fp32     */
   int32_t promote;                /* k-blocks per TMEM chunk (0 = default 4)     */
   int32_t reserve_sms;            /* SMs left free for concurrent collectives    */
-  int32_t splits;                 /* split-K: >1 writes [splits][M][ldc] partials at c_off */
+  int32_t splits;                 /* split-K: >1 writes [splits][M][ldc] partials at c_off
+                                     (sk_mode 0), or reduces them in the kernel (sk_mode 1) */
   /* Fused epilogue (tcgen05 path, splits == 1): the elementwise consumer of
    * C = A.B computed on the accumulator rows before they leave the SM, with
    * the same IEEE operations (and order) as the unfused kernel:
@@ -130,6 +131,14 @@ typedef struct {
   int64_t epi_in_off[2], epi_in_ld[2];
   int64_t epi_out_off[2], epi_out_ld[2];
   float epi_imm[2];
+  /* In-kernel split-K (sk_mode 1, tcgen05 path): the CTAs of split s > 0
+   * store their partial tile into a workspace [splits-1][M][N] at ws_off and
+   * count it into a per-(tile, row slice) flag at flag_off (uint32, zero
+   * between launches); the split-0 CTAs wait for their flags, fold the
+   * partials in split order (deterministic) and write C.  Every work unit
+   * must be co-resident: tiles x splits x 2 <= SM count. */
+  int32_t sk_mode, sk_pad;
+  int64_t ws_off, flag_off;
 } spx_gemm_params;
 
 enum spx_epilogue { SPX_EPI_NONE = 0, SPX_EPI_ADD = 1, SPX_EPI_SQUARE = 2, SPX_EPI_MULSCALE = 3,

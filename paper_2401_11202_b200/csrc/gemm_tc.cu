@@ -160,6 +160,8 @@ struct TcArgs {
   // fused epilogue (spx_gemm_params.epi*): offsets in elements from base
   uint64_t base;
   int tma_store;       // plain C stores through the tensor map (else row stores)
+  int sk_inkernel;     // split-K partials reduced in the kernel (spx_gemm_params.sk_mode)
+  uint64_t ws_base, flag_base;
   int epi;
   int64_t in_off[2], in_ld[2], out_off[2], out_ld[2];
   float imm[2];
@@ -308,7 +310,8 @@ struct CfgT {
 template <int RS_, int LS_, int CG, int EPI>
 __global__ void __launch_bounds__(NTHREADS_T, 1)
 gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ TcArgs args) {
+                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_w,
+                     const __grid_constant__ TcArgs args) {
   using S = CfgT<RS_, LS_, CG>;
   constexpr int RS = S::RSTAGES, LS = S::LSTAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -626,8 +629,53 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
         // 128B-swizzled staging tile (conflict-free float4 writes, lane = row)
         // and leaves the SM as one bulk tensor store
         uint8_t* stg = smem + S::STG_OFF + q * S::STG_WARP;
-        const int rowc = sp * args.M + m0 + q * 32;
         const bool rows_in = m0 + q * 32 < args.M;
+        // in-kernel split-K: split s > 0 stores its partial slice into the
+        // workspace and counts it into the slice's flag; split 0 waits for the
+        // other splits, folds their partials in split order, then stores C
+        const bool sk = args.sk_inkernel && args.splits > 1;
+        uint32_t* flag = reinterpret_cast<uint32_t*>(args.flag_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
+                         ((int64_t)t * CG + crank) * 4 + q;
+        const bool to_ws = sk && sp > 0;
+        const CUtensorMap* map = to_ws ? &tma_w : &tma_c;
+        const int rowc = to_ws ? (sp - 1) * args.M + m0 + q * 32 : (sk ? 0 : sp * args.M) + m0 + q * 32;
+        if (sk && sp == 0 && rows_in) {
+          if (lane == 0) {
+            const uint32_t want = (uint32_t)(args.splits - 1);
+            const long long t0 = clock64();
+            uint32_t v;
+            for (;;) {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+              if (v >= want) break;
+              __nanosleep(64);
+              if (clock64() - t0 > 20000000000LL) __trap();
+            }
+          }
+          __syncwarp();
+          uint32_t v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+          const float* wsd = reinterpret_cast<const float*>(args.ws_base + (uint64_t)((int64_t)dev * args.dev_stride));
+          const int rrow = m0 + q * 32 + lane;
+          for (int s2 = 1; s2 < args.splits; ++s2) {
+            const float* wr = wsd + ((int64_t)(s2 - 1) * args.M + rrow) * args.N;
+#pragma unroll
+            for (int cc = 0; cc < BN / 32; ++cc) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int c = n0 + cc * 32 + 4 * j;
+                if (rrow < args.M && c < args.N) {
+                  const float4 w = __ldcg(reinterpret_cast<const float4*>(wr + c));
+                  acc[cc * 32 + 4 * j] = __fadd_rn(acc[cc * 32 + 4 * j], w.x);
+                  acc[cc * 32 + 4 * j + 1] = __fadd_rn(acc[cc * 32 + 4 * j + 1], w.y);
+                  acc[cc * 32 + 4 * j + 2] = __fadd_rn(acc[cc * 32 + 4 * j + 2], w.z);
+                  acc[cc * 32 + 4 * j + 3] = __fadd_rn(acc[cc * 32 + 4 * j + 3], w.w);
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) *flag = 0u;      // consumed: ready for the next launch
+        }
 #pragma unroll
         for (int cc = 0; cc < BN / 32; ++cc) {
           // every staged slice is stored and committed as one bulk group, so
@@ -649,11 +697,21 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
           if (lane == 0) {
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tma_c)),
+                    reinterpret_cast<uint64_t>(map)),
                 "r"(n0 + cc * 32), "r"(rowc), "r"(dev), "r"(smem_u32(t))
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
+        }
+        if (to_ws && rows_in) {
+          // the partial must be in memory before the owner is told
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+          }
+          __syncwarp();
         }
         // staging is reused by the next tile: all of this tile's stores must have read it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -727,7 +785,7 @@ int make_map(CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer, ui
 }  // namespace
 
 struct SpxGemmTC {
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb, mc, mw;
   TcArgs args;
   dim3 grid;
   int cg;              // CTAs per tile (1, or 2 = cluster pair with cta_group::2 MMAs)
@@ -778,7 +836,8 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
     const bool ok = (a_.c_base & 15) == 0 && (p.ldc & 3) == 0 && (p.dev_stride & 15) == 0 &&
                     (a_.splits == 1 || p.M % 32 == 0);
     if (want && ok && p.epi == SPX_EPI_NONE) {
-      if (make_map(&g->mc, a_.c_base, p.N, (uint64_t)p.M * a_.splits, p.ndev, p.ldc * 4, p.dev_stride, 32, false)) {
+      const uint64_t rows = (uint64_t)p.M * (p.sk_mode == 1 ? 1 : a_.splits);
+      if (make_map(&g->mc, a_.c_base, p.N, rows, p.ndev, p.ldc * 4, p.dev_stride, 32, false)) {
         delete g;
         return -1;
       }
@@ -786,6 +845,24 @@ int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out) {
     }
   }
   if (!a_.tma_store) memset(&g->mc, 0, sizeof(g->mc));
+  memset(&g->mw, 0, sizeof(g->mw));
+  a_.sk_inkernel = 0;
+  if (p.sk_mode == 1 && a_.splits > 1) {
+    const int pairs = (spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0)) / g->cg;
+    if (!a_.tma_store || p.N != p.ldc || p.M % 32 || a_.units > pairs) {
+      delete g;
+      return spx_set_error("gemm %dx%dx%d: in-kernel split-K needs TMA stores, ldc == N, M %% 32 == 0 and "
+                           "units <= SM pairs (%d > %d)", p.M, p.N, p.K, a_.units, pairs);
+    }
+    a_.sk_inkernel = 1;
+    a_.ws_base = p.base + (uint64_t)(p.ws_off * 4);
+    a_.flag_base = p.base + (uint64_t)(p.flag_off * 4);
+    if (make_map(&g->mw, a_.ws_base, p.N, (uint64_t)p.M * (a_.splits - 1), p.ndev, (uint64_t)p.N * 4,
+                 p.dev_stride, 32, false)) {
+      delete g;
+      return -1;
+    }
+  }
   for (int i = 0; i < 2; ++i) {
     a_.in_off[i] = p.epi_in_off[i];
     a_.in_ld[i] = p.epi_in_ld[i];
@@ -835,7 +912,7 @@ static int launch_tmema_e(const SpxGemmTC* g, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  SPX_CUDA(cudaLaunchKernelEx(&cfg, kern, g->ma, g->mb, g->mc, g->args));
+  SPX_CUDA(cudaLaunchKernelEx(&cfg, kern, g->ma, g->mb, g->mc, g->mw, g->args));
   return 0;
 }
 

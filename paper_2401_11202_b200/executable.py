@@ -199,6 +199,20 @@ class Executable:
         self.counter_off = hi + nkeys * 2 * R.PEER_MAX_BLOCKS * 8
         self.flag_elems = _align(nkeys * 2 * R.PEER_MAX_BLOCKS * 8 + nkeys * R.PEER_MAX_BLOCKS) if nkeys else 0
         hi += self.flag_elems
+        # in-kernel split-K (critical-path GEMMs, serialised on the main
+        # stream): one shared partial workspace and one flag array (uint32,
+        # zero between launches)
+        ws = fl = 0
+        for k in ks:
+            if k.kind == "gemm" and k.data.get("sk_inkernel"):
+                d = k.data
+                ws = max(ws, (d["splits"] - 1) * d["M"] * d["N"])
+                fl = max(fl, -(-d["M"] // 256) * -(-d["N"] // 128) * 2 * 4)
+        self.sk_ws_off = hi
+        hi += _align(ws) if ws else 0
+        self.sk_flag_off = hi
+        self.sk_flag_elems = _align(fl) if fl else 0
+        hi += self.sk_flag_elems
         self.off = off
         self.slice_elems = _align(hi, 1 << 18)           # 1 MiB granularity per device
         self.peak_bytes = hi * 4
@@ -210,6 +224,9 @@ class Executable:
             self.device.memset(self.base + self.zero_off * 4, self.zero_elems * 4, 0)
         if self.flag_elems and not self.dry:
             self.device.memset(self.base + self.flag_off * 4, self.flag_elems * 4, 0)
+        if self.sk_flag_elems and not self.dry:
+            for p in range(self.ndev):
+                self.device.memset(self.base + p * self.dev_stride + self.sk_flag_off * 4, self.sk_flag_elems * 4, 0)
 
     def addr(self, p: int, buf: str, extra: int = 0) -> int:
         return self.base + p * self.dev_stride + (self.off[buf] + extra) * 4
@@ -383,7 +400,8 @@ class Executable:
                         side[i] = self.COMM
         if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
             for i in reversed(range(len(ks))):
-                if ks[i].kind == "gemm" and off_critical(i, side):
+                # in-kernel split-K GEMMs share one workspace: main stream only
+                if ks[i].kind == "gemm" and not ks[i].data.get("sk_inkernel") and off_critical(i, side):
                     side[i] = self.COMPUTE
         if os.environ.get("SPX_UPDATE_STREAM", "1") != "0" and side:
             for i, k in enumerate(ks):
@@ -527,6 +545,10 @@ class Executable:
         p.splits = d.get("splits", 1)
         if p.splits > 1:
             p.path = 1                       # split-K partials exist on the tcgen05 path only
+        if d.get("sk_inkernel"):
+            p.sk_mode = 1
+            p.ws_off = self.sk_ws_off
+            p.flag_off = self.sk_flag_off
         epi = d.get("epi")
         if epi is not None:
             p.path = 1                       # fused epilogues exist on the tcgen05 path only

@@ -332,7 +332,14 @@ class Compiler:
         M, K = a_dims
         N = b_dims[1]
         splits = self._splitk(M, N, K, aoff, lda, boff, ldb)
-        if splits == 1:
+        sk = self._splitk_inkernel(M, N, K, aoff, lda, boff, ldb) if splits == 1 and not at else 1
+        if sk > 1:
+            # few-tile activation GEMM on the critical path: partials reduced
+            # inside the kernel (no workspace reduction launch)
+            self.kernels.append(Kernel("gemm", [out], {ab, bb}, op_index=i,
+                                       data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt),
+                                                 splits=sk, sk_inkernel=True, tc_ok=True)))
+        elif splits == 1:
             k = Kernel("gemm", [out], {ab, bb}, op_index=i,
                        data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt), splits=1,
                                  tc_ok=self._tc_ok(M, N, K, aoff, lda, boff, ldb)))
@@ -357,6 +364,26 @@ class Compiler:
         """The runtime's tcgen05 eligibility (gemm_tc.cu: spx_gemm_tc_supported)."""
         return (M >= 64 and N >= 32 and K >= 32 and aoff % 4 == 0 and boff % 4 == 0
                 and lda % 4 == 0 and ldb % 4 == 0)
+
+    def _splitk_inkernel(self, M, N, K, aoff, lda, boff, ldb) -> int:
+        """Split count for the in-kernel split-K of an activation GEMM whose
+        256 x 128 tiles occupy at most half the SMs.  Every (tile, split) unit
+        must be co-resident: the split-0 CTAs wait for the others (gemm_tc.cu).
+        Off by default (SPX_SPLITK_INKERNEL=1 enables): measured on C2 at N=4
+        it made the critical-path GEMMs slower (4.30 vs 3.68 ms/step) -- the
+        split-0 drain warps fold (S-1) x 64 KB of partials per CTA with too
+        little memory-level parallelism, which costs more than the saved MMA
+        time on these shapes."""
+        import os
+        if os.environ.get("SPX_SPLITK_INKERNEL", "0") == "0":
+            return 1
+        if not self._tc_ok(M, N, K, aoff, lda, boff, ldb) or M % 32 or N % 4:
+            return 1
+        pairs = -(-M // 256) * -(-N // 128) * len(self.devices)
+        nk = -(-K // 32)
+        if pairs * 2 * 2 > self.NUM_SMS or nk < 16:
+            return 1
+        return max(1, min(4, nk // 8, (self.NUM_SMS // 2) // pairs))
 
     def _splitk(self, M, N, K, aoff, lda, boff, ldb) -> int:
         """Split K when the output has too few 128x128 tiles to fill the SMs

@@ -62,7 +62,9 @@ class GemmParams(C.Structure):
                 ("epi", C.c_int32), ("epi_pad", C.c_int32),
                 ("epi_in_off", C.c_int64 * 2), ("epi_in_ld", C.c_int64 * 2),
                 ("epi_out_off", C.c_int64 * 2), ("epi_out_ld", C.c_int64 * 2),
-                ("epi_imm", C.c_float * 2)]
+                ("epi_imm", C.c_float * 2),
+                ("sk_mode", C.c_int32), ("sk_pad", C.c_int32),
+                ("ws_off", C.c_int64), ("flag_off", C.c_int64)]
 
 
 EPI_NONE, EPI_ADD, EPI_SQUARE, EPI_MULSCALE, EPI_MOMENTUM = 0, 1, 2, 3, 4

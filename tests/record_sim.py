@@ -111,7 +111,7 @@ class Sim:
                 B = self.gather_view(p, g.b_off, (1, g.ldb), (g.K, g.N))
             else:
                 B = self.gather_view(p, g.b_off, (g.ldb, 1), (g.K, g.N))
-            S = max(1, g.splits)
+            S = max(1, g.splits) if g.sk_mode == 0 else 1     # sk_mode 1: reduced in the kernel
             for sp in range(S):
                 k0, k1 = (g.K * sp) // S, (g.K * (sp + 1)) // S
                 # partial k-ranges are whole 32-wide k-blocks in the kernel

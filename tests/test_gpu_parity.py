@@ -294,3 +294,41 @@ def test_session_feed_pipeline():
         want = O.interpret(m, {"x": x, "w": w})[0]
         assert O.relative_error(g, want) < TOL
     sess.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 512, 1024), (1024, 1024, 512), (1536, 512, 1024), (2048, 512, 640), (1024, 320, 1024)])
+def test_gemm_inkernel_splitk(M, N, K, monkeypatch):
+    """Critical-path GEMMs with few tiles split K inside the kernel (split-0
+    CTAs fold the other splits' partials in split order): matches the oracle,
+    and is bit-reproducible run to run (graph replays included)."""
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.executable import Executable
+    from paper_2401_11202_b200.session import Session
+    monkeypatch.setenv("SPX_SPLITK_INKERNEL", "1")
+    text = f"""func @main(%x: tensor<{M}x{K}xf32>, %w: tensor<{K}x{N}xf32>) -> tensor<{M}x{N}xf32> {{
+  %c = matmul %x, %w : tensor<{M}x{N}xf32>
+  return %c
+}}
+"""
+    m = pkg.parse_module(text)
+    ex = Executable(m, devices=[0], dry=True)
+    (k, p), = [r for r in ex.records() if r[0] == R.K_GEMM]
+    assert p.sk_mode == 1 and p.splits > 1
+    rng = np.random.default_rng(M + N + K)
+    ins = {"x": rng.standard_normal((M, K)).astype(np.float32),
+           "w": rng.standard_normal((K, N)).astype(np.float32)}
+    want = O.interpret(m, ins)[0]
+    sess = Session(m)
+    sess.load(ins)
+    sess.run()
+    sess.sync()
+    a = sess.results()[0][0].copy()
+    sess.capture()
+    for _ in range(3):
+        sess.step()
+    sess.sync()
+    b = sess.results()[0][0]
+    sess.close()
+    assert np.all(np.isfinite(a)) and O.relative_error(a, want) < TOL
+    np.testing.assert_array_equal(a, b)
