@@ -324,7 +324,8 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
   uint64_t* lo_empty = lo_full + LS;
   uint64_t* tfull = lo_empty + LS;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* skbar = tempty + 2;          // [4] in-kernel split-K: partial tiles landed (per drain warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(skbar + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (args.K + BK - 1) / BK;
@@ -366,6 +367,9 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4 * CG);              // one elected lane per drain warp
+    }
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&skbar[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -652,24 +656,35 @@ gemm_tc_tmema_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_con
             }
           }
           __syncwarp();
-          uint32_t v;
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-          const float* wsd = reinterpret_cast<const float*>(args.ws_base + (uint64_t)((int64_t)dev * args.dev_stride));
-          const int rrow = m0 + q * 32 + lane;
+          // The CTA's only work unit is done (units <= CTA pairs), so its raw
+          // TMA ring is idle: bring every partial slice of this warp's 32 rows
+          // in with bulk tensor loads (128B-swizzled 32 x 32 boxes), then fold
+          // them in split order from shared memory.
+          uint8_t* ring = smem + q * (S::RSTAGES * S::RAW / 4);
+          int nbox = 0;
+          for (int cc = 0; cc < BN / 32; ++cc)
+            if (n0 + cc * 32 < args.N) ++nbox;
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&skbar[q], (uint32_t)((args.splits - 1) * nbox * 4096));
+            for (int s2 = 1; s2 < args.splits; ++s2)
+              for (int cc = 0; cc < nbox; ++cc)
+                tma_load_3d(ring + ((s2 - 1) * 4 + cc) * 4096, &tma_w, &skbar[q], n0 + cc * 32,
+                            (s2 - 1) * args.M + m0 + q * 32, dev);
+          }
+          mbar_wait(&skbar[q], 0);
           for (int s2 = 1; s2 < args.splits; ++s2) {
-            const float* wr = wsd + ((int64_t)(s2 - 1) * args.M + rrow) * args.N;
 #pragma unroll
             for (int cc = 0; cc < BN / 32; ++cc) {
+              if (cc >= nbox) break;
+              const uint8_t* box = ring + ((s2 - 1) * 4 + cc) * 4096 + lane * 128;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const int c = n0 + cc * 32 + 4 * j;
-                if (rrow < args.M && c < args.N) {
-                  const float4 w = __ldcg(reinterpret_cast<const float4*>(wr + c));
-                  acc[cc * 32 + 4 * j] = __fadd_rn(acc[cc * 32 + 4 * j], w.x);
-                  acc[cc * 32 + 4 * j + 1] = __fadd_rn(acc[cc * 32 + 4 * j + 1], w.y);
-                  acc[cc * 32 + 4 * j + 2] = __fadd_rn(acc[cc * 32 + 4 * j + 2], w.z);
-                  acc[cc * 32 + 4 * j + 3] = __fadd_rn(acc[cc * 32 + 4 * j + 3], w.w);
-                }
+                const float4 w = *reinterpret_cast<const float4*>(box + ((j ^ (lane & 7)) << 4));
+                acc[cc * 32 + 4 * j] = __fadd_rn(acc[cc * 32 + 4 * j], w.x);
+                acc[cc * 32 + 4 * j + 1] = __fadd_rn(acc[cc * 32 + 4 * j + 1], w.y);
+                acc[cc * 32 + 4 * j + 2] = __fadd_rn(acc[cc * 32 + 4 * j + 2], w.z);
+                acc[cc * 32 + 4 * j + 3] = __fadd_rn(acc[cc * 32 + 4 * j + 3], w.w);
               }
             }
           }

@@ -369,11 +369,13 @@ class Compiler:
         """Split count for the in-kernel split-K of an activation GEMM whose
         256 x 128 tiles occupy at most half the SMs.  Every (tile, split) unit
         must be co-resident: the split-0 CTAs wait for the others (gemm_tc.cu).
-        Off by default (SPX_SPLITK_INKERNEL=1 enables): measured on C2 at N=4
-        it made the critical-path GEMMs slower (4.30 vs 3.68 ms/step) -- the
-        split-0 drain warps fold (S-1) x 64 KB of partials per CTA with too
-        little memory-level parallelism, which costs more than the saved MMA
-        time on these shapes."""
+        The split-0 CTAs bring the partials in with bulk tensor loads into
+        their idle TMA ring and fold them in split order.  Off by default
+        (SPX_SPLITK_INKERNEL=1 enables).  Measured (graph replay): a
+        1024x(1024|512) MP GEMM chain 15.5 -> 14.4 us per GEMM, 1024x1024x2048
+        27.1 -> 22.2 us; whole steps: C2 N=2 3.77 -> 3.64 ms, but C2 N=4 3.71 ->
+        3.85 and C5 N=4 4.00 -> 4.27 ms (the split units take the SMs the
+        side-stream GEMMs and collectives overlap on)."""
         import os
         if os.environ.get("SPX_SPLITK_INKERNEL", "0") == "0":
             return 1
@@ -383,7 +385,9 @@ class Compiler:
         nk = -(-K // 32)
         if pairs * 2 * 2 > self.NUM_SMS or nk < 16:
             return 1
-        return max(1, min(4, nk // 8, (self.NUM_SMS // 2) // pairs))
+        # the split-0 CTAs stage (S-1) partial 128x128 tiles in their idle TMA
+        # ring (144 KB): S <= 3
+        return max(1, min(3, nk // 8, (self.NUM_SMS // 2) // pairs))
 
     def _splitk(self, M, N, K, aoff, lda, boff, ldb) -> int:
         """Split K when the output has too few 128x128 tiles to fill the SMs
