@@ -183,9 +183,10 @@ typedef struct {
 } spx_nccl_params;
 
 /* ---- all-reduce over NVLink peer memory (CUDA IPC-mapped arenas) -------- */
-/* Flag region of a member (uint32): [slot][phase 2][block SPX_PEER_MAX_BLOCKS][member 8];
+/* Flag region of a member (uint32): [slot][phase SPX_PEER_PHASES][block SPX_PEER_MAX_BLOCKS][member 8];
  * epoch counters (local): [slot][block]. */
 #define SPX_PEER_MAX_BLOCKS 512
+#define SPX_PEER_PHASES 3
 typedef struct {
   int32_t kind, n, me, monoid;     /* kind 0 = all-reduce; n members; me = my index */
   int64_t count;                   /* elements */

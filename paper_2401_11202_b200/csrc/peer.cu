@@ -42,7 +42,7 @@ SPX_DEV uint32_t ld_flag(const uint32_t* p) {
 // flag word of (slot, phase, block, member) inside a member's flag region
 SPX_DEV uint32_t* flag_at(uint64_t region, int slot, int phase, int block, int member) {
   return reinterpret_cast<uint32_t*>(region) +
-         (((int64_t)(slot * 2 + phase) * SPX_PEER_MAX_BLOCKS + block) * 8 + member);
+         (((int64_t)(slot * SPX_PEER_PHASES + phase) * SPX_PEER_MAX_BLOCKS + block) * 8 + member);
 }
 
 SPX_DEV void block_barrier(const spx_peer_params& p, int phase, uint32_t epoch) {
@@ -130,6 +130,76 @@ __global__ void __launch_bounds__(256) peer_allreduce(const __grid_constant__ sp
   if (threadIdx.x == 0) *counter = epoch;
 }
 
+// Two-shot (n >= 4): block b owns chunk b of every member's segment.
+//   1. arrive (phase 0), then reduce chunk b of MY segment over all members'
+//      inputs in member order into my output;
+//   2. barrier (phase 1): every member's chunk b of its own segment is final;
+//   3. copy chunk b of every other member's segment from its output;
+//   4. depart (phase 2).
+// NVLink traffic per rank 2(n-1)/n of the tensor instead of (n-1); the fold
+// (and so every replica's bits) is the same as the one-shot kernel's.
+template <int N>
+__global__ void __launch_bounds__(256) peer_allreduce_2shot(const __grid_constant__ spx_peer_params p,
+                                                            int64_t seg4, int64_t per_block) {
+  SPX_PDL_ENTRY();
+  uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
+  const uint32_t epoch = *counter + 1u;
+  block_barrier(p, 0, epoch);
+  // phase A: my segment's chunk b
+  {
+    const int64_t s0 = (int64_t)p.me * seg4;
+    const int64_t b0 = s0 + (int64_t)blockIdx.x * per_block;
+    const int64_t b1 = min(s0 + seg4, b0 + per_block);
+    float4* dst = reinterpret_cast<float4*>(p.dst);
+    for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += 256 * U) {
+      float4 v[N][U];
+#pragma unroll
+      for (int m = 0; m < N; ++m)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * 256;
+          if (i < b1) v[m][u] = reinterpret_cast<const float4*>(p.src[m])[i];
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * 256;
+        if (i >= b1) continue;
+        float4 acc = v[0][u];
+#pragma unroll
+        for (int m = 1; m < N; ++m) acc = fold4(p.monoid, acc, v[m][u]);
+        dst[i] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  block_barrier(p, 1, epoch);
+  // phase B: the other members' chunk b, from their outputs (same arena offset)
+  {
+    float4* dst = reinterpret_cast<float4*>(p.dst);
+    const int64_t dst_off = (int64_t)(p.dst - p.src[p.me]);    // bytes from my input to my output
+#pragma unroll 1
+    for (int k = 1; k < N; ++k) {
+      const int m = (p.me + k) % N;
+      const float4* rem = reinterpret_cast<const float4*>(p.src[m] + dst_off);
+      const int64_t s0 = (int64_t)m * seg4;
+      const int64_t b0 = s0 + (int64_t)blockIdx.x * per_block;
+      const int64_t b1 = min(s0 + seg4, b0 + per_block);
+      for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += 256 * U) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i0 + u * 256 < b1) v[u] = rem[i0 + u * 256];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i0 + u * 256 < b1) dst[i0 + u * 256] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  block_barrier(p, 2, epoch);
+  if (threadIdx.x == 0) *counter = epoch;
+}
+
 }  // namespace
 
 int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
@@ -137,16 +207,31 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if ((p.dst & 15) || p.kind != 0) return spx_set_error("peer collective: unsupported record");
   for (int m = 0; m < p.n; ++m)
     if (p.src[m] & 15) return spx_set_error("peer collective: unaligned source");
-  // blocks: ~8 float4 per thread, at most 2 per SM (co-resident with little
+  // blocks: ~2 float4 per thread, at most 2 per SM (co-resident with little
   // else) and SPX_PEER_MAX_BLOCKS (flag space); identical on every member
   const int64_t n4 = p.count >> 2;
-  int64_t blocks = (n4 + 256 * 8 - 1) / (256 * 8);
+  int64_t blocks = (n4 + 256 * 2 - 1) / (256 * 2);
   const int64_t cap = (int64_t)spx_num_sms() * 2 < SPX_PEER_MAX_BLOCKS ? (int64_t)spx_num_sms() * 2 : SPX_PEER_MAX_BLOCKS;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const int64_t per_block = (n4 + blocks - 1) / blocks;
-  static int dbg = -1;
+  static int dbg = -1, two = -1;
   if (dbg < 0) { const char* e = getenv("SPX_PEER_DBG"); dbg = e ? atoi(e) : 0; }
+  if (two < 0) { const char* e = getenv("SPX_PEER_TWOSHOT"); two = e ? atoi(e) : 1; }
+  // two-shot for 4 and 8 members from 2 MB (4 ranks, 4 MB: 18.7 us vs 25.0 us
+  // one-shot; 1 MB: 14.4 vs 11.2), when every segment is whole float4s
+  if (two && (p.n == 4 || p.n == 8) && (p.count & 3) == 0 && (n4 % p.n) == 0 && n4 >= 131072 && !dbg) {
+    const int64_t seg4 = n4 / p.n;
+    int64_t b2 = (seg4 + 256 * 2 - 1) / (256 * 2);     // ~2 float4 per thread per phase
+    if (b2 > cap) b2 = cap;
+    if (b2 < 1) b2 = 1;
+    const int64_t pb = (seg4 + b2 - 1) / b2;
+    if (p.n == 4) spx_launch(peer_allreduce_2shot<4>, dim3((unsigned)b2), 256, 0, s, p, seg4, pb);
+    else spx_launch(peer_allreduce_2shot<8>, dim3((unsigned)b2), 256, 0, s, p, seg4, pb);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+    return 0;
+  }
   switch (p.n) {
     case 2: spx_launch(peer_allreduce<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
     case 4: spx_launch(peer_allreduce<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;

@@ -196,8 +196,9 @@ class Executable:
         # peers through their mapping of this arena) and local epoch counters
         nkeys = len(self.comm_keys()) if c.comm_mode == "nccl" else 0
         self.flag_off = hi
-        self.counter_off = hi + nkeys * 2 * R.PEER_MAX_BLOCKS * 8
-        self.flag_elems = _align(nkeys * 2 * R.PEER_MAX_BLOCKS * 8 + nkeys * R.PEER_MAX_BLOCKS) if nkeys else 0
+        self.counter_off = hi + nkeys * R.PEER_PHASES * R.PEER_MAX_BLOCKS * 8
+        self.flag_elems = (_align(nkeys * R.PEER_PHASES * R.PEER_MAX_BLOCKS * 8 + nkeys * R.PEER_MAX_BLOCKS)
+                           if nkeys else 0)
         hi += self.flag_elems
         # in-kernel split-K (critical-path GEMMs, serialised on the main
         # stream): one shared partial workspace and one flag array (uint32,
@@ -379,8 +380,8 @@ class Executable:
 
         def off_critical(i, side):
             rd = [j for b in ks[i].outs for j in readers.get(b, [])]
-            if not rd:       # writes only results (a GEMM with a fused update)
-                return all(b in results for b in ks[i].outs)
+            if not rd:       # writes only results: a GEMM with a fused update
+                return ks[i].kind == "gemm" and all(b in results for b in ks[i].outs)
             return all(self._terminal(ks[j]) or j in side for j in rd)
 
         side: dict = {}
@@ -396,7 +397,8 @@ class Executable:
                 k = ks[i]
                 if k.kind == "coll" and k.data["kind"] != "all_slice":
                     if (crit_coll or off_critical(i, side)
-                            or (prefetch and k.ins and all(b in args for b in k.ins))):
+                            or (prefetch and k.data["kind"] == "all_gather" and k.ins
+                                and all(b in args for b in k.ins))):
                         side[i] = self.COMM
         if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
             for i in reversed(range(len(ks))):

@@ -98,6 +98,7 @@ class PeerParams(C.Structure):
 
 K_PEER = 7
 PEER_MAX_BLOCKS = 512      # include/spindle_b200.h
+PEER_PHASES = 3
 
 PARAMS = {K_PEER: PeerParams, K_EW: EwParams, K_REDUCE: ReduceParams, K_GEMM: GemmParams,
           K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams}

@@ -54,7 +54,7 @@ def test_peer_records_replace_critical_path_all_reduces():
         if k == R.K_PEER:
             assert p.n == 2 and 0 <= p.slot < nkeys and p.kind == 0
             assert p.flags[0] == ex.base + ex.flag_off * 4
-            assert p.counter == ex.base + (ex.flag_off + nkeys * 2 * R.PEER_MAX_BLOCKS * 8) * 4
+            assert p.counter == ex.base + (ex.flag_off + nkeys * R.PEER_PHASES * R.PEER_MAX_BLOCKS * 8) * 4
 
 
 def _worker(rank, world, port, q):

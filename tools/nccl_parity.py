@@ -67,6 +67,32 @@ def main():
                 except DivergenceError as e:
                     if case.get("error") != "DivergenceError":
                         fails.append((case["key"], str(e)))
+    # large all_reduce over every rank (the peer-memory kernels: one-shot for 2
+    # members, two-shot for 4 / 8): bit-identical to the member-order fold
+    for rows in (1024, 257):
+        text = (f"mesh {{M:{world}}}\n\nfunc @main(%x: tensor<{rows}x1024xf32>) -> tensor<{rows}x1024xf32> {{\n"
+                f"  %r = all_reduce [\"M\"] %x : tensor<{rows}x1024xf32>\n  return %r\n}}\n")
+        m = parse_module(text)
+        spec = ShardingSpec({"x": [[], []]}, [[[], []]])
+        xs = [np.random.default_rng(100 + r).standard_normal((rows, 1024)).astype(np.float32) for r in range(world)]
+        sess = Session(m, spec, mode="nccl", device=dev, rank=rank, world=world, local_rank=local)
+        sess.ex.upload_args([{"x": xs[rank]}])
+        sess.run()
+        sess.sync()
+        got = sess.results()[0][0]
+        kinds = sorted({k for k, _ in sess.ex.records()})
+        sess.close()
+        want = xs[0].copy()
+        for x in xs[1:]:
+            want = want + x
+        allok = [None] * world
+        dist.all_gather_object(allok, bool(np.array_equal(got, want)))
+        if rank == 0:
+            n += 1
+            if not all(allok):
+                fails.append((f"all_reduce_{rows}x1024", "not bit-identical to the member-order fold"))
+            if world > 1 and R.K_PEER not in kinds:
+                fails.append((f"all_reduce_{rows}x1024", "peer kernel not used"))
     if rank == 0:
         print(json.dumps({"world": world, "cases": n, "failures": fails}))
     dist.barrier()
