@@ -292,29 +292,43 @@ def main():
     # ---- per-record profile (eager, events between records) for the roofline
     rec_ms = sess.ex.plan.profile()
     recs = sess.ex.records()
-    gemm_flops = gemm_ms = 0.0
+    gemm_flops = gemm_ms = ideal_ms = tensor_flops = 0.0
+    hbm, bf16, src = peaks()
+    # tensor-core ceilings per GEMM path: block-scaled 3xFP16 (path 3, kind::f16)
+    # against the measured dense bf16/f16 rate (MEASURED_PEAKS.json, burst);
+    # 3xTF32 (path 1, kind::tf32) against the measured tcgen05 tf32 issue rate
+    # (tools/mma_bench.cu, profiles/r01_mma_bench.txt).  Both do 3 MMAs per fp32
+    # FLOP (hi.hi + hi.lo + lo.hi).
+    tc_peak = {3: bf16, 1: TF32_MMA_PEAK}
+    paths = {}
     cls_ms = {}
-    for (kind, p), t in zip(recs, rec_ms):
+    for idx, ((kind, p), t) in enumerate(zip(recs, rec_ms)):
         name = {R.K_EW: "elementwise", R.K_REDUCE: "reduce", R.K_GEMM: "gemm", R.K_GATHER: "relayout",
                 R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl", R.K_PEER: "peer_allreduce"}[kind]
         cls_ms[name] = cls_ms.get(name, 0.0) + float(t)
         if kind == R.K_GEMM:
-            gemm_flops += 2.0 * p.M * p.N * p.K * p.ndev
+            path = sess.ex.plan.record_info(idx)[1]
+            f = 2.0 * p.M * p.N * p.K * p.ndev
+            paths[path] = paths.get(path, 0) + 1
+            gemm_flops += f
             gemm_ms += float(t)
-    hbm, bf16, src = peaks()
-    # tensor-core tf32 ceiling: measured tcgen05 kind::tf32 issue rate
-    # (tools/mma_bench.cu, profiles/r01_mma_bench.txt); 1/2 x the bf16 figure
-    # would be the datasheet ratio applied to the cuBLAS-measured bf16 number
-    tf32_peak = TF32_MMA_PEAK
-    achieved = 3.0 * gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-    roofline = {"bound": "tensor", "kernel": "tcgen05 3xTF32 GEMM (gemm_tc_tmema_kernel, CTA pairs)",
-                "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+            if path in tc_peak:
+                tensor_flops += 3.0 * f
+                ideal_ms += 3.0 * f / (tc_peak[path] * 1e12) * 1e3
+    achieved = tensor_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    peak_eff = tensor_flops / (ideal_ms / 1e3) / 1e12 if ideal_ms > 0 else bf16
+    kname = ("tcgen05 block-scaled 3xFP16 GEMM (split_h16_kernel + gemm_h3_kernel, CTA pairs)"
+             if paths.get(3, 0) >= paths.get(1, 0) else "tcgen05 3xTF32 GEMM (gemm_tc_tmema_kernel, CTA pairs)")
+    roofline = {"bound": "tensor", "kernel": kname,
+                "achieved": achieved, "peak": peak_eff, "unit": "TFLOP/s",
+                "frac": (ideal_ms / gemm_ms) if gemm_ms > 0 else 0.0,
                 "traffic": None,
-                "note": (f"achieved = tensor-core TF32 work (3 MMAs per fp32 FLOP: hi.hi + hi.lo + lo.hi) "
-                         f"/ GEMM time, summed over the {sum(1 for k, _ in recs if k == R.K_GEMM)} GEMM launches "
-                         f"of one step; peak = measured tcgen05 kind::tf32 rate {tf32_peak:.0f} TF/s "
-                         f"(tools/mma_bench.cu; {src} bf16 {bf16:.1f} TF/s / 2 = {bf16 / 2:.0f}). "
-                         f"fp32-equivalent GEMM rate "
+                "gemm_paths": {("h3" if k == 3 else "tf32" if k == 1 else "simt"): v for k, v in paths.items()},
+                "note": (f"achieved = tensor-core work (3 MMAs per fp32 FLOP) / GEMM record time (the 3xFP16 "
+                         f"records include their two operand-split kernels), summed over the "
+                         f"{sum(paths.values())} GEMM launches of one step; peak = {src} dense bf16 "
+                         f"{bf16:.1f} TF/s for kind::f16, measured tcgen05 kind::tf32 rate {TF32_MMA_PEAK:.0f} "
+                         f"TF/s for 3xTF32 records (time-weighted).  fp32-equivalent GEMM rate "
                          f"{gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0:.1f} TFLOP/s"),
                 "step_ms_by_class": {k: round(v, 4) for k, v in sorted(cls_ms.items())},
                 "gemm_share_of_step": (gemm_ms / float(np.sum(rec_ms))) if np.sum(rec_ms) > 0 else None}

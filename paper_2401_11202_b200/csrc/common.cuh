@@ -70,6 +70,14 @@ int spx_gemm_tc_launch(const SpxGemmTC* g, cudaStream_t s, int* nlaunch);
 void spx_gemm_tc_free(SpxGemmTC* g);
 bool spx_gemm_tc_supported(const spx_gemm_params& p);
 
+struct SpxGemmH3;  // prepared block-scaled 3xFP16 GEMM, see gemm_h3.cu
+bool spx_gemm_h3_supported(const spx_gemm_params& p);
+int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out);
+int64_t spx_gemm_h3_ws_bytes(const SpxGemmH3* g);
+int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws);
+int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch);
+void spx_gemm_h3_free(SpxGemmH3* g);
+
 int spx_num_sms();
 
 // Programmatic dependent launch: every kernel starts with SPX_PDL_ENTRY --

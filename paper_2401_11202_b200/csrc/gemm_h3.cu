@@ -1,0 +1,585 @@
+// Block-scaled 3xFP16 tcgen05 GEMM for the reference's fp32 `matmul`
+// (interp.py:43-44: numpy `@` on float32 arrays).
+//
+// The tf32 kernel (gemm_tc.cu) needs three kind::tf32 MMAs per fp32 product
+// and splits the operands on the SM.  kind::f16 runs at twice the tf32 rate,
+// so three fp16 MMAs cost half as much -- if fp16 pieces can carry fp32
+// precision.  They can, with a power-of-two scale per 128 x 128 block:
+//
+//   split:  s = 2^e with max|x| * s in [2^14, 2^15) over the block,
+//           hi = fp16_rn(x * s), lo = fp16_rn(x * s - hi)      (x * s - hi exact)
+//           => x * s = hi + lo + r, |r| <= 2^-22 |x * s| (or 2^-25 absolute,
+//              i.e. 2^-40 of the block maximum, where lo is subnormal)
+//   GEMM:   per 128-wide k chunk, D_c = hi.lo + hi.hi + lo.hi (tensor core,
+//           products exact in fp32), folded into fp32 registers as
+//           acc += D_c * (1 / (s_A(block) * s_B(block)))      (exact power of 2)
+//
+// 128 x 128 blocks are symmetric in rows and columns, so the same pieces serve
+// a tensor used K-major or MN-major, and one scale per (CTA tile, k chunk) is
+// all the drain needs: an A chunk of a CTA is one block of A's rows, a B chunk
+// of a pair tile one block of B's columns.  Per-chunk fp32 promotion also keeps
+// the tensor core's truncating accumulation out of the error (see gemm_tc.cu).
+// Error vs float64: ~1e-6 max-normalised at any K (fp32 parity bar 1e-5,
+// SPEC.md:92).  Scales are clamped to 2^+-60 (blocks with max |x| outside
+// [2^-45, 2^75] lose precision; fp32 data of a training step is far inside).
+//
+// Two kernels per GEMM, both HBM- or tensor-bound and PDL-chained:
+//   split_h16_kernel  one CTA per 128 x 128 block of an fp32 operand view:
+//                     read 4 B, write hi + lo (4 B) per element, one scale;
+//   gemm_h3_kernel    persistent, CTA pairs (cta_group::2, 256 x 128 tiles,
+//                     each CTA holds 128 A rows and 64 B columns), pure TMA ->
+//                     MMA -> drain: warp 0 TMA (both CTAs' loads complete on
+//                     the leader's barrier), warp 1 of the leader issues
+//                     kind::f16 MMAs (A collector reused by hi.lo / hi.hi),
+//                     warps 4-7 fold TMEM chunks with their scale and store C
+//                     through TMA.
+#include <cstdlib>
+#include <cstring>
+#include <cuda_fp16.h>
+#include "common.cuh"
+#include "tc_util.cuh"
+
+namespace {
+
+constexpr int HB = 128;                  // scale block edge = A rows per CTA = K per chunk
+constexpr int HBK = 64;                  // fp16 per 128-byte swizzle row = K per k-block
+constexpr int HBN = 128;                 // output columns per pair tile
+constexpr int H_CG = 2;
+constexpr int H_BNH = HBN / H_CG;        // B columns per CTA
+constexpr int H_THREADS = 256;
+constexpr int H_A_BYTES = HB * HBK * 2;      // 16 KB per piece
+constexpr int H_B_BYTES = H_BNH * HBK * 2;   // 8 KB per piece
+constexpr int H_STAGE = 2 * H_A_BYTES + 2 * H_B_BYTES;   // 48 KB
+constexpr int H_RS = 4;
+constexpr int H_BAR_OFF = H_RS * H_STAGE;
+constexpr int H_STG_OFF = H_BAR_OFF + 1024;
+constexpr int H_STG_WARP = 8192;
+constexpr int H_TOTAL = H_STG_OFF + 4 * H_STG_WARP + 1024;
+
+struct SplitArgs {
+  uint64_t src;          // device-0 address of element (0, 0) of the fp32 view
+  int64_t src_dev;       // bytes between devices
+  int64_t ld;            // row pitch (elements)
+  int rows, cols;
+  uint64_t dst;          // device-0 address of the pieces [2][rows][pitch] fp16
+  int64_t dst_dev;       // bytes
+  int64_t pitch;         // halves (multiple of 8: 16 B TMA pitch)
+  uint64_t scl;          // device-0 address of 1/s per block [rb][cb] (fp32)
+  int64_t scl_dev;       // bytes
+  int cb;
+};
+
+__global__ void __launch_bounds__(256) split_h16_kernel(const __grid_constant__ SplitArgs a) {
+  __shared__ float wmax[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int dev = blockIdx.z;
+  const int r0 = blockIdx.y * HB, c0 = blockIdx.x * HB;
+  const float* src = reinterpret_cast<const float*>(a.src + (uint64_t)((int64_t)dev * a.src_dev));
+  SPX_PDL_ENTRY();
+  const bool vec = ((a.src | (uint64_t)a.src_dev | (uint64_t)(a.ld * 4)) & 15) == 0 && c0 + HB <= a.cols;
+  float4 v[16];
+  float m = 0.f;
+  const int c = c0 + lane * 4;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = r0 + i * 8 + warp;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < a.rows) {
+      const float* p = src + (int64_t)r * a.ld + c;
+      if (vec) {
+        x = __ldcs(reinterpret_cast<const float4*>(p));
+      } else {
+        if (c < a.cols) x.x = p[0];
+        if (c + 1 < a.cols) x.y = p[1];
+        if (c + 2 < a.cols) x.z = p[2];
+        if (c + 3 < a.cols) x.w = p[3];
+      }
+    }
+    v[i] = x;
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  m = wmax[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, wmax[w]);
+  const int E = (int)((__float_as_uint(m) >> 23) & 0xFF);
+  int e = (m == 0.f || E == 255) ? 0 : 141 - E;     // max * 2^e in [2^14, 2^15)
+  e = e < -60 ? -60 : (e > 60 ? 60 : e);
+  const float up = __uint_as_float((uint32_t)(127 + e) << 23);
+  if (tid == 0)
+    reinterpret_cast<float*>(a.scl + (uint64_t)((int64_t)dev * a.scl_dev))[blockIdx.y * a.cb + blockIdx.x] =
+        __uint_as_float((uint32_t)(127 - e) << 23);
+  __half* hi = reinterpret_cast<__half*>(a.dst + (uint64_t)((int64_t)dev * a.dst_dev));
+  __half* lo = hi + (int64_t)a.rows * a.pitch;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = r0 + i * 8 + warp;
+    if (r >= a.rows || c >= a.cols) continue;
+    const float y0 = __fmul_rn(v[i].x, up), y1 = __fmul_rn(v[i].y, up);
+    const float y2 = __fmul_rn(v[i].z, up), y3 = __fmul_rn(v[i].w, up);
+    const __half2 h01 = __floats2half2_rn(y0, y1), h23 = __floats2half2_rn(y2, y3);
+    const float2 b01 = __half22float2(h01), b23 = __half22float2(h23);
+    const __half2 l01 = __floats2half2_rn(__fsub_rn(y0, b01.x), __fsub_rn(y1, b01.y));
+    const __half2 l23 = __floats2half2_rn(__fsub_rn(y2, b23.x), __fsub_rn(y3, b23.y));
+    const int64_t o = (int64_t)r * a.pitch + c;
+    if (c + 3 < a.cols) {
+      uint2 hv, lv;
+      hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+      lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+      *reinterpret_cast<uint2*>(hi + o) = hv;
+      *reinterpret_cast<uint2*>(lo + o) = lv;
+    } else {
+      const __half hh[4] = {__low2half(h01), __high2half(h01), __low2half(h23), __high2half(h23)};
+      const __half ll[4] = {__low2half(l01), __high2half(l01), __low2half(l23), __high2half(l23)};
+      for (int j = 0; j < 4 && c + j < a.cols; ++j) {
+        hi[o + j] = hh[j];
+        lo[o + j] = ll[j];
+      }
+    }
+  }
+}
+
+struct H3Args {
+  int M, N, K;
+  int a_mn_major, b_k_major;
+  int tiles_m, tiles_n, tiles;
+  int tma_store;
+  uint64_t c_base;
+  int64_t dev_stride;                  // bytes (C)
+  int64_t ldc;
+  uint64_t sa, sb;                     // device-0 addresses of the operand scales
+  int64_t sa_dev, sb_dev;              // bytes
+  int64_t sa_m, sa_k, sb_n, sb_k;      // element strides of the scale grids
+  int rb_a;                            // A row blocks (guards the last pair's second CTA)
+};
+
+template <bool LEADER_BAR>
+SPX_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2, int c3) {
+  if (LEADER_BAR)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+
+// collector: 0 none, 1 fill A, 2 last use of A
+template <int COLLECT>
+SPX_DEV void mma_f16_ss(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+#define SPX_MMA16(SUFFIX)                                                                    \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                             \
+               "tcgen05.mma.cta_group::2.kind::f16" SUFFIX " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d), \
+               "l"(da), "l"(db), "r"(idesc), "r"(acc))
+  if (COLLECT == 1) SPX_MMA16(".collector::a::fill");
+  else if (COLLECT == 2) SPX_MMA16(".collector::a::lastuse");
+  else SPX_MMA16("");
+#undef SPX_MMA16
+}
+
+__global__ void __launch_bounds__(H_THREADS, 1)
+gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+               const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ H3Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + H_BAR_OFF);
+  uint64_t* raw_empty = raw_full + H_RS;
+  uint64_t* tfull = raw_empty + H_RS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (args.K + HBK - 1) / HBK;
+  uint32_t crank = 0;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int pair0 = blockIdx.x / H_CG, npairs = gridDim.x / H_CG;
+  auto a_hi = [&](int s) { return smem + s * H_STAGE; };
+  auto b_hi = [&](int s) { return smem + s * H_STAGE + 2 * H_A_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < H_RS; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4 * H_CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_d = *tmem_slot;
+  SPX_PDL_ENTRY();
+
+  auto tile_of = [&](int t, int& m0, int& n0, int& dev) {
+    const int per_dev = args.tiles_m * args.tiles_n;
+    dev = t / per_dev;
+    const int r = t - dev * per_dev;
+    const int n_blk = r / args.tiles_m;        // M fastest: concurrent pairs share B panels
+    m0 = (r - n_blk * args.tiles_m) * (HB * H_CG);
+    n0 = n_blk * HBN;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; loads land on the leader's barrier) ----------------
+    uint32_t lead_full0;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full0) : "r"(smem_u32(&raw_full[0])));
+    int g = 0;
+    for (int t = pair0; t < args.tiles; t += npairs) {
+      int m0, n0, dev;
+      tile_of(t, m0, n0, dev);
+      m0 += (int)crank * HB;
+      const int nb0 = n0 + (int)crank * H_BNH;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % H_RS;
+        mbar_wait(&raw_empty[s], ((g / H_RS) & 1) ^ 1);
+        if (elect_one()) {
+          if (crank == 0) mbar_expect_tx(&raw_full[s], (uint32_t)(H_CG * H_STAGE));
+          const uint32_t bar = lead_full0 + (uint32_t)(s * 8);
+          const int k0 = kb * HBK;
+          uint8_t* st = a_hi(s);
+#pragma unroll
+          for (int piece = 0; piece < 2; ++piece) {
+            uint8_t* da = st + piece * H_A_BYTES;
+            if (args.a_mn_major) {
+              tma_load_4d<true>(da, &tma_a, bar, m0, k0, piece, dev);
+              tma_load_4d<true>(da + H_A_BYTES / 2, &tma_a, bar, m0 + 64, k0, piece, dev);
+            } else {
+              tma_load_4d<true>(da, &tma_a, bar, k0, m0, piece, dev);
+            }
+            uint8_t* db = b_hi(s) + piece * H_B_BYTES;
+            if (args.b_k_major) tma_load_4d<true>(db, &tma_b, bar, k0, nb0, piece, dev);
+            else tma_load_4d<true>(db, &tma_b, bar, nb0, k0, piece, dev);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1 && crank == 0) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    // kind::f16 idesc: D f32 (bit 4), A/B fp16 (0), K- or MN-major per operand
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(args.a_mn_major ? 1 : 0) << 15) |
+                           ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(HBN >> 3) << 17) |
+                           ((uint32_t)((HB * H_CG) >> 4) << 24);
+    // SWIZZLE_128B descriptors: K-major rows of 128 B, 8-row groups 1 KB apart,
+    // one k-step (16 fp16) = 32 B along the row; MN-major: 64-element MN
+    // chunks (one TMA box, 8 KB) apart by LBO, 8-k groups by SBO, one k-step =
+    // 16 rows of 128 B.
+    const uint32_t a_lbo = args.a_mn_major ? (uint32_t)(H_A_BYTES / 2) : 16u;
+    const uint32_t a_step = args.a_mn_major ? 2048u : 32u;
+    const uint32_t b_lbo = args.b_k_major ? 16u : (uint32_t)H_B_BYTES;
+    const uint32_t b_step = args.b_k_major ? 32u : 2048u;
+    const uint64_t da0 = smem_desc(smem_u32(a_hi(0)), a_lbo, 1024u, 2u);
+    const uint64_t db0 = smem_desc(smem_u32(b_hi(0)), b_lbo, 1024u, 2u);
+    const uint64_t dak = a_step >> 4, dbk = b_step >> 4;
+    const uint64_t alo = H_A_BYTES >> 4, blo = H_B_BYTES >> 4;
+    int rs = 0;
+    uint32_t rph = 0;
+    int cg = 0;
+    for (int t = pair0; t < args.tiles; t += npairs) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int kin = kb & 1;
+        const int buf = cg & 1;
+        const bool chunk_last = kin == 1 || kb == nk - 1;
+        if (kin == 0) mbar_wait<true>(&tempty[buf], ((cg >> 1) & 1) ^ 1);
+        mbar_wait<true>(&raw_full[rs], rph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = da0 + (uint64_t)(rs * (H_STAGE >> 4));
+        const uint64_t db = db0 + (uint64_t)(rs * (H_STAGE >> 4));
+        const uint32_t dacc = tmem_d + (uint32_t)(buf * HBN);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HBK / 16; ++kk) {
+            const uint64_t ah = da + kk * dak, bh = db + kk * dbk;
+            mma_f16_ss<1>(dacc, ah, bh + blo, idesc, (kin | kk) ? 1u : 0u);   // hi.lo
+            mma_f16_ss<2>(dacc, ah, bh, idesc, 1u);                           // hi.hi
+            mma_f16_ss<0>(dacc, ah + alo, bh, idesc, 1u);                     // lo.hi
+          }
+          mma_commit<2>(&raw_empty[rs]);
+          if (chunk_last) mma_commit<2>(&tfull[buf]);
+        }
+        __syncwarp();
+        if (++rs == H_RS) { rs = 0; rph ^= 1u; }
+        if (chunk_last) ++cg;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- drain: scaled fp32 promotion of every k chunk, C stores ----------------
+    const int q = warp & 3;
+    const int nchunks = (nk + 1) / 2;
+    int cg = 0;
+    for (int t = pair0; t < args.tiles; t += npairs) {
+      int m0, n0, dev;
+      tile_of(t, m0, n0, dev);
+      m0 += (int)crank * HB;
+      const int mblk = m0 / HB, nblk = n0 / HB;
+      const float* sa = reinterpret_cast<const float*>(args.sa + (uint64_t)((int64_t)dev * args.sa_dev)) + mblk * args.sa_m;
+      const float* sb = reinterpret_cast<const float*>(args.sb + (uint64_t)((int64_t)dev * args.sb_dev)) + nblk * args.sb_n;
+      const bool rows_exist = mblk < args.rb_a;
+      float acc[HBN];
+#pragma unroll
+      for (int j = 0; j < HBN; ++j) acc[j] = 0.f;
+      for (int c = 0; c < nchunks; ++c, ++cg) {
+        const int buf = cg & 1;
+        const float f = rows_exist ? __fmul_rn(sa[c * args.sa_k], sb[c * args.sb_k]) : 0.f;
+        mbar_wait(&tfull[buf], (cg >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int cc = 0; cc < HBN / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * HBN + cc * 32), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __fmaf_rn(__uint_as_float(v[j]), f, acc[cc * 32 + j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          uint32_t r;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(&tempty[buf])));
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+        }
+      }
+      const int row0 = m0 + q * 32;
+      if (row0 >= args.M) continue;
+      if (args.tma_store) {
+        // each 32 x 32 slice through a 128B-swizzled staging tile, one bulk tensor store
+        uint8_t* stg = smem + H_STG_OFF + q * H_STG_WARP;
+#pragma unroll
+        for (int cc = 0; cc < HBN / 32; ++cc) {
+          if (n0 + cc * 32 >= args.N) break;
+          uint8_t* tt = stg + (cc & 1) * 4096;
+          if (cc >= 2) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(tt + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
+                            acc[cc * 32 + 4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tma_c)),
+                "r"(n0 + cc * 32), "r"(row0), "r"(dev), "r"(smem_u32(tt))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      } else {
+        const int row = row0 + lane;
+        if (row < args.M) {
+          float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
+                        (int64_t)row * args.ldc;
+#pragma unroll
+          for (int j = 0; j < HBN; ++j)
+            if (n0 + j < args.N) crow[n0 + j] = acc[j];
+        }
+      }
+    }
+  }
+  if (warp >= 4 && args.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem_d));
+  }
+}
+
+// 4-D fp16 pieces map {cols, rows, piece, device}, box {64, box_rows, 1, 1}, 128B swizzle.
+int make_map_h16(CUtensorMap* map, uint64_t addr, uint64_t cols, uint64_t rows, uint64_t ndev, uint64_t pitch,
+                 uint64_t dev_bytes, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return spx_set_error("cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {cols, rows, 2, ndev};
+  cuuint64_t strides[3] = {pitch * 2, rows * pitch * 2, dev_bytes};
+  cuuint32_t box[4] = {64, box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, reinterpret_cast<void*>(addr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return spx_set_error("cuTensorMapEncodeTiled (fp16 pieces) failed (%d)", (int)r);
+  return 0;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Geometry of one operand's pieces in the workspace.
+struct Operand {
+  uint64_t src;
+  int64_t ld;
+  int rows, cols, rb, cb;
+  int64_t pitch, piece_dev, scl_dev;   // bytes per device of pieces / scales
+  int64_t piece_off, scl_off;          // offsets in the workspace
+};
+
+void operand_geom(Operand& o, uint64_t src, int64_t ld, int rows, int cols, int ndev, int64_t& ws) {
+  o.src = src;
+  o.ld = ld;
+  o.rows = rows;
+  o.cols = cols;
+  o.rb = (rows + HB - 1) / HB;
+  o.cb = (cols + HB - 1) / HB;
+  o.pitch = align_up(cols, 8);
+  o.piece_dev = align_up(2 * (int64_t)rows * o.pitch * 2, 1024);
+  o.scl_dev = align_up((int64_t)o.rb * o.cb * 4, 256);
+  o.piece_off = ws;
+  ws += o.piece_dev * ndev;
+  o.scl_off = ws;
+  ws += o.scl_dev * ndev;
+  ws = align_up(ws, 1024);
+}
+
+}  // namespace
+
+struct SpxGemmH3 {
+  spx_gemm_params p;
+  Operand A, B;
+  int64_t ws_bytes = 0;
+  uint64_t ws = 0;
+  CUtensorMap ma, mb, mc;
+  H3Args args;
+  SplitArgs sa, sb;
+  dim3 grid;
+};
+
+bool spx_gemm_h3_supported(const spx_gemm_params& p) {
+  return spx_gemm_tc_supported(p) && p.splits <= 1 && p.epi == SPX_EPI_NONE;
+}
+
+int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out) {
+  if (!spx_gemm_h3_supported(p)) return spx_set_error("gemm %dx%dx%d: block-scaled fp16 path unsupported", p.M, p.N, p.K);
+  SpxGemmH3* g = new SpxGemmH3();
+  g->p = p;
+  const uint64_t a = p.base + (uint64_t)(p.a_off * 4), b = p.base + (uint64_t)(p.b_off * 4);
+  int64_t ws = 0;
+  if (p.a_mn_major) operand_geom(g->A, a, p.lda, p.K, p.M, p.ndev, ws);
+  else operand_geom(g->A, a, p.lda, p.M, p.K, p.ndev, ws);
+  if (p.b_k_major) operand_geom(g->B, b, p.ldb, p.N, p.K, p.ndev, ws);
+  else operand_geom(g->B, b, p.ldb, p.K, p.N, p.ndev, ws);
+  g->ws_bytes = ws;
+  *out = g;
+  return 0;
+}
+
+int64_t spx_gemm_h3_ws_bytes(const SpxGemmH3* g) { return g->ws_bytes; }
+
+static void split_args(SplitArgs& s, const Operand& o, const spx_gemm_params& p, uint64_t ws) {
+  s.src = o.src;
+  s.src_dev = p.dev_stride;
+  s.ld = o.ld;
+  s.rows = o.rows;
+  s.cols = o.cols;
+  s.dst = ws + (uint64_t)o.piece_off;
+  s.dst_dev = o.piece_dev;
+  s.pitch = o.pitch;
+  s.scl = ws + (uint64_t)o.scl_off;
+  s.scl_dev = o.scl_dev;
+  s.cb = o.cb;
+}
+
+int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
+  const spx_gemm_params& p = g->p;
+  g->ws = ws;
+  const Operand &A = g->A, &B = g->B;
+  if (make_map_h16(&g->ma, ws + A.piece_off, A.cols, A.rows, p.ndev, A.pitch, A.piece_dev, p.a_mn_major ? 64 : HB))
+    return -1;
+  if (make_map_h16(&g->mb, ws + B.piece_off, B.cols, B.rows, p.ndev, B.pitch, B.piece_dev, 64)) return -1;
+  split_args(g->sa, A, p, ws);
+  split_args(g->sb, B, p, ws);
+  H3Args& a_ = g->args;
+  a_.M = p.M; a_.N = p.N; a_.K = p.K;
+  a_.a_mn_major = p.a_mn_major;
+  a_.b_k_major = p.b_k_major;
+  a_.tiles_m = (p.M + HB * H_CG - 1) / (HB * H_CG);
+  a_.tiles_n = (p.N + HBN - 1) / HBN;
+  a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
+  a_.c_base = p.base + (uint64_t)(p.c_off * 4);
+  a_.dev_stride = p.dev_stride;
+  a_.ldc = p.ldc;
+  a_.sa = ws + (uint64_t)A.scl_off;
+  a_.sb = ws + (uint64_t)B.scl_off;
+  a_.sa_dev = A.scl_dev;
+  a_.sb_dev = B.scl_dev;
+  // A stored [M][K]: scales [m-block][k-block]; stored [K][M]: [k-block][m-block]
+  a_.sa_m = p.a_mn_major ? 1 : A.cb;
+  a_.sa_k = p.a_mn_major ? A.cb : 1;
+  a_.sb_n = p.b_k_major ? B.cb : 1;
+  a_.sb_k = p.b_k_major ? 1 : B.cb;
+  a_.rb_a = (p.M + HB - 1) / HB;
+  a_.tma_store = 0;
+  const char* e = getenv("SPX_GEMM_TMA_STORE");
+  if (!(e && e[0] == '0') && (a_.c_base & 15) == 0 && (p.ldc & 3) == 0 && (p.dev_stride & 15) == 0) {
+    if (make_map(&g->mc, a_.c_base, p.N, p.M, p.ndev, p.ldc * 4, p.dev_stride, 32, false)) return -1;
+    a_.tma_store = 1;
+  } else {
+    memset(&g->mc, 0, sizeof(g->mc));
+  }
+  int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
+  sms -= sms % H_CG;
+  if (sms < H_CG) sms = H_CG;
+  const int want = a_.tiles * H_CG;
+  g->grid = dim3((unsigned)(want < sms ? want : sms));
+  return 0;
+}
+
+int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
+  if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
+  const spx_gemm_params& p = g->p;
+  spx_launch(split_h16_kernel, dim3(g->A.cb, g->A.rb, p.ndev), dim3(256), 0, s, g->sa);
+  SPX_CHECK_LAUNCH();
+  spx_launch(split_h16_kernel, dim3(g->B.cb, g->B.rb, p.ndev), dim3(256), 0, s, g->sb);
+  SPX_CHECK_LAUNCH();
+  static bool attr = false;
+  if (!attr) {
+    SPX_CUDA(cudaFuncSetAttribute(gemm_h3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H_TOTAL));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g->grid;
+  cfg.blockDim = dim3(H_THREADS);
+  cfg.dynamicSmemBytes = H_TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = H_CG;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
+  if (spx_pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  SPX_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel, g->ma, g->mb, g->mc, g->args));
+  SPX_CHECK_LAUNCH();
+  if (nlaunch) *nlaunch += 3;
+  return 0;
+}
+
+void spx_gemm_h3_free(SpxGemmH3* g) { delete g; }

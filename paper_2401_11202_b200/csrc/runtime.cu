@@ -22,6 +22,17 @@ int spx_set_error(const char* fmt, ...) {
 
 static int g_num_sms = 148;
 int spx_num_sms() { return g_num_sms; }
+// GEMMs the plan leaves to the backend (path 0) take the block-scaled 3xFP16
+// kernel where it applies; SPX_GEMM_H3=0 keeps them on 3xTF32.
+static bool h3_default() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SPX_GEMM_H3");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
 bool spx_pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -133,6 +144,7 @@ struct Record {
   int path;  // GEMM: 1 tcgen05, 2 simt
   std::vector<uint8_t> params;
   SpxGemmTC* tc = nullptr;
+  SpxGemmH3* h3 = nullptr;      // path 3: block-scaled 3xFP16 (gemm_h3.cu)
   int stream = 0;               // 0 main, 1..SPX_SIDE_STREAMS side streams
   std::vector<int> waits;       // records on other streams to wait for
   bool signal = false;          // a later record on another stream waits for this one
@@ -151,6 +163,7 @@ struct Plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
+  void* h3ws[SPX_SIDE_STREAMS + 1] = {};   // fp16-pieces workspace per stream (GEMMs of a stream run in order)
 };
 
 static int run_record(Record& r, cudaStream_t s, int* nl) {
@@ -162,6 +175,7 @@ static int run_record(Record& r, cudaStream_t s, int* nl) {
     case SPX_K_GATHER: return spx_launch_gather(*reinterpret_cast<const spx_gather_params*>(r.params.data()), s, nl);
     case SPX_K_CREDUCE: return spx_launch_creduce(*reinterpret_cast<const spx_creduce_params*>(r.params.data()), s, nl);
     case SPX_K_GEMM:
+      if (r.path == 3) return spx_gemm_h3_launch(r.h3, s, nl);
       if (r.path == 1) return spx_gemm_tc_launch(r.tc, s, nl);
       return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
     case SPX_K_NCCL: return run_nccl(*reinterpret_cast<const spx_nccl_params*>(r.params.data()), s);
@@ -319,7 +333,14 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
     const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
     const bool tc_ok = spx_gemm_tc_supported(g);
     if (g.path == 1 && !tc_ok) return spx_set_error("gemm %dx%dx%d: tcgen05 path requested but operands unsupported", g.M, g.N, g.K);
-    r.path = (g.path == 2 || (g.path == 0 && !tc_ok)) ? 2 : 1;
+    if (g.path == 3) {
+      if (!spx_gemm_h3_supported(g))
+        return spx_set_error("gemm %dx%dx%d: block-scaled fp16 path requested but unsupported", g.M, g.N, g.K);
+      r.path = 3;
+    } else {
+      r.path = (g.path == 2 || (g.path == 0 && !tc_ok)) ? 2 : 1;
+      if (g.path == 0 && r.path == 1 && h3_default() && spx_gemm_h3_supported(g)) r.path = 3;
+    }
     if (g.splits > 1 && r.path != 1) return spx_set_error("gemm %dx%dx%d: split-K needs the tcgen05 path", g.M, g.N, g.K);
     if (g.epi != SPX_EPI_NONE && r.path != 1) return spx_set_error("gemm %dx%dx%d: fused epilogue needs the tcgen05 path", g.M, g.N, g.K);
   }
@@ -329,12 +350,22 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
 
 int spx_plan_finalize(uint64_t plan) {
   Plan* P = reinterpret_cast<Plan*>(plan);
+  int64_t h3need[SPX_SIDE_STREAMS + 1] = {};
   for (auto& r : P->recs) {
     if (r.kind == SPX_K_GEMM && r.path == 1 && !r.tc) {
       if (spx_gemm_tc_prepare(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), &r.tc)) return -1;
     }
+    if (r.kind == SPX_K_GEMM && r.path == 3 && !r.h3) {
+      if (spx_gemm_h3_prepare(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), &r.h3)) return -1;
+      const int64_t b = spx_gemm_h3_ws_bytes(r.h3);
+      if (b > h3need[r.stream]) h3need[r.stream] = b;
+    }
     if (r.signal && !r.done) SPX_CUDA(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
   }
+  for (int k = 0; k <= SPX_SIDE_STREAMS; ++k)
+    if (h3need[k] && !P->h3ws[k]) SPX_CUDA(cudaMalloc(&P->h3ws[k], (size_t)h3need[k]));
+  for (auto& r : P->recs)
+    if (r.h3 && spx_gemm_h3_bind(r.h3, reinterpret_cast<uint64_t>(P->h3ws[r.stream]))) return -1;
   if (P->two_streams) {
     int lo = 0, hi = 0;
     SPX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -450,6 +481,7 @@ int spx_plan_destroy(uint64_t plan) {
   if (P->graph) cudaGraphDestroy(P->graph);
   for (auto& r : P->recs) {
     if (r.tc) spx_gemm_tc_free(r.tc);
+    if (r.h3) spx_gemm_h3_free(r.h3);
     if (r.done) cudaEventDestroy(r.done);
   }
   for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
@@ -457,6 +489,8 @@ int spx_plan_destroy(uint64_t plan) {
     if (P->join[k]) cudaEventDestroy(P->join[k]);
   }
   if (P->fork) cudaEventDestroy(P->fork);
+  for (int k = 0; k <= SPX_SIDE_STREAMS; ++k)
+    if (P->h3ws[k]) cudaFree(P->h3ws[k]);
   delete P;
   return 0;
 }

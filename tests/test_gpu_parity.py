@@ -109,6 +109,54 @@ def test_gemm_tcgen05_3xtf32(shape, at, bt):
     assert O.relative_error(got, A @ B) < TOL
 
 
+@pytest.mark.parametrize("at,bt", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("shape", [s for s in GEMM_SHAPES if s != (130, 70, 200)] + [(256, 72, 136), (320, 200, 96)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_gemm_h3_block_scaled(shape, at, bt):
+    """Block-scaled 3xFP16 GEMM (gemm_h3.cu) vs float64: <= 1e-5 max-normalised."""
+    pkg = _pkg()
+    M, K, N = shape
+    rng = np.random.default_rng(hash(shape) % 1000 + 7)
+    a = rng.standard_normal((K, M) if at else (M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K) if bt else (K, N)).astype(np.float32)
+    A = a.T if at else a
+    B = b.T if bt else b
+    (got,) = pkg.interpret(_mm_module(M, K, N, at, bt), {"a": a, "b": b}, gemm_path=3)
+    assert np.all(np.isfinite(got))
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    assert O.relative_error(got, want) < TOL
+    assert O.relative_error(got, A @ B) < TOL
+
+
+@pytest.mark.parametrize("at,bt", [(False, False), (True, True)])
+def test_gemm_h3_dynamic_range(at, bt):
+    """Per-block scales: 128 x 128 blocks spanning 2^-40 .. 2^40, zero blocks,
+    tiny and huge rows -- still <= 1e-5 against float64, per output block too."""
+    pkg = _pkg()
+    M, K, N = 512, 768, 384
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    for i in range(M // 128):
+        for k in range(K // 128):
+            A[i * 128:(i + 1) * 128, k * 128:(k + 1) * 128] *= 2.0 ** rng.integers(-40, 40)
+    A[128:256, 256:384] = 0.0
+    B[:, 5] *= 2.0 ** -30
+    B[7, :] *= 2.0 ** 30
+    A = A.astype(np.float32)
+    B = B.astype(np.float32)
+    a = np.ascontiguousarray(A.T) if at else A
+    b = np.ascontiguousarray(B.T) if bt else B
+    (got,) = pkg.interpret(_mm_module(M, K, N, at, bt), {"a": a, "b": b}, gemm_path=3)
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.all(np.isfinite(got))
+    assert O.relative_error(got, want) < TOL
+    # accuracy does not hinge on the global maximum: every output row block on its own
+    for i in range(M // 128):
+        sl = slice(i * 128, (i + 1) * 128)
+        assert O.relative_error(got[sl], want[sl]) < TOL, i
+
+
 @pytest.mark.parametrize("shape", [(5, 7, 3), (64, 48, 80), (130, 70, 200), (256, 512, 384)])
 def test_gemm_simt(shape):
     pkg = _pkg()
@@ -250,7 +298,7 @@ def test_gemm_fused_epilogue_bitexact(epi, monkeypatch):
     monkeypatch.setenv("SPX_EPILOGUE", "1")
     fused = pkg.interpret(m, ins)
     monkeypatch.setenv("SPX_EPILOGUE", "0")
-    plain = pkg.interpret(m, ins)
+    plain = pkg.interpret(m, ins, gemm_path=1)     # the fused epilogues live on the 3xTF32 kernel
     want = O.interpret(m, ins)
     for f, p, w in zip(fused, plain, want):
         np.testing.assert_array_equal(f, p)

@@ -15,15 +15,16 @@ SHAPES = [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
           (1024, 256, 1024, False, False), (1024, 1024, 256, False, False)]
 if os.environ.get("SHAPES"):
     SHAPES = [SHAPES[int(i)] for i in os.environ["SHAPES"].split(",")]
-for (M, N, K, at, bt) in SHAPES:
+PATHS = [int(x) for x in os.environ.get("GPATHS", "1,3").split(",")]
+for (M, N, K, at, bt), path in [(s, p) for s in SHAPES for p in PATHS]:
     A = rng.standard_normal((K, M) if at else (M, K)).astype(np.float32)
     B = rng.standard_normal((N, K) if bt else (K, N)).astype(np.float32)
-    g = G(dev, A, B, at, bt)
+    g = G(dev, A, B, at, bt, path=path)
     C = g.run()
     AA = A.T if at else A
     BB = B.T if bt else B
     err = rel(C, AA.astype(np.float64) @ BB)
     ms = g.time_ms(10)
     g.close()
-    print(f"{M}x{N}x{K} a_mn={int(at)} b_k={int(bt)} {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:6.1f} TF fp32-eq "
-          f"({3*2*M*N*K/ms/1e9/807.55*100:4.1f}% tf32 peak) rel err {err:.2e}", flush=True)
+    print(f"path {path} {M}x{N}x{K} a_mn={int(at)} b_k={int(bt)} {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:6.1f} TF fp32-eq "
+          f" rel err {err:.2e}", flush=True)
