@@ -304,7 +304,8 @@ def main():
     cls_ms = {}
     for idx, ((kind, p), t) in enumerate(zip(recs, rec_ms)):
         name = {R.K_EW: "elementwise", R.K_REDUCE: "reduce", R.K_GEMM: "gemm", R.K_GATHER: "relayout",
-                R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl", R.K_PEER: "peer_allreduce"}[kind]
+                R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl", R.K_PEER: "peer_allreduce",
+                R.K_SPLIT: "gemm_operand_split"}[kind]
         cls_ms[name] = cls_ms.get(name, 0.0) + float(t)
         if kind == R.K_GEMM:
             path = sess.ex.plan.record_info(idx)[1]
@@ -324,11 +325,11 @@ def main():
                 "frac": (ideal_ms / gemm_ms) if gemm_ms > 0 else 0.0,
                 "traffic": None,
                 "gemm_paths": {("h3" if k == 3 else "tf32" if k == 1 else "simt"): v for k, v in paths.items()},
-                "note": (f"achieved = tensor-core work (3 MMAs per fp32 FLOP) / GEMM record time (the 3xFP16 "
-                         f"records include their two operand-split kernels), summed over the "
+                "note": (f"achieved = tensor-core work (3 MMAs per fp32 FLOP) / GEMM record time, summed over the "
                          f"{sum(paths.values())} GEMM launches of one step; peak = {src} dense bf16 "
                          f"{bf16:.1f} TF/s for kind::f16, measured tcgen05 kind::tf32 rate {TF32_MMA_PEAK:.0f} "
-                         f"TF/s for 3xTF32 records (time-weighted).  fp32-equivalent GEMM rate "
+                         f"TF/s for 3xTF32 records (time-weighted).  The fp32 -> fp16-pieces operand splits are "
+                         f"separate HBM-bound records (step_ms_by_class.gemm_operand_split).  fp32-equivalent GEMM rate "
                          f"{gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0:.1f} TFLOP/s"),
                 "step_ms_by_class": {k: round(v, 4) for k, v in sorted(cls_ms.items())},
                 "gemm_share_of_step": (gemm_ms / float(np.sum(rec_ms))) if np.sum(rec_ms) > 0 else None}

@@ -29,6 +29,8 @@
  *   SPX_K_CREDUCE  spmd_interp.py:66-71,92-104   all_reduce / reduce_scatter
  *                                         (left fold in group order)
  *   SPX_K_NCCL     same collectives across processes (one GPU per mesh device)
+ *   SPX_K_SPLIT    (no reference counterpart) fp32 operand -> block-scaled fp16
+ *                  pieces feeding the 3xFP16 matmul path
  */
 #ifndef SPINDLE_B200_H
 #define SPINDLE_B200_H
@@ -139,7 +141,28 @@ typedef struct {
    * must be co-resident: tiles x splits x 2 <= SM count. */
   int32_t sk_mode, sk_pad;
   int64_t ws_off, flag_off;
+  /* path 3 (block-scaled 3xFP16, splits == 1, no epilogue): with h3_shared the
+   * operands' fp16 pieces and scales were written by SPX_K_SPLIT records into
+   * the arena (offsets in elements from the device base; one split serves
+   * every GEMM that reads the same tensor view); without it the record splits
+   * its operands itself into a per-stream workspace. */
+  int32_t h3_shared, h3_pad;
+  int64_t h3_a_off, h3_a_scl, h3_b_off, h3_b_scl;
 } spx_gemm_params;
+
+/* ---- operand split for the block-scaled 3xFP16 GEMM ------------------------
+ * fp32 view [rows][cols] (row pitch ld) -> per 128 x 128 block a power-of-two
+ * scale s (max |x| * s in [2^14, 2^15)), fp16 pieces hi = rn(x s),
+ * lo = rn(x s - hi) at dst_off: [2][rows][pitch] halves, and 1/s per block at
+ * scl_off: [ceil(rows/128)][ceil(cols/128)] fp32. */
+typedef struct {
+  uint64_t base;
+  int64_t dev_stride;             /* bytes */
+  int32_t ndev, rows, cols, pad;
+  int64_t src_off, ld;            /* elements */
+  int64_t dst_off, pitch;         /* pieces: elements from the device base; pitch in halves (multiple of 8) */
+  int64_t scl_off;                /* elements */
+} spx_split_params;
 
 enum spx_epilogue { SPX_EPI_NONE = 0, SPX_EPI_ADD = 1, SPX_EPI_SQUARE = 2, SPX_EPI_MULSCALE = 3,
                     SPX_EPI_MOMENTUM = 4 };
@@ -199,7 +222,7 @@ typedef struct {
 
 /* ---- plan records --------------------------------------------------------- */
 enum spx_kind { SPX_K_EW = 1, SPX_K_REDUCE = 2, SPX_K_GEMM = 3, SPX_K_GATHER = 4,
-                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6, SPX_K_PEER = 7 };
+                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6, SPX_K_PEER = 7, SPX_K_SPLIT = 8 };
 
 /* library / device */
 const char* spx_last_error(void);

@@ -7,6 +7,7 @@
 // interpretation overhead -- ncu showed the interpreter latency-bound at
 // 0.9-1.7 TB/s on exactly these programs.
 #include "interp.cuh"
+#include "h3_split.cuh"
 
 namespace {
 
@@ -91,10 +92,90 @@ __global__ void __launch_bounds__(256) ew_static_kernel(const __grid_constant__ 
   }
 }
 
+// Pieces of output `which` for the block-scaled 3xFP16 GEMM (h3_split.cuh):
+// the output viewed as [rows][cols] row-major, pieces [2][rows][pitch] fp16.
+struct EwSplit {
+  uint64_t dst, scl;        // device-0 addresses
+  int64_t dev_stride, pitch;
+  int rows, cols, cb, which;
+};
+
+// The same program over 128 x 128 output blocks, a cluster of H3_CL CTAs per
+// block (32 rows each): outputs are stored as usual, and the block maximum of
+// output `which` (exchanged through distributed shared memory) gives the
+// scale for its fp16 pieces -- the split the GEMMs reading this output need,
+// without reading it back from HBM.
+template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
+__global__ void __cluster_dims__(H3_CL, 1, 1) __launch_bounds__(256)
+ew_static_split_kernel(const __grid_constant__ spx_ew_params p, const __grid_constant__ EwSplit q) {
+  __shared__ float wmax[8];
+  __shared__ float cmax[H3_CL];
+  SPX_PDL_ENTRY();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = blockIdx.z;
+  const int crank = blockIdx.x % H3_CL, bx = blockIdx.x / H3_CL;
+  const int r0 = blockIdx.y * H3_BLOCK + crank * H3_ROWS;
+  const int c = bx * H3_BLOCK + lane * 4;
+  const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
+  float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
+  const bool two_d = p.rank == 2;
+  const int64_t ecols = two_d ? p.dims[1] : p.numel;
+  float* out0 = ob + p.out_off[0];
+  float* out1 = ob + p.out_off[NOUT > 1 ? 1 : 0];
+  float4 keep[H3_V];
+  float m = 0.f;
+#pragma unroll
+  for (int i = 0; i < H3_V; ++i) {
+    const int row = r0 + i * 8 + warp;
+    keep[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row >= q.rows || c >= q.cols) continue;
+    const int64_t e = (int64_t)row * q.cols + c;
+    const int64_t erow = two_d ? e / ecols : 0;
+    const int64_t ecol = e - erow * ecols;
+    Vec<4> r[SPX_NREG];
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) {
+      const float* src = fb + p.in[j].off + (two_d ? erow * p.in[j].stride[0] : 0);
+      if (p.in[j].stride[p.rank - 1] != 0) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(src + ecol));
+        r[j].v[0] = t.x; r[j].v[1] = t.y; r[j].v[2] = t.z; r[j].v[3] = t.w;
+      } else {
+        const float t = __ldg(src);
+        r[j].v[0] = t; r[j].v[1] = t; r[j].v[2] = t; r[j].v[3] = t;
+      }
+    }
+    run_static<I...>(r, p.imm, std::make_integer_sequence<int, (int)sizeof...(I)>{});
+    const float4 y0 = make_float4(r[O0].v[0], r[O0].v[1], r[O0].v[2], r[O0].v[3]);
+    *reinterpret_cast<float4*>(out0 + e) = y0;
+    if (NOUT > 1) {
+      const float4 y1 = make_float4(r[O1].v[0], r[O1].v[1], r[O1].v[2], r[O1].v[3]);
+      *reinterpret_cast<float4*>(out1 + e) = y1;
+      keep[i] = q.which ? y1 : y0;
+    } else {
+      keep[i] = y0;
+    }
+    m = h3_absmax4(m, keep[i]);
+  }
+  m = h3_cluster_max(m, wmax, cmax, crank);
+  const int ex = h3_scale_exp(m);
+  const float up = h3_pow2(ex);
+  if (threadIdx.x == 0 && crank == 0)
+    reinterpret_cast<float*>(q.scl + (uint64_t)((int64_t)d * q.dev_stride))[blockIdx.y * q.cb + bx] = h3_pow2(-ex);
+  __half* hi = reinterpret_cast<__half*>(q.dst + (uint64_t)((int64_t)d * q.dev_stride));
+  __half* lo = hi + (int64_t)q.rows * q.pitch;
+#pragma unroll
+  for (int i = 0; i < H3_V; ++i) {
+    const int row = r0 + i * 8 + warp;
+    if (row >= q.rows || c >= q.cols) continue;
+    h3_store4(hi, lo, (int64_t)row * q.pitch + c, keep[i], up, 4);
+  }
+}
+
 struct Entry {
   int n_in, n_out, out0, out1, n_prog;
   uint32_t prog[8];
   void (*launch)(const spx_ew_params&, dim3, cudaStream_t);
+  void (*launch_split)(const spx_ew_params&, const EwSplit&, dim3, cudaStream_t);
 };
 
 template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
@@ -102,10 +183,16 @@ void launch_static(const spx_ew_params& p, dim3 g, cudaStream_t s) {
   spx_launch(ew_static_kernel<NIN, NOUT, O0, O1, I...>, g, 256, 0, s, p);
 }
 
+template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
+void launch_static_split(const spx_ew_params& p, const EwSplit& q, dim3 g, cudaStream_t s) {
+  spx_launch(ew_static_split_kernel<NIN, NOUT, O0, O1, I...>, g, 256, 0, s, p, q);
+}
+
 #define OP(x) SPX_OP_##x
 // The catalog (program slots as allocated by plan.Program.build).
 #define E(NIN, NOUT, O0, O1, N, ...) \
-  {NIN, NOUT, O0, O1, N, {__VA_ARGS__}, launch_static<NIN, NOUT, O0, O1, __VA_ARGS__>}
+  {NIN, NOUT, O0, O1, N, {__VA_ARGS__}, launch_static<NIN, NOUT, O0, O1, __VA_ARGS__>, \
+   launch_static_split<NIN, NOUT, O0, O1, __VA_ARGS__>}
 const Entry kCatalog[] = {
     // momentum update  m' = c0*m + g ; p' = p + -(c2*m')        (models.py:79-85)
     E(3, 2, 0, 1, 5, ins(OP(IMUL), 0, 0, 0), ins(OP(ADD), 0, 1, 0), ins(OP(IMUL), 0, 0, 1), ins(OP(NEG), 1, 0, 1),
@@ -156,6 +243,35 @@ int spx_launch_ew_static(int id, const spx_ew_params& p, cudaStream_t s, int* nl
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   kCatalog[id].launch(p, dim3((unsigned)b, (unsigned)p.ndev), s);
+  SPX_CHECK_LAUNCH();
+  if (nlaunch) ++*nlaunch;
+  return 0;
+}
+
+// Can split record `sp` be fused into static elementwise record `p`?  Returns
+// the output index it splits, or -1.
+int spx_ew_split_match(const spx_ew_params& p, const spx_split_params& sp) {
+  if (!p.vec || sp.ld != sp.cols || (int64_t)sp.rows * sp.cols != p.numel || sp.cols % 4 || sp.ndev != p.ndev ||
+      sp.base != p.base || sp.dev_stride != p.dev_stride)
+    return -1;
+  for (int j = 0; j < p.n_out; ++j)
+    if (p.out_off[j] == sp.src_off) return j;
+  return -1;
+}
+
+int spx_launch_ew_static_split(int id, const spx_ew_params& p, const spx_split_params& sp, int which,
+                               cudaStream_t s, int* nlaunch) {
+  EwSplit q;
+  q.dst = sp.base + (uint64_t)(sp.dst_off * 4);
+  q.scl = sp.base + (uint64_t)(sp.scl_off * 4);
+  q.dev_stride = sp.dev_stride;
+  q.pitch = sp.pitch;
+  q.rows = sp.rows;
+  q.cols = sp.cols;
+  q.cb = (sp.cols + H3_BLOCK - 1) / H3_BLOCK;
+  q.which = which;
+  const dim3 g((unsigned)(H3_CL * q.cb), (unsigned)((sp.rows + H3_BLOCK - 1) / H3_BLOCK), (unsigned)p.ndev);
+  kCatalog[id].launch_split(p, q, g, s);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;

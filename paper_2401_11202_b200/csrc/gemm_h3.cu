@@ -38,6 +38,7 @@
 #include <cuda_fp16.h>
 #include "common.cuh"
 #include "tc_util.cuh"
+#include "h3_split.cuh"
 
 namespace {
 
@@ -69,25 +70,32 @@ struct SplitArgs {
   int cb;
 };
 
-__global__ void __launch_bounds__(256) split_h16_kernel(const __grid_constant__ SplitArgs a) {
+// A cluster of H3_CL CTAs splits one 128 x 128 block (CTA rank r takes rows
+// 32r..32r+31): the block maximum is exchanged through distributed shared
+// memory, so a 1024 x 1024 operand spreads over 256 CTAs instead of 64.
+__global__ void __cluster_dims__(H3_CL, 1, 1) __launch_bounds__(256)
+split_h16_kernel(const __grid_constant__ SplitArgs a) {
   __shared__ float wmax[8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float cmax[H3_CL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dev = blockIdx.z;
-  const int r0 = blockIdx.y * HB, c0 = blockIdx.x * HB;
+  const int crank = blockIdx.x % H3_CL;
+  const int bx = blockIdx.x / H3_CL;
+  const int r0 = blockIdx.y * HB + crank * H3_ROWS, c0 = bx * HB;
   const float* src = reinterpret_cast<const float*>(a.src + (uint64_t)((int64_t)dev * a.src_dev));
   SPX_PDL_ENTRY();
   const bool vec = ((a.src | (uint64_t)a.src_dev | (uint64_t)(a.ld * 4)) & 15) == 0 && c0 + HB <= a.cols;
-  float4 v[16];
+  float4 v[H3_V];
   float m = 0.f;
   const int c = c0 + lane * 4;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < H3_V; ++i) {
     const int r = r0 + i * 8 + warp;
     float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < a.rows) {
       const float* p = src + (int64_t)r * a.ld + c;
       if (vec) {
-        x = __ldcs(reinterpret_cast<const float4*>(p));
+        x = *reinterpret_cast<const float4*>(p);
       } else {
         if (c < a.cols) x.x = p[0];
         if (c + 1 < a.cols) x.y = p[1];
@@ -96,49 +104,20 @@ __global__ void __launch_bounds__(256) split_h16_kernel(const __grid_constant__ 
       }
     }
     v[i] = x;
-    m = fmaxf(m, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+    m = h3_absmax4(m, x);
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) wmax[warp] = m;
-  __syncthreads();
-  m = wmax[0];
-#pragma unroll
-  for (int w = 1; w < 8; ++w) m = fmaxf(m, wmax[w]);
-  const int E = (int)((__float_as_uint(m) >> 23) & 0xFF);
-  int e = (m == 0.f || E == 255) ? 0 : 141 - E;     // max * 2^e in [2^14, 2^15)
-  e = e < -60 ? -60 : (e > 60 ? 60 : e);
-  const float up = __uint_as_float((uint32_t)(127 + e) << 23);
-  if (tid == 0)
-    reinterpret_cast<float*>(a.scl + (uint64_t)((int64_t)dev * a.scl_dev))[blockIdx.y * a.cb + blockIdx.x] =
-        __uint_as_float((uint32_t)(127 - e) << 23);
+  m = h3_cluster_max(m, wmax, cmax, crank);
+  const int e = h3_scale_exp(m);
+  const float up = h3_pow2(e);
+  if (threadIdx.x == 0 && crank == 0)
+    reinterpret_cast<float*>(a.scl + (uint64_t)((int64_t)dev * a.scl_dev))[blockIdx.y * a.cb + bx] = h3_pow2(-e);
   __half* hi = reinterpret_cast<__half*>(a.dst + (uint64_t)((int64_t)dev * a.dst_dev));
   __half* lo = hi + (int64_t)a.rows * a.pitch;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < H3_V; ++i) {
     const int r = r0 + i * 8 + warp;
     if (r >= a.rows || c >= a.cols) continue;
-    const float y0 = __fmul_rn(v[i].x, up), y1 = __fmul_rn(v[i].y, up);
-    const float y2 = __fmul_rn(v[i].z, up), y3 = __fmul_rn(v[i].w, up);
-    const __half2 h01 = __floats2half2_rn(y0, y1), h23 = __floats2half2_rn(y2, y3);
-    const float2 b01 = __half22float2(h01), b23 = __half22float2(h23);
-    const __half2 l01 = __floats2half2_rn(__fsub_rn(y0, b01.x), __fsub_rn(y1, b01.y));
-    const __half2 l23 = __floats2half2_rn(__fsub_rn(y2, b23.x), __fsub_rn(y3, b23.y));
-    const int64_t o = (int64_t)r * a.pitch + c;
-    if (c + 3 < a.cols) {
-      uint2 hv, lv;
-      hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-      lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-      *reinterpret_cast<uint2*>(hi + o) = hv;
-      *reinterpret_cast<uint2*>(lo + o) = lv;
-    } else {
-      const __half hh[4] = {__low2half(h01), __high2half(h01), __low2half(h23), __high2half(h23)};
-      const __half ll[4] = {__low2half(l01), __high2half(l01), __low2half(l23), __high2half(l23)};
-      for (int j = 0; j < 4 && c + j < a.cols; ++j) {
-        hi[o + j] = hh[j];
-        lo[o + j] = ll[j];
-      }
-    }
+    h3_store4(hi, lo, (int64_t)r * a.pitch + c, v[i], up, min(4, a.cols - c));
   }
 }
 
@@ -426,13 +405,19 @@ int make_map_h16(CUtensorMap* map, uint64_t addr, uint64_t cols, uint64_t rows, 
 
 int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-// Geometry of one operand's pieces in the workspace.
+void launch_split_args(const SplitArgs& a, int ndev, cudaStream_t s) {
+  spx_launch(split_h16_kernel, dim3(H3_CL * ((a.cols + HB - 1) / HB), (a.rows + HB - 1) / HB, ndev), dim3(256), 0, s, a);
+}
+
+// Geometry of one operand's pieces: in the record's own workspace (offsets
+// from its start, per-device strides of their own) or, shared, in the arena.
 struct Operand {
   uint64_t src;
   int64_t ld;
   int rows, cols, rb, cb;
-  int64_t pitch, piece_dev, scl_dev;   // bytes per device of pieces / scales
-  int64_t piece_off, scl_off;          // offsets in the workspace
+  int64_t pitch;                       // halves
+  int64_t piece_off, scl_off;          // workspace offsets (bytes) or arena addresses (shared)
+  int64_t piece_dev, scl_dev;          // bytes between devices
 };
 
 void operand_geom(Operand& o, uint64_t src, int64_t ld, int rows, int cols, int ndev, int64_t& ws) {
@@ -450,6 +435,20 @@ void operand_geom(Operand& o, uint64_t src, int64_t ld, int rows, int cols, int 
   o.scl_off = ws;
   ws += o.scl_dev * ndev;
   ws = align_up(ws, 1024);
+}
+
+void split_args(SplitArgs& s, const Operand& o, int64_t src_dev, uint64_t ws) {
+  s.src = o.src;
+  s.src_dev = src_dev;
+  s.ld = o.ld;
+  s.rows = o.rows;
+  s.cols = o.cols;
+  s.dst = ws + (uint64_t)o.piece_off;
+  s.dst_dev = o.piece_dev;
+  s.pitch = o.pitch;
+  s.scl = ws + (uint64_t)o.scl_off;
+  s.scl_dev = o.scl_dev;
+  s.cb = o.cb;
 }
 
 }  // namespace
@@ -479,6 +478,17 @@ int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out) {
   else operand_geom(g->A, a, p.lda, p.M, p.K, p.ndev, ws);
   if (p.b_k_major) operand_geom(g->B, b, p.ldb, p.N, p.K, p.ndev, ws);
   else operand_geom(g->B, b, p.ldb, p.K, p.N, p.ndev, ws);
+  if (p.h3_shared) {
+    // pieces and scales live in the arena, written by SPX_K_SPLIT records
+    auto shared = [&](Operand& o, int64_t off, int64_t scl) {
+      o.piece_off = (int64_t)(p.base + (uint64_t)(off * 4));
+      o.scl_off = (int64_t)(p.base + (uint64_t)(scl * 4));
+      o.piece_dev = o.scl_dev = p.dev_stride;
+    };
+    shared(g->A, p.h3_a_off, p.h3_a_scl);
+    shared(g->B, p.h3_b_off, p.h3_b_scl);
+    ws = 0;
+  }
   g->ws_bytes = ws;
   *out = g;
   return 0;
@@ -486,29 +496,17 @@ int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out) {
 
 int64_t spx_gemm_h3_ws_bytes(const SpxGemmH3* g) { return g->ws_bytes; }
 
-static void split_args(SplitArgs& s, const Operand& o, const spx_gemm_params& p, uint64_t ws) {
-  s.src = o.src;
-  s.src_dev = p.dev_stride;
-  s.ld = o.ld;
-  s.rows = o.rows;
-  s.cols = o.cols;
-  s.dst = ws + (uint64_t)o.piece_off;
-  s.dst_dev = o.piece_dev;
-  s.pitch = o.pitch;
-  s.scl = ws + (uint64_t)o.scl_off;
-  s.scl_dev = o.scl_dev;
-  s.cb = o.cb;
-}
-
 int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   const spx_gemm_params& p = g->p;
+  if (p.h3_shared) ws = 0;            // operand addresses are absolute
+  else if (!ws) return spx_set_error("gemm h3: workspace not bound");
   g->ws = ws;
   const Operand &A = g->A, &B = g->B;
   if (make_map_h16(&g->ma, ws + A.piece_off, A.cols, A.rows, p.ndev, A.pitch, A.piece_dev, p.a_mn_major ? 64 : HB))
     return -1;
   if (make_map_h16(&g->mb, ws + B.piece_off, B.cols, B.rows, p.ndev, B.pitch, B.piece_dev, 64)) return -1;
-  split_args(g->sa, A, p, ws);
-  split_args(g->sb, B, p, ws);
+  split_args(g->sa, A, p.dev_stride, ws);
+  split_args(g->sb, B, p.dev_stride, ws);
   H3Args& a_ = g->args;
   a_.M = p.M; a_.N = p.N; a_.K = p.K;
   a_.a_mn_major = p.a_mn_major;
@@ -546,12 +544,15 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
 }
 
 int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
-  if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
   const spx_gemm_params& p = g->p;
-  spx_launch(split_h16_kernel, dim3(g->A.cb, g->A.rb, p.ndev), dim3(256), 0, s, g->sa);
-  SPX_CHECK_LAUNCH();
-  spx_launch(split_h16_kernel, dim3(g->B.cb, g->B.rb, p.ndev), dim3(256), 0, s, g->sb);
-  SPX_CHECK_LAUNCH();
+  if (!p.h3_shared) {
+    if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
+    launch_split_args(g->sa, p.ndev, s);
+    SPX_CHECK_LAUNCH();
+    launch_split_args(g->sb, p.ndev, s);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) *nlaunch += 2;
+  }
   static bool attr = false;
   if (!attr) {
     SPX_CUDA(cudaFuncSetAttribute(gemm_h3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H_TOTAL));
@@ -578,7 +579,28 @@ int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
   cfg.numAttrs = na;
   SPX_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel, g->ma, g->mb, g->mc, g->args));
   SPX_CHECK_LAUNCH();
-  if (nlaunch) *nlaunch += 3;
+  if (nlaunch) ++*nlaunch;
+  return 0;
+}
+
+int spx_launch_split(const spx_split_params& p, cudaStream_t s, int* nlaunch) {
+  if (p.rows <= 0 || p.cols <= 0 || (p.pitch & 7) || p.pitch < p.cols)
+    return spx_set_error("split: bad geometry %dx%d pitch %lld", p.rows, p.cols, (long long)p.pitch);
+  SplitArgs a;
+  a.src = p.base + (uint64_t)(p.src_off * 4);
+  a.src_dev = p.dev_stride;
+  a.ld = p.ld;
+  a.rows = p.rows;
+  a.cols = p.cols;
+  a.dst = p.base + (uint64_t)(p.dst_off * 4);
+  a.dst_dev = p.dev_stride;
+  a.pitch = p.pitch;
+  a.scl = p.base + (uint64_t)(p.scl_off * 4);
+  a.scl_dev = p.dev_stride;
+  a.cb = (p.cols + HB - 1) / HB;
+  launch_split_args(a, p.ndev, s);
+  SPX_CHECK_LAUNCH();
+  if (nlaunch) ++*nlaunch;
   return 0;
 }
 

@@ -145,6 +145,10 @@ struct Record {
   std::vector<uint8_t> params;
   SpxGemmTC* tc = nullptr;
   SpxGemmH3* h3 = nullptr;      // path 3: block-scaled 3xFP16 (gemm_h3.cu)
+  int fused_split = -1;         // EW: the next record (SPX_K_SPLIT of output `split_out`) runs inside this launch
+  int split_out = -1;
+  std::vector<uint8_t> split_params;
+  bool fused = false;           // SPLIT done by the preceding EW record
   int stream = 0;               // 0 main, 1..SPX_SIDE_STREAMS side streams
   std::vector<int> waits;       // records on other streams to wait for
   bool signal = false;          // a later record on another stream waits for this one
@@ -167,8 +171,13 @@ struct Plan {
 };
 
 static int run_record(Record& r, cudaStream_t s, int* nl) {
+  if (r.fused) return 0;
   switch (r.kind) {
     case SPX_K_EW:
+      if (r.fused_split >= 0)
+        return spx_launch_ew_static_split(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()),
+                                          *reinterpret_cast<const spx_split_params*>(r.split_params.data()),
+                                          r.split_out, s, nl);
       if (r.path > 0) return spx_launch_ew_static(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
       return spx_launch_ew(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
     case SPX_K_REDUCE: return spx_launch_reduce(*reinterpret_cast<const spx_reduce_params*>(r.params.data()), s, nl);
@@ -180,6 +189,7 @@ static int run_record(Record& r, cudaStream_t s, int* nl) {
       return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
     case SPX_K_NCCL: return run_nccl(*reinterpret_cast<const spx_nccl_params*>(r.params.data()), s);
     case SPX_K_PEER: return spx_launch_peer(*reinterpret_cast<const spx_peer_params*>(r.params.data()), s, nl);
+    case SPX_K_SPLIT: return spx_launch_split(*reinterpret_cast<const spx_split_params*>(r.params.data()), s, nl);
   }
   return spx_set_error("unknown record kind %d", r.kind);
 }
@@ -193,6 +203,7 @@ static size_t params_size(int kind) {
     case SPX_K_CREDUCE: return sizeof(spx_creduce_params);
     case SPX_K_NCCL: return sizeof(spx_nccl_params);
     case SPX_K_PEER: return sizeof(spx_peer_params);
+    case SPX_K_SPLIT: return sizeof(spx_split_params);
   }
   return 0;
 }
@@ -333,6 +344,7 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
     const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
     const bool tc_ok = spx_gemm_tc_supported(g);
     if (g.path == 1 && !tc_ok) return spx_set_error("gemm %dx%dx%d: tcgen05 path requested but operands unsupported", g.M, g.N, g.K);
+    if (g.h3_shared && g.path != 3) return spx_set_error("gemm %dx%dx%d: shared fp16 pieces need path 3", g.M, g.N, g.K);
     if (g.path == 3) {
       if (!spx_gemm_h3_supported(g))
         return spx_set_error("gemm %dx%dx%d: block-scaled fp16 path requested but unsupported", g.M, g.N, g.K);
@@ -361,6 +373,26 @@ int spx_plan_finalize(uint64_t plan) {
       if (b > h3need[r.stream]) h3need[r.stream] = b;
     }
     if (r.signal && !r.done) SPX_CUDA(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+  }
+  // elementwise record + the split of its output right after it on the same
+  // stream: one launch (ew_static.cu ew_static_split_kernel)
+  static int fuse = -1;
+  if (fuse < 0) {
+    const char* e = getenv("SPX_EW_SPLIT_FUSE");
+    fuse = e ? atoi(e) != 0 : 1;
+  }
+  for (size_t i = 0; fuse && i + 1 < P->recs.size(); ++i) {
+    Record &a = P->recs[i], &b = P->recs[i + 1];
+    if (a.kind != SPX_K_EW || a.path <= 0 || b.kind != SPX_K_SPLIT || a.stream != b.stream || !b.waits.empty() ||
+        a.fused_split >= 0)
+      continue;
+    const int j = spx_ew_split_match(*reinterpret_cast<const spx_ew_params*>(a.params.data()),
+                                     *reinterpret_cast<const spx_split_params*>(b.params.data()));
+    if (j < 0) continue;
+    a.fused_split = (int)(i + 1);
+    a.split_out = j;
+    a.split_params = b.params;
+    b.fused = true;
   }
   for (int k = 0; k <= SPX_SIDE_STREAMS; ++k)
     if (h3need[k] && !P->h3ws[k]) SPX_CUDA(cudaMalloc(&P->h3ws[k], (size_t)h3need[k]));

@@ -20,7 +20,7 @@ import ctypes as C
 import numpy as np
 
 from . import runtime as R
-from .plan import ALIGN, Compiler, Leaf, Node, Program, _align, _contig, _prod
+from .plan import ALIGN, Compiler, Kernel, Leaf, Node, Program, _align, _contig, _prod
 
 
 def _collapse(dims, views):
@@ -60,6 +60,7 @@ class Executable:
             overlap = os.environ.get("SPX_OVERLAP", "1") != "0"
         if overlap:
             self._hoist_terminal()
+        self._share_splits()
         self.stream_of = self._streams() if overlap else {}
         self.side = set(self.stream_of)
         self.overlap = bool(self.side)
@@ -317,11 +318,97 @@ class Executable:
                 self._emit_reduce(k)
             elif k.kind == "gemm":
                 self._emit_gemm(k)
+            elif k.kind == "split":
+                self._emit_split(k)
             elif k.kind == "coll":
                 if c.comm_mode == "local":
                     self._emit_coll_local(k)
                 else:
                     self._emit_coll_nccl(k)
+
+    def _h3_eligible(self, d) -> bool:
+        """The block-scaled 3xFP16 kernel takes this GEMM (runtime.cu h3_default,
+        gemm_h3.cu spx_gemm_h3_supported, gemm_tc.cu spx_gemm_tc_supported)."""
+        import os
+        if self.gemm_path != 0 or os.environ.get("SPX_GEMM_H3", "1") == "0":
+            return False
+        if d.get("splits", 1) != 1 or d.get("epi") is not None or d.get("sk_inkernel") or not d.get("tc_ok"):
+            return False
+        (_, aoff, lda, _), (_, boff, ldb, _) = d["a"], d["b"]
+        return (aoff % 4 == 0 and boff % 4 == 0 and lda % 4 == 0 and ldb % 4 == 0
+                and d["M"] >= 64 and d["N"] >= 32 and d["K"] >= 32)
+
+    def _share_splits(self):
+        """One SPX_K_SPLIT per distinct fp32 operand view of the 3xFP16 GEMMs.
+        Buffers are single-assignment, so the fp16 pieces of a tensor serve
+        every GEMM that reads the same view -- a weight in the forward GEMM and,
+        transposed, in the input-gradient GEMM; an activation in the forward
+        GEMM and in the weight-gradient GEMM (128 x 128 scale blocks are
+        symmetric, the GEMM reads either orientation).  The split kernel runs
+        just before the first GEMM that needs it."""
+        import os
+        if os.environ.get("SPX_H3_SHARE", "1") == "0":
+            return
+        c = self.comp
+        out = []
+        made = {}
+        args = set(c.arg_bufs)
+        pre = []            # splits of function arguments (weights, the batch): no producer, hoisted
+        producer = {}
+        for k in c.kernels:
+            for b in k.outs:
+                producer[b] = k
+        after: dict = {}    # elementwise producer -> splits of its outputs (fused into it by the runtime)
+        self.n_splits = 0
+        for k in c.kernels:
+            if k.kind == "gemm" and self._h3_eligible(k.data):
+                d = k.data
+                M, N, K = d["M"], d["N"], d["K"]
+                for side, (buf, off, ld, t), shape in (("a", d["a"], (K, M) if d["a"][3] else (M, K)),
+                                                       ("b", d["b"], (N, K) if d["b"][3] else (K, N))):
+                    rows, cols = shape
+                    key = (buf, off, ld, rows, cols)
+                    if key not in made:
+                        pitch = (cols + 7) // 8 * 8
+                        pieces = _align(rows * pitch)          # [2][rows][pitch] halves = rows * pitch floats
+                        scl = -(-rows // 128) * -(-cols // 128)
+                        name = f"%h3#{len(made)}"
+                        c.buffers[name] = pieces + scl
+                        c.bufdims[name] = (pieces + scl,)
+                        made[key] = name
+                        sk = Kernel("split", [name], {buf}, op_index=k.op_index,
+                                    data=dict(src=(buf, off, ld), rows=rows, cols=cols, pitch=pitch,
+                                              scl_off=pieces))
+                        pk = producer.get(buf)
+                        if buf in args and os.environ.get("SPX_SPLIT_PREFETCH", "1") != "0":
+                            pre.append(sk)
+                        elif pk is not None and pk.kind == "ew" and off == 0 and ld == cols:
+                            after.setdefault(id(pk), []).append(sk)
+                        else:
+                            out.append(sk)
+                        self.n_splits += 1
+                    k.ins = set(k.ins) | {made[key]}
+                    d["h3" + side] = made[key]
+                    d["h3" + side + "_scl"] = c.bufdims[made[key]][0] - (-(-rows // 128) * -(-cols // 128))
+            out.append(k)
+        final = list(pre)
+        for k in out:
+            final.append(k)
+            final.extend(after.get(id(k), []))
+        c.kernels = final
+
+    def _emit_split(self, k):
+        d = k.data
+        buf, off, ld = d["src"]
+        p = R.SplitParams()
+        p.base, p.dev_stride, p.ndev = self.base, self.dev_stride, self.ndev
+        p.rows, p.cols = d["rows"], d["cols"]
+        p.src_off = self.off[buf] + off
+        p.ld = ld
+        p.dst_off = self.off[k.outs[0]]
+        p.pitch = d["pitch"]
+        p.scl_off = self.off[k.outs[0]] + d["scl_off"]
+        self._records.append((R.K_SPLIT, p))
 
     # streams of a two-level schedule (runtime.cu: SPX_SIDE_STREAMS)
     MAIN, COMPUTE, COMM, UPDATE = 0, 1, 2, 3
@@ -400,10 +487,16 @@ class Executable:
                             or (prefetch and k.data["kind"] == "all_gather" and k.ins
                                 and all(b in args for b in k.ins))):
                         side[i] = self.COMM
+        # splits of function arguments run on the compute stream from the start
+        # of the step, overlapped with the forward pass (their GEMMs wait for them)
+        for i, k in enumerate(ks):
+            if k.kind == "split" and k.data["src"][0] in args:
+                side[i] = self.COMPUTE
         if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
             for i in reversed(range(len(ks))):
                 # in-kernel split-K GEMMs share one workspace: main stream only
-                if ks[i].kind == "gemm" and not ks[i].data.get("sk_inkernel") and off_critical(i, side):
+                if (ks[i].kind in ("gemm", "split") and not ks[i].data.get("sk_inkernel")
+                        and off_critical(i, side)):
                     side[i] = self.COMPUTE
         if os.environ.get("SPX_UPDATE_STREAM", "1") != "0" and side:
             for i, k in enumerate(ks):
@@ -563,6 +656,13 @@ class Executable:
                 p.epi_out_ld[j] = d["N"]
             p.epi_imm[0], p.epi_imm[1] = epi["imm"]
             p.c_off = self.off[epi["outs"][0]]
+        if "h3a" in d:
+            p.path = 3
+            p.h3_shared = 1
+            p.h3_a_off = self.off[d["h3a"]]
+            p.h3_b_off = self.off[d["h3b"]]
+            p.h3_a_scl = p.h3_a_off + d["h3a_scl"]
+            p.h3_b_scl = p.h3_b_off + d["h3b_scl"]
         # with collectives overlapped on a side stream, leave SMs for NCCL's CTAs
         p.reserve_sms = self.reserve_sms
         self._records.append((R.K_GEMM, p))

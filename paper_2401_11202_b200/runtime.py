@@ -64,7 +64,16 @@ class GemmParams(C.Structure):
                 ("epi_out_off", C.c_int64 * 2), ("epi_out_ld", C.c_int64 * 2),
                 ("epi_imm", C.c_float * 2),
                 ("sk_mode", C.c_int32), ("sk_pad", C.c_int32),
-                ("ws_off", C.c_int64), ("flag_off", C.c_int64)]
+                ("ws_off", C.c_int64), ("flag_off", C.c_int64),
+                ("h3_shared", C.c_int32), ("h3_pad", C.c_int32),
+                ("h3_a_off", C.c_int64), ("h3_a_scl", C.c_int64), ("h3_b_off", C.c_int64), ("h3_b_scl", C.c_int64)]
+
+
+class SplitParams(C.Structure):
+    _fields_ = [("base", C.c_uint64), ("dev_stride", C.c_int64),
+                ("ndev", C.c_int32), ("rows", C.c_int32), ("cols", C.c_int32), ("pad", C.c_int32),
+                ("src_off", C.c_int64), ("ld", C.c_int64),
+                ("dst_off", C.c_int64), ("pitch", C.c_int64), ("scl_off", C.c_int64)]
 
 
 EPI_NONE, EPI_ADD, EPI_SQUARE, EPI_MULSCALE, EPI_MOMENTUM = 0, 1, 2, 3, 4
@@ -97,11 +106,12 @@ class PeerParams(C.Structure):
 
 
 K_PEER = 7
+K_SPLIT = 8
 PEER_MAX_BLOCKS = 512      # include/spindle_b200.h
 PEER_PHASES = 3
 
 PARAMS = {K_PEER: PeerParams, K_EW: EwParams, K_REDUCE: ReduceParams, K_GEMM: GemmParams,
-          K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams}
+          K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams, K_SPLIT: SplitParams}
 
 EXPORTS = [
     "spx_last_error", "spx_version", "spx_params_size", "spx_device_init", "spx_malloc", "spx_free",

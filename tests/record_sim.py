@@ -101,7 +101,59 @@ class Sim:
             s = self.dev_base(p) + r.out_off
             self.arena[s:s + red.size] = red
 
+    # --- block-scaled 3xFP16 operands (gemm_h3.cu): pieces in the arena as fp16
+    def run_split(self, q: R.SplitParams):
+        h16 = self.arena.view(np.float16)
+        for p in range(q.ndev):
+            X = self.gather_view(p, q.src_off, (q.ld, 1), (q.rows, q.cols)).astype(np.float32)
+            hi = np.zeros((q.rows, q.pitch), np.float16)
+            lo = np.zeros((q.rows, q.pitch), np.float16)
+            rb, cb = -(-q.rows // 128), -(-q.cols // 128)
+            inv = np.zeros((rb, cb), np.float32)
+            for i in range(rb):
+                for j in range(cb):
+                    blk = X[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128]
+                    m = np.float32(np.max(np.abs(blk)))
+                    E = int((m.view(np.uint32) >> 23) & 0xFF)
+                    e = 0 if (m == 0 or E == 255) else 141 - E
+                    e = min(60, max(-60, e))
+                    y = blk * np.float32(2.0 ** e)
+                    h = y.astype(np.float16)
+                    hi[i * 128:(i + 1) * 128, j * 128:j * 128 + blk.shape[1]] = h
+                    lo[i * 128:(i + 1) * 128, j * 128:j * 128 + blk.shape[1]] = (y - h.astype(np.float32)).astype(np.float16)
+                    inv[i, j] = np.float32(2.0 ** -e)
+            d = 2 * (self.dev_base(p) + q.dst_off)
+            n = q.rows * q.pitch
+            h16[d:d + n] = hi.reshape(-1)
+            h16[d + n:d + 2 * n] = lo.reshape(-1)
+            s0 = self.dev_base(p) + q.scl_off
+            self.arena[s0:s0 + inv.size] = inv.reshape(-1)
+
+    def _h3_operand(self, p, off, scl, rows, cols):
+        """fp32 view an h3 GEMM reads: (hi + lo) / s per block, from the arena."""
+        h16 = self.arena.view(np.float16)
+        pitch = (cols + 7) // 8 * 8
+        d = 2 * (self.dev_base(p) + off)
+        n = rows * pitch
+        hi = h16[d:d + n].reshape(rows, pitch)[:, :cols].astype(np.float64)
+        lo = h16[d + n:d + 2 * n].reshape(rows, pitch)[:, :cols].astype(np.float64)
+        rb, cb = -(-rows // 128), -(-cols // 128)
+        s0 = self.dev_base(p) + scl
+        inv = self.arena[s0:s0 + rb * cb].reshape(rb, cb).astype(np.float64)
+        f = np.repeat(np.repeat(inv, 128, axis=0), 128, axis=1)[:rows, :cols]
+        return (hi + lo) * f
+
     def run_gemm(self, g: R.GemmParams):
+        if g.h3_shared:
+            for p in range(g.ndev):
+                A = self._h3_operand(p, g.h3_a_off, g.h3_a_scl, *((g.K, g.M) if g.a_mn_major else (g.M, g.K)))
+                B = self._h3_operand(p, g.h3_b_off, g.h3_b_scl, *((g.N, g.K) if g.b_k_major else (g.K, g.N)))
+                C = (A.T if g.a_mn_major else A) @ (B.T if g.b_k_major else B)
+                C = C.astype(np.float32)
+                for m in range(g.M):
+                    s = self.dev_base(p) + g.c_off + m * g.ldc
+                    self.arena[s:s + g.N] = C[m]
+            return
         for p in range(g.ndev):
             if g.a_mn_major:
                 A = self.gather_view(p, g.a_off, (1, g.lda), (g.M, g.K))
@@ -192,7 +244,7 @@ class Sim:
     def run(self):
         for kind, p in self.ex.records():
             {R.K_EW: self.run_ew, R.K_REDUCE: self.run_reduce, R.K_GEMM: self.run_gemm,
-             R.K_GATHER: self.run_gather, R.K_CREDUCE: self.run_creduce}[kind](p)
+             R.K_GATHER: self.run_gather, R.K_CREDUCE: self.run_creduce, R.K_SPLIT: self.run_split}[kind](p)
 
     def upload(self, per_device):
         for p in range(self.ex.ndev):
@@ -303,7 +355,7 @@ def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
             for s, e in zip(sims, exs):
                 k, p = e.records()[i]
                 {R.K_EW: s.run_ew, R.K_REDUCE: s.run_reduce, R.K_GEMM: s.run_gemm,
-                 R.K_GATHER: s.run_gather, R.K_CREDUCE: s.run_creduce}[k](p)
+                 R.K_GATHER: s.run_gather, R.K_CREDUCE: s.run_creduce, R.K_SPLIT: s.run_split}[k](p)
             continue
         p0 = exs[0].records()[i][1]
         key, groups = plan[p0.comm]
