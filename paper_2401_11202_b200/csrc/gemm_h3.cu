@@ -44,18 +44,8 @@ namespace {
 
 constexpr int HB = 128;                  // scale block edge = A rows per CTA = K per chunk
 constexpr int HBK = 64;                  // fp16 per 128-byte swizzle row = K per k-block
-constexpr int HBN = 128;                 // output columns per pair tile
 constexpr int H_CG = 2;
-constexpr int H_BNH = HBN / H_CG;        // B columns per CTA
-constexpr int H_THREADS = 256;
 constexpr int H_A_BYTES = HB * HBK * 2;      // 16 KB per piece
-constexpr int H_B_BYTES = H_BNH * HBK * 2;   // 8 KB per piece
-constexpr int H_STAGE = 2 * H_A_BYTES + 2 * H_B_BYTES;   // 48 KB
-constexpr int H_RS = 4;
-constexpr int H_BAR_OFF = H_RS * H_STAGE;
-constexpr int H_STG_OFF = H_BAR_OFF + 1024;
-constexpr int H_STG_WARP = 8192;
-constexpr int H_TOTAL = H_STG_OFF + 4 * H_STG_WARP + 1024;
 
 struct SplitArgs {
   uint64_t src;          // device-0 address of element (0, 0) of the fp32 view
@@ -164,14 +154,40 @@ SPX_DEV void mma_f16_ss(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t ides
 #undef SPX_MMA16
 }
 
-__global__ void __launch_bounds__(H_THREADS, 1)
+// Tile configuration: BN output columns per CTA pair (each CTA holds BN/2 B
+// columns and drains a 128 x BN accumulator with BN/128 drain warpgroups).
+//   BN = 128: 48 KB stages x 4; 256 threads (WG0 TMA/MMA, WG1 drain)
+//   BN = 256: 64 KB stages x 3; 384 threads (WG0, WG1-2 drain column halves),
+//             the largest MMA (256 x 256 x 16): per SM the tensor core then
+//             reads 52 B/cycle of operands from shared memory instead of 73
+//             (+ 42 instead of 64 B/cycle of TMA writes) -- BN = 128 sits just
+//             above the shared-memory port once TMA traffic is counted.
+template <int BN>
+struct H3Cfg {
+  static constexpr int BNH = BN / H_CG;
+  static constexpr int B_BYTES = BNH * HBK * 2;
+  static constexpr int STAGE = 2 * H_A_BYTES + 2 * B_BYTES;
+  static constexpr int RS = BN == 128 ? 4 : 3;
+  static constexpr int NDG = BN / 128;                      // drain warpgroups
+  static constexpr int THREADS = 128 * (1 + NDG);
+  static constexpr int BAR_OFF = RS * STAGE;
+  static constexpr int STG_OFF = BAR_OFF + 1024;
+  static constexpr int STG_WARP = BN == 128 ? 8192 : 4096;  // 2 or 1 staging slices per drain warp
+  static constexpr int TOTAL = STG_OFF + 4 * NDG * STG_WARP + 1024;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(H3Cfg<BN>::THREADS, 1)
 gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ H3Args args) {
+  using S = H3Cfg<BN>;
+  constexpr int RS = S::RS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + H_BAR_OFF);
-  uint64_t* raw_empty = raw_full + H_RS;
-  uint64_t* tfull = raw_empty + H_RS;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* tfull = raw_empty + RS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -180,24 +196,25 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   uint32_t crank = 0;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   const int pair0 = blockIdx.x / H_CG, npairs = gridDim.x / H_CG;
-  auto a_hi = [&](int s) { return smem + s * H_STAGE; };
-  auto b_hi = [&](int s) { return smem + s * H_STAGE + 2 * H_A_BYTES; };
+  auto a_hi = [&](int s) { return smem + s * S::STAGE; };
+  auto b_hi = [&](int s) { return smem + s * S::STAGE + 2 * H_A_BYTES; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < H_RS; ++s) {
+    for (int s = 0; s < RS; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4 * H_CG);
+      mbar_init(&tempty[b], 4 * S::NDG * H_CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(S::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -212,117 +229,127 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     const int r = t - dev * per_dev;
     const int n_blk = r / args.tiles_m;        // M fastest: concurrent pairs share B panels
     m0 = (r - n_blk * args.tiles_m) * (HB * H_CG);
-    n0 = n_blk * HBN;
+    n0 = n_blk * BN;
   };
 
-  if (warp == 0) {
-    // ---------------- TMA producer (both CTAs; loads land on the leader's barrier) ----------------
-    uint32_t lead_full0;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full0) : "r"(smem_u32(&raw_full[0])));
-    int g = 0;
-    for (int t = pair0; t < args.tiles; t += npairs) {
-      int m0, n0, dev;
-      tile_of(t, m0, n0, dev);
-      m0 += (int)crank * HB;
-      const int nb0 = n0 + (int)crank * H_BNH;
-      for (int kb = 0; kb < nk; ++kb, ++g) {
-        const int s = g % H_RS;
-        mbar_wait(&raw_empty[s], ((g / H_RS) & 1) ^ 1);
-        if (elect_one()) {
-          if (crank == 0) mbar_expect_tx(&raw_full[s], (uint32_t)(H_CG * H_STAGE));
-          const uint32_t bar = lead_full0 + (uint32_t)(s * 8);
-          const int k0 = kb * HBK;
-          uint8_t* st = a_hi(s);
+  if (warp < 4) {
+    if (BN > 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == 0) {
+      // ---------------- TMA producer (both CTAs; loads land on the leader's barrier) ----------------
+      uint32_t lead_full0;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full0) : "r"(smem_u32(&raw_full[0])));
+      int g = 0;
+      for (int t = pair0; t < args.tiles; t += npairs) {
+        int m0, n0, dev;
+        tile_of(t, m0, n0, dev);
+        m0 += (int)crank * HB;
+        const int nb0 = n0 + (int)crank * S::BNH;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % RS;
+          mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
+          if (elect_one()) {
+            if (crank == 0) mbar_expect_tx(&raw_full[s], (uint32_t)(H_CG * S::STAGE));
+            const uint32_t bar = lead_full0 + (uint32_t)(s * 8);
+            const int k0 = kb * HBK;
+            uint8_t* st = a_hi(s);
 #pragma unroll
-          for (int piece = 0; piece < 2; ++piece) {
-            uint8_t* da = st + piece * H_A_BYTES;
-            if (args.a_mn_major) {
-              tma_load_4d<true>(da, &tma_a, bar, m0, k0, piece, dev);
-              tma_load_4d<true>(da + H_A_BYTES / 2, &tma_a, bar, m0 + 64, k0, piece, dev);
-            } else {
-              tma_load_4d<true>(da, &tma_a, bar, k0, m0, piece, dev);
+            for (int piece = 0; piece < 2; ++piece) {
+              uint8_t* da = st + piece * H_A_BYTES;
+              if (args.a_mn_major) {
+                tma_load_4d<true>(da, &tma_a, bar, m0, k0, piece, dev);
+                tma_load_4d<true>(da + H_A_BYTES / 2, &tma_a, bar, m0 + 64, k0, piece, dev);
+              } else {
+                tma_load_4d<true>(da, &tma_a, bar, k0, m0, piece, dev);
+              }
+              uint8_t* db = b_hi(s) + piece * S::B_BYTES;
+              if (args.b_k_major) {
+                tma_load_4d<true>(db, &tma_b, bar, k0, nb0, piece, dev);
+              } else {
+#pragma unroll
+                for (int c = 0; c < S::BNH / 64; ++c)
+                  tma_load_4d<true>(db + c * 8192, &tma_b, bar, nb0 + 64 * c, k0, piece, dev);
+              }
             }
-            uint8_t* db = b_hi(s) + piece * H_B_BYTES;
-            if (args.b_k_major) tma_load_4d<true>(db, &tma_b, bar, k0, nb0, piece, dev);
-            else tma_load_4d<true>(db, &tma_b, bar, nb0, k0, piece, dev);
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
-    }
-  } else if (warp == 1 && crank == 0) {
-    // ---------------- MMA issuer (leader CTA) ----------------
-    // kind::f16 idesc: D f32 (bit 4), A/B fp16 (0), K- or MN-major per operand
-    const uint32_t idesc = (1u << 4) | ((uint32_t)(args.a_mn_major ? 1 : 0) << 15) |
-                           ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(HBN >> 3) << 17) |
-                           ((uint32_t)((HB * H_CG) >> 4) << 24);
-    // SWIZZLE_128B descriptors: K-major rows of 128 B, 8-row groups 1 KB apart,
-    // one k-step (16 fp16) = 32 B along the row; MN-major: 64-element MN
-    // chunks (one TMA box, 8 KB) apart by LBO, 8-k groups by SBO, one k-step =
-    // 16 rows of 128 B.
-    const uint32_t a_lbo = args.a_mn_major ? (uint32_t)(H_A_BYTES / 2) : 16u;
-    const uint32_t a_step = args.a_mn_major ? 2048u : 32u;
-    const uint32_t b_lbo = args.b_k_major ? 16u : (uint32_t)H_B_BYTES;
-    const uint32_t b_step = args.b_k_major ? 32u : 2048u;
-    const uint64_t da0 = smem_desc(smem_u32(a_hi(0)), a_lbo, 1024u, 2u);
-    const uint64_t db0 = smem_desc(smem_u32(b_hi(0)), b_lbo, 1024u, 2u);
-    const uint64_t dak = a_step >> 4, dbk = b_step >> 4;
-    const uint64_t alo = H_A_BYTES >> 4, blo = H_B_BYTES >> 4;
-    int rs = 0;
-    uint32_t rph = 0;
-    int cg = 0;
-    for (int t = pair0; t < args.tiles; t += npairs) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int kin = kb & 1;
-        const int buf = cg & 1;
-        const bool chunk_last = kin == 1 || kb == nk - 1;
-        if (kin == 0) mbar_wait<true>(&tempty[buf], ((cg >> 1) & 1) ^ 1);
-        mbar_wait<true>(&raw_full[rs], rph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = da0 + (uint64_t)(rs * (H_STAGE >> 4));
-        const uint64_t db = db0 + (uint64_t)(rs * (H_STAGE >> 4));
-        const uint32_t dacc = tmem_d + (uint32_t)(buf * HBN);
-        if (elect_one()) {
+    } else if (warp == 1 && crank == 0) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      // kind::f16 idesc: D f32 (bit 4), A/B fp16 (0), K- or MN-major per operand
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(args.a_mn_major ? 1 : 0) << 15) |
+                             ((uint32_t)(args.b_k_major ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)((HB * H_CG) >> 4) << 24);
+      // SWIZZLE_128B descriptors: K-major rows of 128 B, 8-row groups 1 KB apart,
+      // one k-step (16 fp16) = 32 B along the row; MN-major: 64-element MN
+      // chunks (one TMA box, 8 KB) apart by LBO, 8-k groups by SBO, one k-step =
+      // 16 rows of 128 B.
+      const uint32_t a_lbo = args.a_mn_major ? 8192u : 16u;
+      const uint32_t a_step = args.a_mn_major ? 2048u : 32u;
+      const uint32_t b_lbo = args.b_k_major ? 16u : 8192u;
+      const uint32_t b_step = args.b_k_major ? 32u : 2048u;
+      const uint64_t da0 = smem_desc(smem_u32(a_hi(0)), a_lbo, 1024u, 2u);
+      const uint64_t db0 = smem_desc(smem_u32(b_hi(0)), b_lbo, 1024u, 2u);
+      const uint64_t dak = a_step >> 4, dbk = b_step >> 4;
+      const uint64_t alo = H_A_BYTES >> 4, blo = S::B_BYTES >> 4;
+      int rs = 0;
+      uint32_t rph = 0;
+      int cg = 0;
+      for (int t = pair0; t < args.tiles; t += npairs) {
+        for (int kb = 0; kb < nk; ++kb) {
+          const int kin = kb & 1;
+          const int buf = cg & 1;
+          const bool chunk_last = kin == 1 || kb == nk - 1;
+          if (kin == 0) mbar_wait<true>(&tempty[buf], ((cg >> 1) & 1) ^ 1);
+          mbar_wait<true>(&raw_full[rs], rph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = da0 + (uint64_t)(rs * (S::STAGE >> 4));
+          const uint64_t db = db0 + (uint64_t)(rs * (S::STAGE >> 4));
+          const uint32_t dacc = tmem_d + (uint32_t)(buf * BN);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < HBK / 16; ++kk) {
-            const uint64_t ah = da + kk * dak, bh = db + kk * dbk;
-            mma_f16_ss<1>(dacc, ah, bh + blo, idesc, (kin | kk) ? 1u : 0u);   // hi.lo
-            mma_f16_ss<2>(dacc, ah, bh, idesc, 1u);                           // hi.hi
-            mma_f16_ss<0>(dacc, ah + alo, bh, idesc, 1u);                     // lo.hi
+            for (int kk = 0; kk < HBK / 16; ++kk) {
+              const uint64_t ah = da + kk * dak, bh = db + kk * dbk;
+              mma_f16_ss<1>(dacc, ah, bh + blo, idesc, (kin | kk) ? 1u : 0u);   // hi.lo
+              mma_f16_ss<2>(dacc, ah, bh, idesc, 1u);                           // hi.hi
+              mma_f16_ss<0>(dacc, ah + alo, bh, idesc, 1u);                     // lo.hi
+            }
+            mma_commit<2>(&raw_empty[rs]);
+            if (chunk_last) mma_commit<2>(&tfull[buf]);
           }
-          mma_commit<2>(&raw_empty[rs]);
-          if (chunk_last) mma_commit<2>(&tfull[buf]);
+          __syncwarp();
+          if (++rs == RS) { rs = 0; rph ^= 1u; }
+          if (chunk_last) ++cg;
         }
-        __syncwarp();
-        if (++rs == H_RS) { rs = 0; rph ^= 1u; }
-        if (chunk_last) ++cg;
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ---------------- drain: scaled fp32 promotion of every k chunk, C stores ----------------
+    if (BN > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     const int q = warp & 3;
+    const int dg = (warp - 4) >> 2;            // column group: columns [128 dg, 128 dg + 128)
     const int nchunks = (nk + 1) / 2;
     int cg = 0;
     for (int t = pair0; t < args.tiles; t += npairs) {
       int m0, n0, dev;
       tile_of(t, m0, n0, dev);
       m0 += (int)crank * HB;
-      const int mblk = m0 / HB, nblk = n0 / HB;
+      const int mblk = m0 / HB, nblk = (n0 + dg * 128) / HB;
       const float* sa = reinterpret_cast<const float*>(args.sa + (uint64_t)((int64_t)dev * args.sa_dev)) + mblk * args.sa_m;
       const float* sb = reinterpret_cast<const float*>(args.sb + (uint64_t)((int64_t)dev * args.sb_dev)) + nblk * args.sb_n;
-      const bool rows_exist = mblk < args.rb_a;
-      float acc[HBN];
+      const bool live = mblk < args.rb_a && n0 + dg * 128 < args.N;
+      float acc[128];
 #pragma unroll
-      for (int j = 0; j < HBN; ++j) acc[j] = 0.f;
+      for (int j = 0; j < 128; ++j) acc[j] = 0.f;
       for (int c = 0; c < nchunks; ++c, ++cg) {
         const int buf = cg & 1;
-        const float f = rows_exist ? __fmul_rn(sa[c * args.sa_k], sb[c * args.sb_k]) : 0.f;
+        const float f = live ? __fmul_rn(sa[c * args.sa_k], sb[c * args.sb_k]) : 0.f;
         mbar_wait(&tfull[buf], (cg >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int cc = 0; cc < HBN / 32; ++cc) {
+        for (int cc = 0; cc < 4; ++cc) {
           uint32_t v[32];
-          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * HBN + cc * 32), v);
+          tmem_ld32(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + dg * 128 + cc * 32), v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __fmaf_rn(__uint_as_float(v[j]), f, acc[cc * 32 + j]);
@@ -336,16 +363,21 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         }
       }
       const int row0 = m0 + q * 32;
-      if (row0 >= args.M) continue;
+      const int col0 = n0 + dg * 128;
+      if (row0 >= args.M || col0 >= args.N) continue;
       if (args.tma_store) {
         // each 32 x 32 slice through a 128B-swizzled staging tile, one bulk tensor store
-        uint8_t* stg = smem + H_STG_OFF + q * H_STG_WARP;
+        uint8_t* stg = smem + S::STG_OFF + (warp - 4) * S::STG_WARP;
+        constexpr int NSTG = S::STG_WARP / 4096;
 #pragma unroll
-        for (int cc = 0; cc < HBN / 32; ++cc) {
-          if (n0 + cc * 32 >= args.N) break;
-          uint8_t* tt = stg + (cc & 1) * 4096;
-          if (cc >= 2) {
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        for (int cc = 0; cc < 4; ++cc) {
+          if (col0 + cc * 32 >= args.N) break;
+          uint8_t* tt = stg + (cc % NSTG) * 4096;
+          if (cc >= NSTG) {
+            if (lane == 0) {
+              if (NSTG == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
             __syncwarp();
           }
 #pragma unroll
@@ -359,7 +391,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                     reinterpret_cast<uint64_t>(&tma_c)),
-                "r"(n0 + cc * 32), "r"(row0), "r"(dev), "r"(smem_u32(tt))
+                "r"(col0 + cc * 32), "r"(row0), "r"(dev), "r"(smem_u32(tt))
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -372,18 +404,18 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
           float* crow = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride)) +
                         (int64_t)row * args.ldc;
 #pragma unroll
-          for (int j = 0; j < HBN; ++j)
-            if (n0 + j < args.N) crow[n0 + j] = acc[j];
+          for (int j = 0; j < 128; ++j)
+            if (col0 + j < args.N) crow[col0 + j] = acc[j];
         }
       }
     }
+    if (args.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
-  if (warp >= 4 && args.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem_d));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(S::TMEM_COLS));
   }
 }
 
@@ -462,6 +494,7 @@ struct SpxGemmH3 {
   H3Args args;
   SplitArgs sa, sb;
   dim3 grid;
+  int bn = 128;         // output columns per CTA pair (H3Cfg)
 };
 
 bool spx_gemm_h3_supported(const spx_gemm_params& p) {
@@ -504,7 +537,23 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   const Operand &A = g->A, &B = g->B;
   if (make_map_h16(&g->ma, ws + A.piece_off, A.cols, A.rows, p.ndev, A.pitch, A.piece_dev, p.a_mn_major ? 64 : HB))
     return -1;
-  if (make_map_h16(&g->mb, ws + B.piece_off, B.cols, B.rows, p.ndev, B.pitch, B.piece_dev, 64)) return -1;
+  // tile width: BN = 256 (the largest MMA, least shared-memory traffic per
+  // FLOP) unless its coarser tiles leave more of the last wave idle --
+  // compared in waves of CTA pairs, a BN = 256 tile costing ~0.95 of two
+  // BN = 128 tiles
+  {
+    int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
+    const int pairs = sms / H_CG > 0 ? sms / H_CG : 1;
+    const int64_t tm = (p.M + HB * H_CG - 1) / (HB * H_CG);
+    const int64_t t128 = tm * ((p.N + 127) / 128) * p.ndev, t256 = tm * ((p.N + 255) / 256) * p.ndev;
+    const double w128 = (double)((t128 + pairs - 1) / pairs), w256 = (double)((t256 + pairs - 1) / pairs);
+    g->bn = (p.N > 128 && w256 * 2 * 0.95 < w128) ? 256 : 128;
+    const char* e = getenv("SPX_H3_BN");
+    if (e) g->bn = atoi(e) == 256 ? 256 : 128;
+  }
+  if (make_map_h16(&g->mb, ws + B.piece_off, B.cols, B.rows, p.ndev, B.pitch, B.piece_dev,
+                   p.b_k_major ? g->bn / H_CG : 64))
+    return -1;
   split_args(g->sa, A, p.dev_stride, ws);
   split_args(g->sb, B, p.dev_stride, ws);
   H3Args& a_ = g->args;
@@ -512,7 +561,7 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   a_.a_mn_major = p.a_mn_major;
   a_.b_k_major = p.b_k_major;
   a_.tiles_m = (p.M + HB * H_CG - 1) / (HB * H_CG);
-  a_.tiles_n = (p.N + HBN - 1) / HBN;
+  a_.tiles_n = (p.N + g->bn - 1) / g->bn;
   a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
   a_.c_base = p.base + (uint64_t)(p.c_off * 4);
   a_.dev_stride = p.dev_stride;
@@ -543,25 +592,19 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   return 0;
 }
 
-int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
-  const spx_gemm_params& p = g->p;
-  if (!p.h3_shared) {
-    if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
-    launch_split_args(g->sa, p.ndev, s);
-    SPX_CHECK_LAUNCH();
-    launch_split_args(g->sb, p.ndev, s);
-    SPX_CHECK_LAUNCH();
-    if (nlaunch) *nlaunch += 2;
-  }
+template <int BN>
+static cudaError_t launch_h3(const SpxGemmH3* g, cudaStream_t s) {
+  using S = H3Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    SPX_CUDA(cudaFuncSetAttribute(gemm_h3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H_TOTAL));
+    cudaError_t e = cudaFuncSetAttribute(gemm_h3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g->grid;
-  cfg.blockDim = dim3(H_THREADS);
-  cfg.dynamicSmemBytes = H_TOTAL;
+  cfg.blockDim = dim3(S::THREADS);
+  cfg.dynamicSmemBytes = S::TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int na = 0;
@@ -577,7 +620,22 @@ int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  SPX_CUDA(cudaLaunchKernelEx(&cfg, gemm_h3_kernel, g->ma, g->mb, g->mc, g->args));
+  return cudaLaunchKernelEx(&cfg, gemm_h3_kernel<BN>, g->ma, g->mb, g->mc, g->args);
+}
+
+int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
+  const spx_gemm_params& p = g->p;
+  if (!p.h3_shared) {
+    if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
+    launch_split_args(g->sa, p.ndev, s);
+    SPX_CHECK_LAUNCH();
+    launch_split_args(g->sb, p.ndev, s);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) *nlaunch += 2;
+  }
+  if (g->bn == 256) SPX_CUDA(launch_h3<256>(g, s));
+  else SPX_CUDA(launch_h3<128>(g, s));
+
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;

@@ -112,8 +112,11 @@ def test_gemm_tcgen05_3xtf32(shape, at, bt):
 @pytest.mark.parametrize("at,bt", [(False, False), (True, False), (False, True), (True, True)])
 @pytest.mark.parametrize("shape", [s for s in GEMM_SHAPES if s != (130, 70, 200)] + [(256, 72, 136), (320, 200, 96)],
                          ids=lambda s: "x".join(map(str, s)))
-def test_gemm_h3_block_scaled(shape, at, bt):
-    """Block-scaled 3xFP16 GEMM (gemm_h3.cu) vs float64: <= 1e-5 max-normalised."""
+@pytest.mark.parametrize("bn", ["128", "256"])
+def test_gemm_h3_block_scaled(shape, at, bt, bn, monkeypatch):
+    """Block-scaled 3xFP16 GEMM (gemm_h3.cu) vs float64: <= 1e-5 max-normalised,
+    both tile widths (BN = 128 / 256 output columns per CTA pair)."""
+    monkeypatch.setenv("SPX_H3_BN", bn)
     pkg = _pkg()
     M, K, N = shape
     rng = np.random.default_rng(hash(shape) % 1000 + 7)
@@ -129,9 +132,11 @@ def test_gemm_h3_block_scaled(shape, at, bt):
 
 
 @pytest.mark.parametrize("at,bt", [(False, False), (True, True)])
-def test_gemm_h3_dynamic_range(at, bt):
+@pytest.mark.parametrize("bn", ["128", "256"])
+def test_gemm_h3_dynamic_range(at, bt, bn, monkeypatch):
     """Per-block scales: 128 x 128 blocks spanning 2^-40 .. 2^40, zero blocks,
     tiny and huge rows -- still <= 1e-5 against float64, per output block too."""
+    monkeypatch.setenv("SPX_H3_BN", bn)
     pkg = _pkg()
     M, K, N = 512, 768, 384
     rng = np.random.default_rng(11)

@@ -16,7 +16,9 @@ SHAPES = [(2048, 4096, 1024, False, False), (2048, 1024, 4096, False, True),
 if os.environ.get("SHAPES"):
     SHAPES = [SHAPES[int(i)] for i in os.environ["SHAPES"].split(",")]
 PATHS = [int(x) for x in os.environ.get("GPATHS", "1,3").split(",")]
-for (M, N, K, at, bt), path in [(s, p) for s in SHAPES for p in PATHS]:
+BNS = os.environ.get("BNS", "").split(",") if os.environ.get("BNS") else [None]
+for (M, N, K, at, bt), path, bn in [(s, p, b) for s in SHAPES for p in PATHS for b in BNS]:
+    if bn: os.environ["SPX_H3_BN"] = bn
     A = rng.standard_normal((K, M) if at else (M, K)).astype(np.float32)
     B = rng.standard_normal((N, K) if bt else (K, N)).astype(np.float32)
     g = G(dev, A, B, at, bt, path=path)
@@ -26,5 +28,5 @@ for (M, N, K, at, bt), path in [(s, p) for s in SHAPES for p in PATHS]:
     err = rel(C, AA.astype(np.float64) @ BB)
     ms = g.time_ms(10)
     g.close()
-    print(f"path {path} {M}x{N}x{K} a_mn={int(at)} b_k={int(bt)} {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:6.1f} TF fp32-eq "
+    print(f"path {path} bn {bn} {M}x{N}x{K} a_mn={int(at)} b_k={int(bt)} {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:6.1f} TF fp32-eq "
           f" rel err {err:.2e}", flush=True)
