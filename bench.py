@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--program", default=None, help="override the config's program for this GPU count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-out", default=None, help="write per-record timings (json)")
@@ -179,7 +180,7 @@ def main():
     if world != n and not (world == 1 and n == 1):
         raise SystemExit(f"--gpus {n} needs torchrun with {n} processes (WORLD_SIZE={world})")
     wl = WORKLOADS[args.config]
-    prog = load_program(wl["programs"][n])
+    prog = load_program(args.program or wl["programs"][n])
     batch = prog.batch
     base = prog.dense
     mesh = prog.meta.get("mesh") or "dense (1 device)"

@@ -146,7 +146,8 @@ typedef struct {
    * the arena (offsets in elements from the device base; one split serves
    * every GEMM that reads the same tensor view); without it the record splits
    * its operands itself into a per-stream workspace. */
-  int32_t h3_shared, h3_pad;
+  int32_t h3_shared;
+  int32_t h3_splitk;              /* path 3 split-K of few-tile GEMMs: <= 1 off (default), n = at most n splits */
   int64_t h3_a_off, h3_a_scl, h3_b_off, h3_b_scl;
 } spx_gemm_params;
 

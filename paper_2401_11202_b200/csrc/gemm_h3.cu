@@ -123,6 +123,16 @@ struct H3Args {
   int64_t sa_dev, sb_dev;              // bytes
   int64_t sa_m, sa_k, sb_n, sb_k;      // element strides of the scale grids
   int rb_a;                            // A row blocks (guards the last pair's second CTA)
+  // split-K (splits > 1): unit u = tile u / splits, k chunks [nc s / S, nc (s+1) / S);
+  // every unit stores its partial 32-row slices to the workspace [S][M][N] and
+  // counts them into a per-slice flag; the LAST unit of a slice to arrive folds
+  // all S partials in split order (deterministic) and stores C.  No unit waits
+  // for another, so units need not be co-resident.
+  int splits, units;
+  uint64_t flag_base;                  // uint32 [tiles][2 CTAs][BN/128][4 warps] per device, zero between launches
+  int64_t flag_dev;                    // bytes
+  uint64_t ws_base;                    // device-0 address of the partials
+  int64_t ws_dev;                      // bytes
 };
 
 template <bool LEADER_BAR>
@@ -180,7 +190,8 @@ struct H3Cfg {
 template <int BN>
 __global__ void __launch_bounds__(H3Cfg<BN>::THREADS, 1)
 gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-               const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ H3Args args) {
+               const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_w,
+               const __grid_constant__ H3Args args) {
   using S = H3Cfg<BN>;
   constexpr int RS = S::RS;
   extern __shared__ uint8_t smem_raw[];
@@ -223,6 +234,14 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   const uint32_t tmem_d = *tmem_slot;
   SPX_PDL_ENTRY();
 
+  const int nch = (nk + 1) / 2;               // 128-wide k chunks
+  // unit -> (tile, split, first chunk, chunk count)
+  auto unit_of = [&](int u, int& t, int& sp, int& c0, int& ncu) {
+    t = u / args.splits;
+    sp = u - t * args.splits;
+    c0 = (int)(((long long)nch * sp) / args.splits);
+    ncu = (int)(((long long)nch * (sp + 1)) / args.splits) - c0;
+  };
   auto tile_of = [&](int t, int& m0, int& n0, int& dev) {
     const int per_dev = args.tiles_m * args.tiles_n;
     dev = t / per_dev;
@@ -239,12 +258,14 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       uint32_t lead_full0;
       asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full0) : "r"(smem_u32(&raw_full[0])));
       int g = 0;
-      for (int t = pair0; t < args.tiles; t += npairs) {
-        int m0, n0, dev;
+      for (int u = pair0; u < args.units; u += npairs) {
+        int t, sp, c0, ncu, m0, n0, dev;
+        unit_of(u, t, sp, c0, ncu);
         tile_of(t, m0, n0, dev);
         m0 += (int)crank * HB;
         const int nb0 = n0 + (int)crank * S::BNH;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int kbe = min(nk, 2 * (c0 + ncu));
+        for (int kb = 2 * c0; kb < kbe; ++kb, ++g) {
           const int s = g % RS;
           mbar_wait(&raw_empty[s], ((g / RS) & 1) ^ 1);
           if (elect_one()) {
@@ -295,11 +316,14 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       int rs = 0;
       uint32_t rph = 0;
       int cg = 0;
-      for (int t = pair0; t < args.tiles; t += npairs) {
-        for (int kb = 0; kb < nk; ++kb) {
+      for (int u = pair0; u < args.units; u += npairs) {
+        int t, sp, c0, ncu;
+        unit_of(u, t, sp, c0, ncu);
+        const int kbe = min(nk, 2 * (c0 + ncu));
+        for (int kb = 2 * c0; kb < kbe; ++kb) {
           const int kin = kb & 1;
           const int buf = cg & 1;
-          const bool chunk_last = kin == 1 || kb == nk - 1;
+          const bool chunk_last = kin == 1 || kb == kbe - 1;
           if (kin == 0) mbar_wait<true>(&tempty[buf], ((cg >> 1) & 1) ^ 1);
           mbar_wait<true>(&raw_full[rs], rph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -328,10 +352,10 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     if (BN > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     const int q = warp & 3;
     const int dg = (warp - 4) >> 2;            // column group: columns [128 dg, 128 dg + 128)
-    const int nchunks = (nk + 1) / 2;
     int cg = 0;
-    for (int t = pair0; t < args.tiles; t += npairs) {
-      int m0, n0, dev;
+    for (int u = pair0; u < args.units; u += npairs) {
+      int t, sp, c0, ncu, m0, n0, dev;
+      unit_of(u, t, sp, c0, ncu);
       tile_of(t, m0, n0, dev);
       m0 += (int)crank * HB;
       const int mblk = m0 / HB, nblk = (n0 + dg * 128) / HB;
@@ -341,8 +365,9 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       float acc[128];
 #pragma unroll
       for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-      for (int c = 0; c < nchunks; ++c, ++cg) {
+      for (int ci = 0; ci < ncu; ++ci, ++cg) {
         const int buf = cg & 1;
+        const int c = c0 + ci;
         const float f = live ? __fmul_rn(sa[c * args.sa_k], sb[c * args.sb_k]) : 0.f;
         mbar_wait(&tfull[buf], (cg >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -365,10 +390,11 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       const int row0 = m0 + q * 32;
       const int col0 = n0 + dg * 128;
       if (row0 >= args.M || col0 >= args.N) continue;
-      if (args.tma_store) {
-        // each 32 x 32 slice through a 128B-swizzled staging tile, one bulk tensor store
-        uint8_t* stg = smem + S::STG_OFF + (warp - 4) * S::STG_WARP;
-        constexpr int NSTG = S::STG_WARP / 4096;
+      uint8_t* stg = smem + S::STG_OFF + (warp - 4) * S::STG_WARP;
+      constexpr int NSTG = S::STG_WARP / 4096;
+      // one 32 x 128 slice (this warp's rows, its column group) through TMA
+      // stores: 32 x 32 sub-slices via a 128B-swizzled staging tile
+      auto store_slice = [&](const CUtensorMap* map, int row) {
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           if (col0 + cc * 32 >= args.N) break;
@@ -390,14 +416,56 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
           if (lane == 0) {
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tma_c)),
-                "r"(col0 + cc * 32), "r"(row0), "r"(dev), "r"(smem_u32(tt))
+                    reinterpret_cast<uint64_t>(map)),
+                "r"(col0 + cc * 32), "r"(row), "r"(dev), "r"(smem_u32(tt))
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
+      };
+      if (args.splits > 1) {
+        // partial slice -> workspace; the last of the S units of this slice folds
+        store_slice(&tma_w, sp * args.M + row0);
+        uint32_t* flag = reinterpret_cast<uint32_t*>(args.flag_base + (uint64_t)((int64_t)dev * args.flag_dev)) +
+                         (((int64_t)(t % (args.tiles_m * args.tiles_n)) * H_CG + crank) * S::NDG + dg) * 4 + q;
+        uint32_t old = 0;
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(flag) : "memory");
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old != (uint32_t)(args.splits - 1)) continue;
+        // last: fold the S partials in split order (own one re-read from L2)
+        const float* ws = reinterpret_cast<const float*>(args.ws_base + (uint64_t)((int64_t)dev * args.ws_dev));
+        const int row = row0 + lane;
+        if (row < args.M) {               // split-K needs N % 128 == 0: whole 128-column rows
+          const float4* pr = reinterpret_cast<const float4*>(ws + (int64_t)row * args.N + col0);
+          const int64_t sstride = (int64_t)args.M * args.N / 4;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float4 w = __ldcg(pr + j);
+            acc[4 * j] = w.x; acc[4 * j + 1] = w.y; acc[4 * j + 2] = w.z; acc[4 * j + 3] = w.w;
+          }
+#pragma unroll 1
+          for (int s2 = 1; s2 < args.splits; ++s2) {
+            pr += sstride;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float4 w = __ldcg(pr + j);
+              acc[4 * j] = __fadd_rn(acc[4 * j], w.x);
+              acc[4 * j + 1] = __fadd_rn(acc[4 * j + 1], w.y);
+              acc[4 * j + 2] = __fadd_rn(acc[4 * j + 2], w.z);
+              acc[4 * j + 3] = __fadd_rn(acc[4 * j + 3], w.w);
+            }
+          }
+        }
+        if (lane == 0) *flag = 0u;            // consumed: ready for the next launch
+      }
+      if (args.tma_store) {
+        store_slice(&tma_c, row0);
       } else {
         const int row = row0 + lane;
         if (row < args.M) {
@@ -490,15 +558,56 @@ struct SpxGemmH3 {
   Operand A, B;
   int64_t ws_bytes = 0;
   uint64_t ws = 0;
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb, mc, mw;
   H3Args args;
   SplitArgs sa, sb;
   dim3 grid;
   int bn = 128;         // output columns per CTA pair (H3Cfg)
+  int splits = 1;       // split-K units per tile
+  int64_t part_off = 0; // split-K partials in the workspace (after the flag words at 0)
 };
+
+// Split-K flag words live at the start of every stream workspace (a fixed
+// region, so no other GEMM's partials ever overwrite them): uint32
+// [tiles][2][BN/128][4] per device, tiles <= SM pairs when split.
+constexpr int64_t H3_FLAG_DEV = 8192;
 
 bool spx_gemm_h3_supported(const spx_gemm_params& p) {
   return spx_gemm_tc_supported(p) && p.splits <= 1 && p.epi == SPX_EPI_NONE;
+}
+
+// BN and split count for one GEMM.  BN = 256 (the largest MMA, least
+// shared-memory traffic per FLOP) unless its coarser tiles leave more of the
+// last wave idle -- compared in waves of CTA pairs, a BN = 256 tile costing
+// ~0.95 of two BN = 128 tiles.  Split-K when the tiles fill at most half the
+// pairs: S units per tile, each >= 2 k chunks (256 of K).
+static void h3_shape(const spx_gemm_params& p, int& bn, int& splits) {
+  const int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
+  const int pairs = sms / H_CG > 0 ? sms / H_CG : 1;
+  const int64_t tm = (p.M + HB * H_CG - 1) / (HB * H_CG);
+  const int64_t t128 = tm * ((p.N + 127) / 128) * p.ndev, t256 = tm * ((p.N + 255) / 256) * p.ndev;
+  const double w128 = (double)((t128 + pairs - 1) / pairs), w256 = (double)((t256 + pairs - 1) / pairs);
+  bn = (p.N > 128 && w256 * 2 * 0.95 < w128) ? 256 : 128;
+  if (const char* e = getenv("SPX_H3_BN")) bn = atoi(e) == 256 ? 256 : 128;
+  const int64_t tiles = bn == 256 ? t256 : t128;
+  const int nch = (int)(((p.K + HBK - 1) / HBK + 1) / 2);
+  // off by default: measured slower (512x1024x1024: 20 -> 36 us; C2 N=4 steps
+  // 3.40 -> 4.2 ms) -- the partial stores, the acq_rel counter and the
+  // latency-bound fold of S partials by the last unit outweigh the shorter
+  // k loop; SPX_H3_SPLITK=n (or h3_splitk = n > 1) enables up to n splits
+  int maxs = p.h3_splitk > 1 ? p.h3_splitk : 1;
+  if (const char* e = getenv("SPX_H3_SPLITK"))
+    if (p.h3_splitk != 1) maxs = atoi(e);
+  splits = 1;
+  const uint64_t cb = p.base + (uint64_t)(p.c_off * 4);
+  const bool tma_ok = (cb & 15) == 0 && (p.ldc & 3) == 0 && (p.dev_stride & 15) == 0 && p.ldc == p.N;
+  if (maxs > 1 && tma_ok && p.M % 32 == 0 && p.N % 128 == 0 && tiles * 2 <= pairs &&
+      tiles * H_CG * 2 * 4 * 4 <= H3_FLAG_DEV) {
+    int sk = (int)(pairs / tiles);
+    sk = sk < nch / 2 ? sk : nch / 2;
+    sk = sk < maxs ? sk : maxs;
+    splits = sk > 1 ? sk : 1;
+  }
 }
 
 int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out) {
@@ -506,7 +615,13 @@ int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out) {
   SpxGemmH3* g = new SpxGemmH3();
   g->p = p;
   const uint64_t a = p.base + (uint64_t)(p.a_off * 4), b = p.base + (uint64_t)(p.b_off * 4);
+  h3_shape(p, g->bn, g->splits);
   int64_t ws = 0;
+  if (g->splits > 1) {
+    ws = H3_FLAG_DEV * p.ndev;
+    g->part_off = ws;
+    ws += align_up((int64_t)g->splits * p.M * p.N * 4, 1024) * p.ndev;
+  }
   if (p.a_mn_major) operand_geom(g->A, a, p.lda, p.K, p.M, p.ndev, ws);
   else operand_geom(g->A, a, p.lda, p.M, p.K, p.ndev, ws);
   if (p.b_k_major) operand_geom(g->B, b, p.ldb, p.N, p.K, p.ndev, ws);
@@ -520,7 +635,7 @@ int spx_gemm_h3_prepare(const spx_gemm_params& p, SpxGemmH3** out) {
     };
     shared(g->A, p.h3_a_off, p.h3_a_scl);
     shared(g->B, p.h3_b_off, p.h3_b_scl);
-    ws = 0;
+    ws = g->splits > 1 ? g->part_off + align_up((int64_t)g->splits * p.M * p.N * 4, 1024) * p.ndev : 0;
   }
   g->ws_bytes = ws;
   *out = g;
@@ -531,26 +646,13 @@ int64_t spx_gemm_h3_ws_bytes(const SpxGemmH3* g) { return g->ws_bytes; }
 
 int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   const spx_gemm_params& p = g->p;
+  if (!ws && g->ws_bytes) return spx_set_error("gemm h3: workspace not bound");
+  const uint64_t wsb = ws;            // the stream workspace (split-K flags + partials)
   if (p.h3_shared) ws = 0;            // operand addresses are absolute
-  else if (!ws) return spx_set_error("gemm h3: workspace not bound");
-  g->ws = ws;
+  g->ws = wsb ? wsb : 1;
   const Operand &A = g->A, &B = g->B;
   if (make_map_h16(&g->ma, ws + A.piece_off, A.cols, A.rows, p.ndev, A.pitch, A.piece_dev, p.a_mn_major ? 64 : HB))
     return -1;
-  // tile width: BN = 256 (the largest MMA, least shared-memory traffic per
-  // FLOP) unless its coarser tiles leave more of the last wave idle --
-  // compared in waves of CTA pairs, a BN = 256 tile costing ~0.95 of two
-  // BN = 128 tiles
-  {
-    int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
-    const int pairs = sms / H_CG > 0 ? sms / H_CG : 1;
-    const int64_t tm = (p.M + HB * H_CG - 1) / (HB * H_CG);
-    const int64_t t128 = tm * ((p.N + 127) / 128) * p.ndev, t256 = tm * ((p.N + 255) / 256) * p.ndev;
-    const double w128 = (double)((t128 + pairs - 1) / pairs), w256 = (double)((t256 + pairs - 1) / pairs);
-    g->bn = (p.N > 128 && w256 * 2 * 0.95 < w128) ? 256 : 128;
-    const char* e = getenv("SPX_H3_BN");
-    if (e) g->bn = atoi(e) == 256 ? 256 : 128;
-  }
   if (make_map_h16(&g->mb, ws + B.piece_off, B.cols, B.rows, p.ndev, B.pitch, B.piece_dev,
                    p.b_k_major ? g->bn / H_CG : 64))
     return -1;
@@ -584,10 +686,23 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   } else {
     memset(&g->mc, 0, sizeof(g->mc));
   }
+  a_.splits = g->splits;
+  a_.units = a_.tiles * g->splits;
+  memset(&g->mw, 0, sizeof(g->mw));
+  a_.flag_base = wsb;
+  a_.flag_dev = H3_FLAG_DEV;
+  a_.ws_base = wsb + (uint64_t)g->part_off;
+  a_.ws_dev = align_up((int64_t)g->splits * p.M * p.N * 4, 1024);
+  if (g->splits > 1) {
+    if (!a_.tma_store) return spx_set_error("gemm h3 %dx%dx%d: split-K needs TMA stores", p.M, p.N, p.K);
+    if (make_map(&g->mw, a_.ws_base, p.N, (uint64_t)p.M * g->splits, p.ndev, (uint64_t)p.N * 4, a_.ws_dev, 32, false))
+      return -1;
+    SPX_CUDA(cudaMemset(reinterpret_cast<void*>(wsb), 0, (size_t)(H3_FLAG_DEV * p.ndev)));
+  }
   int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
   sms -= sms % H_CG;
   if (sms < H_CG) sms = H_CG;
-  const int want = a_.tiles * H_CG;
+  const int want = a_.units * H_CG;
   g->grid = dim3((unsigned)(want < sms ? want : sms));
   return 0;
 }
@@ -620,13 +735,13 @@ static cudaError_t launch_h3(const SpxGemmH3* g, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, gemm_h3_kernel<BN>, g->ma, g->mb, g->mc, g->args);
+  return cudaLaunchKernelEx(&cfg, gemm_h3_kernel<BN>, g->ma, g->mb, g->mc, g->mw, g->args);
 }
 
 int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
   const spx_gemm_params& p = g->p;
+  if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
   if (!p.h3_shared) {
-    if (!g->ws) return spx_set_error("gemm h3: workspace not bound");
     launch_split_args(g->sa, p.ndev, s);
     SPX_CHECK_LAUNCH();
     launch_split_args(g->sb, p.ndev, s);

@@ -397,6 +397,12 @@ class Executable:
             final.extend(after.get(id(k), []))
         c.kernels = final
 
+    def _first_side_gemm(self) -> int:
+        if not hasattr(self, "_fsg"):
+            ks = self.comp.kernels
+            self._fsg = next((i for i, k in enumerate(ks) if k.kind == "gemm" and self.stream_of.get(i)), len(ks))
+        return self._fsg
+
     def _emit_split(self, k):
         d = k.data
         buf, off, ld = d["src"]
@@ -659,6 +665,9 @@ class Executable:
         if "h3a" in d:
             p.path = 3
             p.h3_shared = 1
+            # split-K (opt-in, SPX_H3_SPLITK) only while nothing else computes:
+            # before the first GEMM of a side stream (the forward pass)
+            p.h3_splitk = 0 if self._cur < self._first_side_gemm() else 1
             p.h3_a_off = self.off[d["h3a"]]
             p.h3_b_off = self.off[d["h3b"]]
             p.h3_a_scl = p.h3_a_off + d["h3a_scl"]

@@ -65,7 +65,7 @@ class GemmParams(C.Structure):
                 ("epi_imm", C.c_float * 2),
                 ("sk_mode", C.c_int32), ("sk_pad", C.c_int32),
                 ("ws_off", C.c_int64), ("flag_off", C.c_int64),
-                ("h3_shared", C.c_int32), ("h3_pad", C.c_int32),
+                ("h3_shared", C.c_int32), ("h3_splitk", C.c_int32),
                 ("h3_a_off", C.c_int64), ("h3_a_scl", C.c_int64), ("h3_b_off", C.c_int64), ("h3_b_scl", C.c_int64)]
 
 

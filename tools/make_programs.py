@@ -55,6 +55,7 @@ CONFIGS = {
     "c2_tf8_dense": ("transformer", TF_C2, None, [], []),
     "c2_tf8_bp_B2": ("transformer", TF_C2, "B:2", ["bp"], []),
     "c2_tf8_bpmp_B2M2": ("transformer", TF_C2, "B:2,M:2", ["bp", "mp"], []),
+    "c2_tf8_bp_B4": ("transformer", TF_C2, "B:4", ["bp"], []),
     "c2_tf8_bpmp_B2M4": ("transformer", TF_C2, "B:2,M:4", ["bp", "mp"], []),
     # C3: transformer 32 blocks d=2048, BP+Z3 on B:8 (+ B:4, B:2)
     "c3_tf32_dense": ("transformer", TF_C3, None, [], []),
