@@ -355,6 +355,34 @@ def main():
                          f"{gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0:.1f} TFLOP/s"),
                 "step_ms_by_class": {k: round(v, 4) for k, v in sorted(cls_ms.items())},
                 "gemm_share_of_step": (gemm_ms / float(np.sum(rec_ms))) if np.sum(rec_ms) > 0 else None}
+    # streaming (HBM-bound) records: algorithmic bytes / eager record time
+    def _ew_bytes(q):
+        tot = 4 * q.numel * q.n_out
+        for j in range(q.n_in):
+            cnt = 1
+            for k in range(q.rank):
+                if q.inp[j].stride[k] != 0:
+                    cnt *= q.dims[k]
+            tot += 4 * cnt
+        return tot
+    s_bytes = s_ms = 0.0
+    for idx, ((kind, p), t) in enumerate(zip(recs, rec_ms)):
+        if kind == R.K_EW:
+            s_bytes += _ew_bytes(p)
+            s_ms += float(t)
+        elif kind == R.K_SPLIT:
+            fused = sess.ex.plan.record_info(idx)[1] == -1
+            # pieces written (+ the fp32 read when standalone); fused: time is in the EW record
+            s_bytes += 4.0 * p.rows * p.cols * (1 if fused else 2)
+            if not fused:
+                s_ms += float(t)
+    streaming = {"bound": "hbm", "kernels": "ew_static(_split)_kernel, ew_vec/gen_kernel, split_h16_kernel",
+                 "achieved": s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else 0.0, "peak": hbm, "unit": "GB/s",
+                 "frac": (s_bytes / (s_ms / 1e3) / 1e9 / hbm) if s_ms > 0 else 0.0,
+                 "bytes_per_step": s_bytes, "ms_per_step_eager": s_ms,
+                 "note": "algorithmic bytes (inputs once, broadcast operands at their own size, outputs, fp16 "
+                         "pieces) over the eager per-record time (CUDA events between records, launch gaps "
+                         "included) of every elementwise and split record of one step"}
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as fh:
             json.dump({"records": [[int(k), float(t)] for (k, _), t in zip(recs, rec_ms)],
@@ -373,7 +401,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-                "config": config, "roofline": roofline, "cpu_baseline": cpu,
+                "config": config, "roofline": roofline, "streaming_roofline": streaming, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_total),
                         "d2h_bytes_per_step": int(d2h_total),
                         "note": "Session.feed + Session.step: every step's batch (x, y) H2D from pinned memory (the copy of batch i+1 overlaps step i) and the "

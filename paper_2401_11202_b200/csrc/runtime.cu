@@ -393,6 +393,7 @@ int spx_plan_finalize(uint64_t plan) {
     a.split_out = j;
     a.split_params = b.params;
     b.fused = true;
+    b.path = -1;                 // reported by spx_plan_record_info: runs inside record i
   }
   for (int k = 0; k <= SPX_SIDE_STREAMS; ++k)
     if (h3need[k] && !P->h3ws[k]) SPX_CUDA(cudaMalloc(&P->h3ws[k], (size_t)h3need[k]));
