@@ -425,7 +425,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
       };
-      if (args.splits > 1) {
+      if (BN == 128 && args.splits > 1) {
         // partial slice -> workspace; the last of the S units of this slice folds
         store_slice(&tma_w, sp * args.M + row0);
         uint32_t* flag = reinterpret_cast<uint32_t*>(args.flag_base + (uint64_t)((int64_t)dev * args.flag_dev)) +
@@ -439,30 +439,36 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         old = __shfl_sync(0xffffffffu, old, 0);
         if (old != (uint32_t)(args.splits - 1)) continue;
         // last: fold the S partials in split order (own one re-read from L2)
+        // straight from global to C: lane = column, every load and store one
+        // 128-byte line (row-per-lane reads were L2-request bound)
         const float* ws = reinterpret_cast<const float*>(args.ws_base + (uint64_t)((int64_t)dev * args.ws_dev));
-        const int row = row0 + lane;
-        if (row < args.M) {               // split-K needs N % 128 == 0: whole 128-column rows
-          const float4* pr = reinterpret_cast<const float4*>(ws + (int64_t)row * args.N + col0);
-          const int64_t sstride = (int64_t)args.M * args.N / 4;
+        float* cb = reinterpret_cast<float*>(args.c_base + (uint64_t)((int64_t)dev * args.dev_stride));
+        const int64_t sst = (int64_t)args.M * args.N;
+        // acc (already stored as this unit's partial) is reused as x[row][col
+        // group]: every split's 128 lines per warp are in flight at once
+        const int nrow = min(32, args.M - row0);
+        const float* p0 = ws + (int64_t)row0 * args.N + col0 + lane;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float4 w = __ldcg(pr + j);
-            acc[4 * j] = w.x; acc[4 * j + 1] = w.y; acc[4 * j + 2] = w.z; acc[4 * j + 3] = w.w;
-          }
+        for (int r = 0; r < 32; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) acc[r * 4 + cc] = r < nrow ? __ldcg(p0 + (int64_t)r * args.N + cc * 32) : 0.f;
 #pragma unroll 1
-          for (int s2 = 1; s2 < args.splits; ++s2) {
-            pr += sstride;
+        for (int s2 = 1; s2 < args.splits; ++s2) {
+          const float* ps = p0 + s2 * sst;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float4 w = __ldcg(pr + j);
-              acc[4 * j] = __fadd_rn(acc[4 * j], w.x);
-              acc[4 * j + 1] = __fadd_rn(acc[4 * j + 1], w.y);
-              acc[4 * j + 2] = __fadd_rn(acc[4 * j + 2], w.z);
-              acc[4 * j + 3] = __fadd_rn(acc[4 * j + 3], w.w);
-            }
-          }
+          for (int r = 0; r < 32; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+              if (r < nrow) acc[r * 4 + cc] = __fadd_rn(acc[r * 4 + cc], __ldcg(ps + (int64_t)r * args.N + cc * 32));
         }
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            if (r < nrow) cb[(int64_t)(row0 + r) * args.ldc + col0 + cc * 32 + lane] = acc[r * 4 + cc];
         if (lane == 0) *flag = 0u;            // consumed: ready for the next launch
+        continue;
+
       }
       if (args.tma_store) {
         store_slice(&tma_c, row0);
@@ -591,17 +597,18 @@ static void h3_shape(const spx_gemm_params& p, int& bn, int& splits) {
   if (const char* e = getenv("SPX_H3_BN")) bn = atoi(e) == 256 ? 256 : 128;
   const int64_t tiles = bn == 256 ? t256 : t128;
   const int nch = (int)(((p.K + HBK - 1) / HBK + 1) / 2);
-  // off by default: measured slower (512x1024x1024: 20 -> 36 us; C2 N=4 steps
-  // 3.40 -> 4.2 ms) -- the partial stores, the acq_rel counter and the
-  // latency-bound fold of S partials by the last unit outweigh the shorter
-  // k loop; SPX_H3_SPLITK=n (or h3_splitk = n > 1) enables up to n splits
+  // off by default.  Measured (profiles/r01_gemm_h3_splitk.txt): long-K GEMMs
+  // gain (512x1024x4096: 44 -> 36 us) but short ones lose (512x1024x1024:
+  // 19 -> 27 us: partial stores + counter + fold ~8 us), and whole C2 steps at
+  // N=2/4 get 2-6% slower even with forward-only splits; SPX_H3_SPLITK=n (or
+  // h3_splitk = n > 1) enables up to n splits
   int maxs = p.h3_splitk > 1 ? p.h3_splitk : 1;
   if (const char* e = getenv("SPX_H3_SPLITK"))
     if (p.h3_splitk != 1) maxs = atoi(e);
   splits = 1;
   const uint64_t cb = p.base + (uint64_t)(p.c_off * 4);
   const bool tma_ok = (cb & 15) == 0 && (p.ldc & 3) == 0 && (p.dev_stride & 15) == 0 && p.ldc == p.N;
-  if (maxs > 1 && tma_ok && p.M % 32 == 0 && p.N % 128 == 0 && tiles * 2 <= pairs &&
+  if (maxs > 1 && bn == 128 && tma_ok && p.M % 32 == 0 && p.N % 128 == 0 && tiles * 2 <= pairs &&
       tiles * H_CG * 2 * 4 * 4 <= H3_FLAG_DEV) {
     int sk = (int)(pairs / tiles);
     sk = sk < nch / 2 ? sk : nch / 2;
