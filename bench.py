@@ -44,6 +44,14 @@ def peaks():
         return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+def bf16_sustained():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops_sustained"])
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -322,6 +330,7 @@ def main():
                 tensor_flops += 3.0 * f
                 ideal_ms += 3.0 * f / (tc_peak[path] * 1e12) * 1e3
     achieved = tensor_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    sust = bf16_sustained()       # MEASURED_PEAKS: cuBLAS bf16 back to back for 4 s (the step's regime)
     # DRAM traffic of one GEMM launch from the committed `ncu --set full` capture
     traffic, traffic_note = None, None
     try:
@@ -344,6 +353,8 @@ def main():
     roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": peak_eff, "unit": "TFLOP/s",
                 "frac": (ideal_ms / gemm_ms) if gemm_ms > 0 else 0.0,
+                "peak_sustained": sust,
+                "frac_vs_sustained": (achieved / sust) if (sust and paths.get(3, 0) == sum(paths.values())) else None,
                 "traffic": traffic,
                 "traffic_note": traffic_note,
                 "gemm_paths": {("h3" if k == 3 else "tf32" if k == 1 else "simt"): v for k, v in paths.items()},
