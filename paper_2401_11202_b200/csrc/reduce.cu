@@ -252,6 +252,75 @@ __global__ void __launch_bounds__(256) reduce_final_block(const __grid_constant_
   if (threadIdx.x == 0) dev_ptr(p.x.base, p.x.dev_stride, d, p.out_off)[o] = red[0];
 }
 
+// OUT mapping for a plain view (one input, no elementwise program, <= 64
+// reduced elements: the pooling windows of the U-Net analog): the reduced
+// offsets do not depend on the output, so they are computed once per block
+// into shared memory, and every thread issues all loads of a window before
+// folding them (in r order, as reduce_out).  The generic kernel recomputed
+// them with 64-bit divisions per element and loaded one element at a time.
+constexpr int OUTV_MAX_RED = 64;
+__global__ void __launch_bounds__(256) reduce_out_view(const __grid_constant__ spx_reduce_params p) {
+  __shared__ int64_t sred[OUTV_MAX_RED];
+  const spx_ew_params& x = p.x;
+  const int nk = p.n_kept;
+  const int nred = (int)p.n_red_elems;
+  for (int r = threadIdx.x; r < nred; r += blockDim.x) {
+    int64_t rr = r, off = 0;
+#pragma unroll
+    for (int k = SPX_MAX_RANK - 1; k >= 0; --k) {
+      if (k < nk || k >= x.rank) continue;
+      const int64_t ik = k == nk ? rr : rr % x.dims[k];
+      rr = k == nk ? 0 : rr / x.dims[k];
+      off += ik * x.in[0].stride[k];
+    }
+    sred[r] = off;
+  }
+  __syncthreads();
+  SPX_PDL_ENTRY();
+  const int d = blockIdx.y;
+  const float* fb = dev_ptr(x.base, x.dev_stride, d, 0);
+  float* out = dev_ptr(x.base, x.dev_stride, d, p.out_off);
+  const bool v4 = x.in[0].stride[nk - 1] == 1;
+  for (int64_t o4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o4 * 4 < p.n_out;
+       o4 += (int64_t)gridDim.x * blockDim.x) {
+    int64_t base = x.in[0].off;
+    int64_t rem = o4 * 4;
+#pragma unroll
+    for (int k = SPX_MAX_RANK - 1; k >= 0; --k) {
+      if (k >= nk) continue;
+      const int64_t ik = k == 0 ? rem : rem % x.dims[k];
+      rem = k == 0 ? 0 : rem / x.dims[k];
+      base += ik * x.in[0].stride[k];
+    }
+    const float* src = fb + base;
+    float4 acc = make_float4(ident(p.monoid), ident(p.monoid), ident(p.monoid), ident(p.monoid));
+    for (int r0 = 0; r0 < nred; r0 += 8) {
+      float4 t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u < nred) {
+          if (v4) {
+            t[u] = __ldg(reinterpret_cast<const float4*>(src + sred[r0 + u]));
+          } else {
+            const float v = __ldg(src + sred[r0 + u]);
+            t[u] = make_float4(v, v, v, v);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u < nred) {
+          acc.x = fold(p.monoid, acc.x, t[u].x);
+          acc.y = fold(p.monoid, acc.y, t[u].y);
+          acc.z = fold(p.monoid, acc.z, t[u].z);
+          acc.w = fold(p.monoid, acc.w, t[u].w);
+        }
+      }
+    }
+    *reinterpret_cast<float4*>(out + o4 * 4) = acc;
+  }
+}
+
 __global__ void reduce_final(const __grid_constant__ spx_reduce_params p, int nchunks) {
   SPX_PDL_ENTRY();
   const int d = blockIdx.y;
@@ -276,7 +345,9 @@ int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch) 
     const int64_t cap = (int64_t)spx_num_sms() * 16;
     if (b > cap) b = cap;
     if (b < 1) b = 1;
-    spx_launch(reduce_out, dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s, p);
+    const bool view = p.x.n_in == 1 && p.x.n_prog == 0 && p.x.out_reg[0] == 0 && p.n_red_elems <= OUTV_MAX_RED;
+    if (view) spx_launch(reduce_out_view, dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s, p);
+    else spx_launch(reduce_out, dim3((unsigned)b, (unsigned)p.x.ndev), 256, 0, s, p);
     SPX_CHECK_LAUNCH();
     if (nlaunch) ++*nlaunch;
     return 0;
