@@ -195,7 +195,8 @@ class Executable:
         hi += 2 * self.stage_elems
         # peer collectives: flag words [comm key][phase][member] (written by the
         # peers through their mapping of this arena) and local epoch counters
-        nkeys = len(self.comm_keys()) if c.comm_mode == "nccl" else 0
+        nkeys = len(self.peer_slots()) if c.comm_mode == "nccl" else 0
+        self.n_peer_slots = nkeys
         self.flag_off = hi
         self.counter_off = hi + nkeys * R.PEER_PHASES * R.PEER_MAX_BLOCKS * 8
         self.flag_elems = (_align(nkeys * R.PEER_PHASES * R.PEER_MAX_BLOCKS * 8 + nkeys * R.PEER_MAX_BLOCKS)
@@ -800,6 +801,36 @@ class Executable:
         g.dst = self._tref(np.array([out_addr], dtype=np.uint64))
         self._records.append((R.K_GATHER, g))
 
+    def _ar_key(self, k):
+        a = k.data["attrs"]
+        axes = a["axes"] if "axes" in a else [x for axs in a["axes_per_dim"] for x in axs]
+        return tuple(sorted(set(axes), key=self.comp.mesh.names().index))
+
+    def peer_slots(self):
+        """Flag/epoch slots of the peer all-reduce: one per (communicator,
+        stream).  Peer all-reduces on one slot run in stream order; different
+        streams never share flag words, so the gradient reductions on the
+        collective stream and the critical-path ones on the main stream both
+        take the peer path.  Same order on every rank (same program and
+        schedule).  SPX_PEER_SIDE=0: critical-path all-reduces only."""
+        import os
+        if not hasattr(self, "_slots"):
+            slots = [(key, self.MAIN) for key in self.comm_keys()]
+            if os.environ.get("SPX_PEER_SIDE", "1") != "0":
+                for i, k in enumerate(self.comp.kernels):
+                    if k.kind == "coll" and k.data["kind"] == "all_reduce":
+                        sk = (self._ar_key(k), self.stream_of.get(i, self.MAIN))
+                        if sk not in slots:
+                            slots.append(sk)
+            self._slots = slots
+        return self._slots
+
+    def _peer_slot(self, key):
+        st = self.stream_of.get(self._cur, self.MAIN)
+        if st != self.MAIN and (key, st) not in self.peer_slots():
+            return None
+        return self.peer_slots().index((key, st))
+
     def _emit_coll_nccl(self, k):
         c = self.comp
         d = k.data
@@ -825,9 +856,9 @@ class Executable:
         monoid = 0 if attrs.get("monoid", "sum") == "sum" else 1
         if kind == "all_reduce":
             count = _prod(in_dims)
-            if (self.peer_bases is not None and self._cur not in self.side and 1 < n <= 8
-                    and count * 4 <= self.peer_max_bytes):
-                slot = self.comm_keys().index(key)
+            slot = self._peer_slot(key)
+            if (self.peer_bases is not None and 1 < n <= 8 and count * 4 <= self.peer_max_bytes
+                    and slot is not None):
                 p = R.PeerParams()
                 p.kind, p.n, p.me, p.monoid, p.count, p.slot = 0, n, grp.index(me), monoid, count, slot
                 for j, r in enumerate(grp):

@@ -339,7 +339,7 @@ def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
             outs = []
             for r in range(world):
                 p = exs[r].records()[i][1]
-                grp = plan[[k for k, _ in plan].index(exs[r].comm_keys()[p.slot])][1]
+                grp = plan[[k for k, _ in plan].index(exs[r].peer_slots()[p.slot][0])][1]
                 grp = next(g for g in grp if r in g)
                 assert grp.index(r) == p.me and len(grp) == p.n
                 acc = None

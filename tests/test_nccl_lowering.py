@@ -49,7 +49,7 @@ def test_peer_records_replace_critical_path_all_reduces():
     ex = Executable(m, devices=[0], comm_mode="nccl", dry=True, comm_factory=lambda e: _dry_comms(e, True))
     kinds = [k for k, _ in ex.records()]
     assert R.K_PEER in kinds
-    nkeys = len(ex.comm_keys())
+    nkeys = ex.n_peer_slots
     for k, p in ex.records():
         if k == R.K_PEER:
             assert p.n == 2 and 0 <= p.slot < nkeys and p.kind == 0
