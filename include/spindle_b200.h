@@ -206,19 +206,21 @@ typedef struct {
   int64_t count;                   /* elements: per-rank send count (AG/A2A chunk), recv count (RS), total (AR) */
 } spx_nccl_params;
 
-/* ---- all-reduce over NVLink peer memory (CUDA IPC-mapped arenas) -------- */
+/* ---- all-reduce / reduce-scatter / all-gather over NVLink peer memory ----- */
 /* Flag region of a member (uint32): [slot][phase SPX_PEER_PHASES][block SPX_PEER_MAX_BLOCKS][member 8];
  * epoch counters (local): [slot][block]. */
 #define SPX_PEER_MAX_BLOCKS 512
 #define SPX_PEER_PHASES 3
 typedef struct {
-  int32_t kind, n, me, monoid;     /* kind 0 = all-reduce; n members; me = my index */
-  int64_t count;                   /* elements */
+  int32_t kind, n, me, monoid;     /* kind 0 = all-reduce, 1 = all-gather (dst[m * count ..] = member m's src),
+                                      2 = reduce-scatter (src[] point at my chunk of each member's input);
+                                      n members; me = my index */
+  int64_t count;                   /* elements (all-gather: per member) */
   uint64_t src[8];                 /* members' input buffers, mapped into this process */
   uint64_t dst;                    /* local output */
   uint64_t flags[8];               /* members' flag regions (mapped), layout above */
   uint64_t counter;                /* local epoch counters, u32 [slot][block] */
-  int32_t slot, pad;
+  int32_t slot, max_blocks;        /* max_blocks: 0 = default (2 per SM); fewer leave SMs to concurrent compute */
 } spx_peer_params;
 
 /* ---- plan records --------------------------------------------------------- */

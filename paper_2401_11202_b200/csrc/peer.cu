@@ -200,18 +200,55 @@ __global__ void __launch_bounds__(256) peer_allreduce_2shot(const __grid_constan
   if (threadIdx.x == 0) *counter = epoch;
 }
 
+// All-gather: dst[m * count + i] = member m's src[i] (chunks in member order,
+// the reference's all_gather layout for a dim-0 gather in group order).  The
+// same arrive / depart barriers: inputs complete before anyone reads, nobody
+// leaves while a peer still reads its input.
+template <int N>
+__global__ void __launch_bounds__(256) peer_allgather(const __grid_constant__ spx_peer_params p, int64_t per_block) {
+  SPX_PDL_ENTRY();
+  uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
+  const uint32_t epoch = *counter + 1u;
+  block_barrier(p, 0, epoch);
+  const int64_t n4 = p.count >> 2;
+  const int64_t b0 = (int64_t)blockIdx.x * per_block, b1 = min(n4, b0 + per_block);
+  float4* dst = reinterpret_cast<float4*>(p.dst);
+  for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += 256 * U) {
+    float4 v[N][U];
+#pragma unroll
+    for (int m = 0; m < N; ++m)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * 256;
+        if (i < b1) v[m][u] = reinterpret_cast<const float4*>(p.src[m])[i];
+      }
+#pragma unroll
+    for (int m = 0; m < N; ++m)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * 256;
+        if (i < b1) dst[m * n4 + i] = v[m][u];
+      }
+  }
+  __syncthreads();
+  block_barrier(p, 1, epoch);
+  if (threadIdx.x == 0) *counter = epoch;
+}
+
 }  // namespace
 
 int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if (p.n < 1 || p.n > 8) return spx_set_error("peer collective: group size %d", p.n);
-  if ((p.dst & 15) || p.kind != 0) return spx_set_error("peer collective: unsupported record");
+  if ((p.dst & 15) || p.kind < 0 || p.kind > 2 || (p.kind == 1 && (p.count & 3)))
+    return spx_set_error("peer collective: unsupported record");
   for (int m = 0; m < p.n; ++m)
     if (p.src[m] & 15) return spx_set_error("peer collective: unaligned source");
   // blocks: ~2 float4 per thread, at most 2 per SM (co-resident with little
   // else) and SPX_PEER_MAX_BLOCKS (flag space); identical on every member
   const int64_t n4 = p.count >> 2;
   int64_t blocks = (n4 + 256 * 2 - 1) / (256 * 2);
-  const int64_t cap = (int64_t)spx_num_sms() * 2 < SPX_PEER_MAX_BLOCKS ? (int64_t)spx_num_sms() * 2 : SPX_PEER_MAX_BLOCKS;
+  int64_t cap = (int64_t)spx_num_sms() * 2 < SPX_PEER_MAX_BLOCKS ? (int64_t)spx_num_sms() * 2 : SPX_PEER_MAX_BLOCKS;
+  if (p.max_blocks > 0 && p.max_blocks < cap) cap = p.max_blocks;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const int64_t per_block = (n4 + blocks - 1) / blocks;
@@ -220,7 +257,21 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if (two < 0) { const char* e = getenv("SPX_PEER_TWOSHOT"); two = e ? atoi(e) : 1; }
   // two-shot for 4 and 8 members from 2 MB (4 ranks, 4 MB: 18.7 us vs 25.0 us
   // one-shot; 1 MB: 14.4 vs 11.2), when every segment is whole float4s
-  if (two && (p.n == 4 || p.n == 8) && (p.count & 3) == 0 && (n4 % p.n) == 0 && n4 >= 131072 && !dbg) {
+  if (p.kind == 1) {
+    switch (p.n) {
+      case 2: spx_launch(peer_allgather<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
+      case 3: spx_launch(peer_allgather<3>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
+      case 4: spx_launch(peer_allgather<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
+      case 8: spx_launch(peer_allgather<8>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
+      default: return spx_set_error("peer all-gather: group size %d", p.n);
+    }
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+    return 0;
+  }
+  // kind 2, reduce-scatter: the sources point at this member's chunk of every
+  // member's input, and only that chunk is folded (one-shot kernel)
+  if (two && p.kind == 0 && p.max_blocks == 0 && (p.n == 4 || p.n == 8) && (p.count & 3) == 0 && (n4 % p.n) == 0 && n4 >= 131072 && !dbg) {
     const int64_t seg4 = n4 / p.n;
     int64_t b2 = (seg4 + 256 * 2 - 1) / (256 * 2);     // ~2 float4 per thread per phase
     if (b2 > cap) b2 = cap;

@@ -69,6 +69,9 @@ class Executable:
         # reductions (csrc/peer.cu) once the factory maps the peers' arenas
         self.wants_peer = comm_mode == "nccl" and os.environ.get("SPX_PEER", "1") != "0"
         self.peer_max_bytes = int(os.environ.get("SPX_PEER_MAX_BYTES", str(64 << 20)))
+        self.peer_ag = os.environ.get("SPX_PEER_AG", "1") != "0"
+        self.peer_rs = os.environ.get("SPX_PEER_RS", "1") != "0"
+        self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
         self.peer_bases = None          # [arena base of rank r, mapped here]
         self._peer_handles = []
         self._layout()
@@ -818,7 +821,7 @@ class Executable:
             slots = [(key, self.MAIN) for key in self.comm_keys()]
             if os.environ.get("SPX_PEER_SIDE", "1") != "0":
                 for i, k in enumerate(self.comp.kernels):
-                    if k.kind == "coll" and k.data["kind"] == "all_reduce":
+                    if k.kind == "coll" and k.data["kind"] in ("all_reduce", "reduce_scatter", "all_gather"):
                         sk = (self._ar_key(k), self.stream_of.get(i, self.MAIN))
                         if sk not in slots:
                             slots.append(sk)
@@ -854,19 +857,25 @@ class Executable:
         comm = self.comms[key]
         n = len(grp)
         monoid = 0 if attrs.get("monoid", "sum") == "sum" else 1
+        slot = self._peer_slot(key)
+        use_peer = self.peer_bases is not None and 1 < n <= 8 and slot is not None
+
+        def peer(pkind, count, src_shift=0):
+            p = R.PeerParams()
+            p.kind, p.n, p.me, p.monoid, p.count, p.slot = pkind, n, grp.index(me), monoid, count, slot
+            for j, r in enumerate(grp):
+                p.src[j] = self.peer_bases[r] + (src_a - self.base) + src_shift
+                p.flags[j] = self.peer_bases[r] + self.flag_off * 4
+            p.dst = out_a
+            p.counter = self.base + self.counter_off * 4
+            # off the critical path: leave most SMs to the concurrent GEMMs
+            p.max_blocks = self.peer_side_blocks if self._cur in self.side else 0
+            self._records.append((R.K_PEER, p))
+
         if kind == "all_reduce":
             count = _prod(in_dims)
-            slot = self._peer_slot(key)
-            if (self.peer_bases is not None and 1 < n <= 8 and count * 4 <= self.peer_max_bytes
-                    and slot is not None):
-                p = R.PeerParams()
-                p.kind, p.n, p.me, p.monoid, p.count, p.slot = 0, n, grp.index(me), monoid, count, slot
-                for j, r in enumerate(grp):
-                    p.src[j] = self.peer_bases[r] + (src_a - self.base)
-                    p.flags[j] = self.peer_bases[r] + self.flag_off * 4
-                p.dst = out_a
-                p.counter = self.base + self.counter_off * 4
-                self._records.append((R.K_PEER, p))
+            if use_peer and count * 4 <= self.peer_max_bytes:
+                peer(0, count)
                 return
             self._nccl(R.NCCL_ALLREDUCE, comm, src_a, out_a, count, monoid)
             return
@@ -878,6 +887,9 @@ class Executable:
             combo_of = [sum(c._chunk_index(coords[m], apd[j]) * cm[j] for j in range(len(apd))) for m in grp]
             direct = (all(not apd[j] for j in range(1, len(apd))) and combo_of == list(range(n))
                       and _prod(nper) == n)
+            if direct and use_peer and nloc % 4 == 0 and n * nloc * 4 <= self.peer_max_bytes and self.peer_ag:
+                peer(1, nloc)
+                return
             if direct:
                 self._nccl(R.NCCL_ALLGATHER, comm, src_a, out_a, nloc)
                 return
@@ -893,6 +905,9 @@ class Executable:
             offs = [sum(c._chunk_index(coords[m], apd[j]) * out_dims[j] * S[j] for j in range(len(apd)))
                     for m in grp]
             if offs == [j * nout for j in range(n)]:
+                if use_peer and nout % 4 == 0 and n * nout * 4 <= self.peer_max_bytes and self.peer_rs:
+                    peer(2, nout, grp.index(me) * nout * 4)
+                    return
                 self._nccl(R.NCCL_REDUCESCATTER, comm, src_a, out_a, nout, monoid)
                 return
             # relayout send buffer as [member j][chunk of member j]

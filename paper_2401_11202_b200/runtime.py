@@ -102,7 +102,7 @@ class PeerParams(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("me", C.c_int32), ("monoid", C.c_int32),
                 ("count", C.c_int64), ("src", C.c_uint64 * 8), ("dst", C.c_uint64),
                 ("flags", C.c_uint64 * 8), ("counter", C.c_uint64), ("slot", C.c_int32),
-                ("pad", C.c_int32)]
+                ("max_blocks", C.c_int32)]
 
 
 K_PEER = 7

@@ -346,6 +346,9 @@ def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
                 for j, m in enumerate(grp):
                     o = sims[m].idx(p.src[j])
                     x = sims[m].arena[o:o + p.count]
+                    if p.kind == 1:          # all-gather: member chunks in member order
+                        acc = x.copy() if acc is None else np.concatenate([acc, x])
+                        continue
                     acc = x.copy() if acc is None else (np.add(acc, x) if p.monoid == 0 else np.maximum(acc, x))
                 outs.append((r, sims[r].idx(p.dst), acc))
             for r, d0, acc in outs:
