@@ -887,7 +887,8 @@ class Executable:
             combo_of = [sum(c._chunk_index(coords[m], apd[j]) * cm[j] for j in range(len(apd))) for m in grp]
             direct = (all(not apd[j] for j in range(1, len(apd))) and combo_of == list(range(n))
                       and _prod(nper) == n)
-            if direct and use_peer and nloc % 4 == 0 and n * nloc * 4 <= self.peer_max_bytes and self.peer_ag:
+            if (direct and use_peer and n in (2, 3, 4, 8) and nloc % 4 == 0 and n * nloc * 4 <= self.peer_max_bytes
+                    and self.peer_ag):
                 peer(1, nloc)
                 return
             if direct:
