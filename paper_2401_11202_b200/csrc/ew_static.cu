@@ -6,6 +6,7 @@
 // with the same per-op IEEE rounding (bit-identical results) but no
 // interpretation overhead -- ncu showed the interpreter latency-bound at
 // 0.9-1.7 TB/s on exactly these programs.
+#include <cstdlib>
 #include "interp.cuh"
 #include "h3_split.cuh"
 
@@ -98,6 +99,7 @@ struct EwSplit {
   uint64_t dst, scl;        // device-0 addresses
   int64_t dev_stride, pitch;
   int rows, cols, cb, which;
+  int nb;                   // row blocks per cluster (pipelined)
 };
 
 // The same program over 128 x 128 output blocks, a cluster of H3_CL CTAs per
@@ -109,12 +111,11 @@ template <int NIN, int NOUT, int O0, int O1, uint32_t... I>
 __global__ void __cluster_dims__(H3_CL, 1, 1) __launch_bounds__(256)
 ew_static_split_kernel(const __grid_constant__ spx_ew_params p, const __grid_constant__ EwSplit q) {
   __shared__ float wmax[8];
-  __shared__ float cmax[H3_CL];
+  __shared__ float cmax[2][H3_CL];
   SPX_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = blockIdx.z;
   const int crank = blockIdx.x % H3_CL, bx = blockIdx.x / H3_CL;
-  const int r0 = blockIdx.y * H3_BLOCK + crank * H3_ROWS;
   const int c = bx * H3_BLOCK + lane * 4;
   const float* __restrict__ fb = dev_ptr(p.base, p.dev_stride, d, 0);
   float* __restrict__ ob = dev_ptr(p.base, p.dev_stride, d, 0);
@@ -122,52 +123,69 @@ ew_static_split_kernel(const __grid_constant__ spx_ew_params p, const __grid_con
   const int64_t ecols = two_d ? p.dims[1] : p.numel;
   float* out0 = ob + p.out_off[0];
   float* out1 = ob + p.out_off[NOUT > 1 ? 1 : 0];
-  float4 keep[H3_V];
-  float m = 0.f;
-#pragma unroll
-  for (int i = 0; i < H3_V; ++i) {
-    const int row = r0 + i * 8 + warp;
-    keep[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (row >= q.rows || c >= q.cols) continue;
-    const int64_t e = (int64_t)row * q.cols + c;
-    const int64_t erow = two_d ? e / ecols : 0;
-    const int64_t ecol = e - erow * ecols;
-    Vec<4> r[SPX_NREG];
-#pragma unroll
-    for (int j = 0; j < NIN; ++j) {
-      const float* src = fb + p.in[j].off + (two_d ? erow * p.in[j].stride[0] : 0);
-      if (p.in[j].stride[p.rank - 1] != 0) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(src + ecol));
-        r[j].v[0] = t.x; r[j].v[1] = t.y; r[j].v[2] = t.z; r[j].v[3] = t.w;
-      } else {
-        const float t = __ldg(src);
-        r[j].v[0] = t; r[j].v[1] = t; r[j].v[2] = t; r[j].v[3] = t;
-      }
-    }
-    run_static<I...>(r, p.imm, std::make_integer_sequence<int, (int)sizeof...(I)>{});
-    const float4 y0 = make_float4(r[O0].v[0], r[O0].v[1], r[O0].v[2], r[O0].v[3]);
-    *reinterpret_cast<float4*>(out0 + e) = y0;
-    if (NOUT > 1) {
-      const float4 y1 = make_float4(r[O1].v[0], r[O1].v[1], r[O1].v[2], r[O1].v[3]);
-      *reinterpret_cast<float4*>(out1 + e) = y1;
-      keep[i] = q.which ? y1 : y0;
-    } else {
-      keep[i] = y0;
-    }
-    m = h3_absmax4(m, keep[i]);
-  }
-  m = h3_cluster_max(m, wmax, cmax, crank);
-  const int ex = h3_scale_exp(m);
-  const float up = h3_pow2(ex);
-  if (threadIdx.x == 0 && crank == 0)
-    reinterpret_cast<float*>(q.scl + (uint64_t)((int64_t)d * q.dev_stride))[blockIdx.y * q.cb + bx] = h3_pow2(-ex);
   __half* hi = reinterpret_cast<__half*>(q.dst + (uint64_t)((int64_t)d * q.dev_stride));
   __half* lo = hi + (int64_t)q.rows * q.pitch;
+  // q.nb row blocks per cluster, software-pipelined: the inputs of block
+  // it + 1 are loaded before the pieces of block it are stored, so the read
+  // and write streams of consecutive blocks overlap
+  auto load = [&](int rb, Vec<4> (&r)[H3_V][SPX_NREG]) {
 #pragma unroll
-  for (int i = 0; i < H3_V; ++i) {
-    const int row = r0 + i * 8 + warp;
-    if (row >= q.rows || c >= q.cols) continue;
-    h3_store4(hi, lo, (int64_t)row * q.pitch + c, keep[i], up, 4);
+    for (int i = 0; i < H3_V; ++i) {
+      const int row = rb * H3_BLOCK + crank * H3_ROWS + i * 8 + warp;
+      if (row >= q.rows || c >= q.cols) continue;
+      const int64_t e = (int64_t)row * q.cols + c;
+      const int64_t erow = two_d ? e / ecols : 0;
+      const int64_t ecol = e - erow * ecols;
+#pragma unroll
+      for (int j = 0; j < NIN; ++j) {
+        const float* src = fb + p.in[j].off + (two_d ? erow * p.in[j].stride[0] : 0);
+        if (p.in[j].stride[p.rank - 1] != 0) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(src + ecol));
+          r[i][j].v[0] = t.x; r[i][j].v[1] = t.y; r[i][j].v[2] = t.z; r[i][j].v[3] = t.w;
+        } else {
+          const float t = __ldg(src);
+          r[i][j].v[0] = t; r[i][j].v[1] = t; r[i][j].v[2] = t; r[i][j].v[3] = t;
+        }
+      }
+    }
+  };
+  const int rb0 = blockIdx.y * q.nb;
+  const int rb1 = min(rb0 + q.nb, (q.rows + H3_BLOCK - 1) / H3_BLOCK);
+  Vec<4> r[H3_V][SPX_NREG];
+  load(rb0, r);
+  for (int rb = rb0; rb < rb1; ++rb) {
+    float4 keep[H3_V];
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < H3_V; ++i) {
+      const int row = rb * H3_BLOCK + crank * H3_ROWS + i * 8 + warp;
+      keep[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row >= q.rows || c >= q.cols) continue;
+      const int64_t e = (int64_t)row * q.cols + c;
+      run_static<I...>(r[i], p.imm, std::make_integer_sequence<int, (int)sizeof...(I)>{});
+      const float4 y0 = make_float4(r[i][O0].v[0], r[i][O0].v[1], r[i][O0].v[2], r[i][O0].v[3]);
+      *reinterpret_cast<float4*>(out0 + e) = y0;
+      if (NOUT > 1) {
+        const float4 y1 = make_float4(r[i][O1].v[0], r[i][O1].v[1], r[i][O1].v[2], r[i][O1].v[3]);
+        *reinterpret_cast<float4*>(out1 + e) = y1;
+        keep[i] = q.which ? y1 : y0;
+      } else {
+        keep[i] = y0;
+      }
+      m = h3_absmax4(m, keep[i]);
+    }
+    m = h3_cluster_max(m, wmax, cmax[rb & 1], crank);
+    if (rb + 1 < rb1) load(rb + 1, r);
+    const int ex = h3_scale_exp(m);
+    const float up = h3_pow2(ex);
+    if (threadIdx.x == 0 && crank == 0)
+      reinterpret_cast<float*>(q.scl + (uint64_t)((int64_t)d * q.dev_stride))[rb * q.cb + bx] = h3_pow2(-ex);
+#pragma unroll
+    for (int i = 0; i < H3_V; ++i) {
+      const int row = rb * H3_BLOCK + crank * H3_ROWS + i * 8 + warp;
+      if (row >= q.rows || c >= q.cols) continue;
+      h3_store4(hi, lo, (int64_t)row * q.pitch + c, keep[i], up, 4);
+    }
   }
 }
 
@@ -270,7 +288,15 @@ int spx_launch_ew_static_split(int id, const spx_ew_params& p, const spx_split_p
   q.cols = sp.cols;
   q.cb = (sp.cols + H3_BLOCK - 1) / H3_BLOCK;
   q.which = which;
-  const dim3 g((unsigned)(H3_CL * q.cb), (unsigned)((sp.rows + H3_BLOCK - 1) / H3_BLOCK), (unsigned)p.ndev);
+  const int rbs = (sp.rows + H3_BLOCK - 1) / H3_BLOCK;
+  // two row blocks per cluster once the grid still covers every SM twice
+  static int nbe = -1;
+  if (nbe < 0) {
+    const char* e = getenv("SPX_EW_SPLIT_NB");
+    nbe = e ? atoi(e) : 0;
+  }
+  q.nb = nbe > 0 ? nbe : ((int64_t)q.cb * H3_CL * ((rbs + 1) / 2) >= 2 * spx_num_sms() ? 2 : 1);
+  const dim3 g((unsigned)(H3_CL * q.cb), (unsigned)((rbs + q.nb - 1) / q.nb), (unsigned)p.ndev);
   kCatalog[id].launch_split(p, q, g, s);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;

@@ -887,8 +887,12 @@ class Executable:
             combo_of = [sum(c._chunk_index(coords[m], apd[j]) * cm[j] for j in range(len(apd))) for m in grp]
             direct = (all(not apd[j] for j in range(1, len(apd))) and combo_of == list(range(n))
                       and _prod(nper) == n)
+            # peer all-gathers only for gathers of function arguments (the
+            # ZeRO-3 parameter prefetch at the start of the step, C3/C5): a
+            # ZeRO-2 gather of freshly updated shards at the end of the step
+            # (C4 on 4 GPUs) hit a launch failure that is not understood yet
             if (direct and use_peer and n in (2, 3, 4, 8) and nloc % 4 == 0 and n * nloc * 4 <= self.peer_max_bytes
-                    and self.peer_ag):
+                    and self.peer_ag and src in c.arg_bufs):
                 peer(1, nloc)
                 return
             if direct:
