@@ -19,6 +19,16 @@
 //      overwrite its input) while a peer still reads it.
 // Epochs are per (slot, block) counters in the local arena, so graph replays
 // and eager runs keep counting without host involvement.
+//
+// Forward progress.  A block spins until the same block of every member has
+// arrived, so a member must never let one peer kernel starve another of SM
+// slots: with two slots in flight (main and collective streams), rank A may
+// start X before Y and rank B Y before X.  Hence (1) a peer kernel never lets
+// its stream's NEXT kernel launch early (no PDL trigger before the final
+// barrier: PDL dependents parked at griddepcontrol.wait would fill the SMs
+// while X waits on a peer), and (2) a peer kernel holds at most one block per
+// SM while every variant fits two per SM (__launch_bounds__(256, 2)), so a
+// second peer kernel -- or an NCCL kernel -- always finds room.
 #include <cstdlib>
 #include "common.cuh"
 
@@ -69,13 +79,21 @@ SPX_DEV float4 fold4(int monoid, float4 a, float4 v) {
   return a;
 }
 
-constexpr int U = 4;   // float4 per thread per iteration (loads in flight per member)
+// float4 per thread per iteration (loads in flight per member): N * U float4
+// registers, kept under the 128-register cap of two blocks per SM
+template <int N>
+struct PeerU { static constexpr int value = N >= 8 ? 2 : 4; };
+
+// wait for the previous grid; no early launch of the next one (see above)
+#define SPX_PEER_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define SPX_PEER_EXIT() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 
 // N > 0: member count known at compile time (all loads issued before folding)
 template <int N>
-__global__ void __launch_bounds__(256) peer_allreduce(const __grid_constant__ spx_peer_params p, int64_t per_block,
+__global__ void __launch_bounds__(256, 2) peer_allreduce(const __grid_constant__ spx_peer_params p, int64_t per_block,
                                                       int dbg) {
-  SPX_PDL_ENTRY();
+  SPX_PEER_ENTRY();
+  constexpr int U = PeerU<N>::value;
   const int n = N > 0 ? N : p.n;
   uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
   const uint32_t epoch = *counter + 1u;
@@ -128,6 +146,7 @@ __global__ void __launch_bounds__(256) peer_allreduce(const __grid_constant__ sp
   __syncthreads();
   if (!(dbg & 2)) block_barrier(p, 1, epoch);
   if (threadIdx.x == 0) *counter = epoch;
+  SPX_PEER_EXIT();
 }
 
 // Two-shot (n >= 4): block b owns chunk b of every member's segment.
@@ -139,9 +158,10 @@ __global__ void __launch_bounds__(256) peer_allreduce(const __grid_constant__ sp
 // NVLink traffic per rank 2(n-1)/n of the tensor instead of (n-1); the fold
 // (and so every replica's bits) is the same as the one-shot kernel's.
 template <int N>
-__global__ void __launch_bounds__(256) peer_allreduce_2shot(const __grid_constant__ spx_peer_params p,
+__global__ void __launch_bounds__(256, 2) peer_allreduce_2shot(const __grid_constant__ spx_peer_params p,
                                                             int64_t seg4, int64_t per_block) {
-  SPX_PDL_ENTRY();
+  SPX_PEER_ENTRY();
+  constexpr int U = PeerU<N>::value;
   uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
   const uint32_t epoch = *counter + 1u;
   block_barrier(p, 0, epoch);
@@ -198,6 +218,7 @@ __global__ void __launch_bounds__(256) peer_allreduce_2shot(const __grid_constan
   __syncthreads();
   block_barrier(p, 2, epoch);
   if (threadIdx.x == 0) *counter = epoch;
+  SPX_PEER_EXIT();
 }
 
 // All-gather: dst[m * count + i] = member m's src[i] (chunks in member order,
@@ -205,8 +226,9 @@ __global__ void __launch_bounds__(256) peer_allreduce_2shot(const __grid_constan
 // same arrive / depart barriers: inputs complete before anyone reads, nobody
 // leaves while a peer still reads its input.
 template <int N>
-__global__ void __launch_bounds__(256) peer_allgather(const __grid_constant__ spx_peer_params p, int64_t per_block) {
-  SPX_PDL_ENTRY();
+__global__ void __launch_bounds__(256, 2) peer_allgather(const __grid_constant__ spx_peer_params p, int64_t per_block) {
+  SPX_PEER_ENTRY();
+  constexpr int U = PeerU<N>::value;
   uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
   const uint32_t epoch = *counter + 1u;
   block_barrier(p, 0, epoch);
@@ -233,6 +255,7 @@ __global__ void __launch_bounds__(256) peer_allgather(const __grid_constant__ sp
   __syncthreads();
   block_barrier(p, 1, epoch);
   if (threadIdx.x == 0) *counter = epoch;
+  SPX_PEER_EXIT();
 }
 
 }  // namespace
@@ -243,11 +266,14 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
     return spx_set_error("peer collective: unsupported record");
   for (int m = 0; m < p.n; ++m)
     if (p.src[m] & 15) return spx_set_error("peer collective: unaligned source");
-  // blocks: ~2 float4 per thread, at most 2 per SM (co-resident with little
-  // else) and SPX_PEER_MAX_BLOCKS (flag space); identical on every member
+  // blocks: ~2 float4 per thread, at most one per SM (forward progress, see
+  // the top of the file) and SPX_PEER_MAX_BLOCKS (flag space); identical on
+  // every member
   const int64_t n4 = p.count >> 2;
   int64_t blocks = (n4 + 256 * 2 - 1) / (256 * 2);
-  int64_t cap = (int64_t)spx_num_sms() * 2 < SPX_PEER_MAX_BLOCKS ? (int64_t)spx_num_sms() * 2 : SPX_PEER_MAX_BLOCKS;
+  static int per_sm = -1;
+  if (per_sm < 0) { const char* e = getenv("SPX_PEER_BLOCKS_PER_SM"); per_sm = e ? atoi(e) : 1; }
+  int64_t cap = (int64_t)spx_num_sms() * per_sm < SPX_PEER_MAX_BLOCKS ? (int64_t)spx_num_sms() * per_sm : SPX_PEER_MAX_BLOCKS;
   if (p.max_blocks > 0 && p.max_blocks < cap) cap = p.max_blocks;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;

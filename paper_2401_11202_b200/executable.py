@@ -70,6 +70,7 @@ class Executable:
         self.wants_peer = comm_mode == "nccl" and os.environ.get("SPX_PEER", "1") != "0"
         self.peer_max_bytes = int(os.environ.get("SPX_PEER_MAX_BYTES", str(64 << 20)))
         self.peer_ag = os.environ.get("SPX_PEER_AG", "1") != "0"
+        self.peer_ag_all = os.environ.get("SPX_PEER_AG_ALL", "1") != "0"
         self.peer_rs = os.environ.get("SPX_PEER_RS", "1") != "0"
         self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
         self.peer_bases = None          # [arena base of rank r, mapped here]
@@ -888,12 +889,12 @@ class Executable:
             combo_of = [sum(c._chunk_index(coords[m], apd[j]) * cm[j] for j in range(len(apd))) for m in grp]
             direct = (all(not apd[j] for j in range(1, len(apd))) and combo_of == list(range(n))
                       and _prod(nper) == n)
-            # peer all-gathers only for gathers of function arguments (the
-            # ZeRO-3 parameter prefetch at the start of the step, C3/C5): a
-            # ZeRO-2 gather of freshly updated shards at the end of the step
-            # (C4 on 4 GPUs) hit a launch failure that is not understood yet
+            # every direct gather: the ZeRO-3 parameter prefetch (function
+            # arguments, C3/C5) and the ZeRO-2 gathers of freshly updated
+            # shards at the end of the step (C4); SPX_PEER_AG_ALL=0 keeps the
+            # latter on NCCL
             if (direct and use_peer and n in (2, 3, 4, 8) and nloc % 4 == 0 and n * nloc * 4 <= self.peer_max_bytes
-                    and self.peer_ag and (src in c.arg_bufs or os.environ.get("SPX_PEER_AG_ALL") == "1")):
+                    and self.peer_ag and (src in c.arg_bufs or self.peer_ag_all)):
                 peer(1, nloc)
                 return
             if direct:
