@@ -17,6 +17,13 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# the reference package (tactic front end) where it exists: this container's
+# source tree, or the offline install that travels to the GPU box
+# (DESIGN.md §6); appended before the backend is imported so the backend's
+# errors subclass the reference's
+for _ref in ("/root/reference/pkg/src", os.path.join(ROOT, "baseline", "_ref")):
+    if os.path.isdir(_ref) and _ref not in sys.path:
+        sys.path.append(_ref)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 TOL = 1e-5
