@@ -382,12 +382,14 @@ def main():
             s_bytes += _ew_bytes(p)
             s_ms += float(t)
         elif kind == R.K_SPLIT:
-            fused = sess.ex.plan.record_info(idx)[1] == -1
-            # pieces written (+ the fp32 read when standalone); fused: time is in the EW record
+            spath = sess.ex.plan.record_info(idx)[1]
+            fused = spath == -1
+            # pieces written (+ the fp32 read when standalone); fused (-1): time is in the EW record;
+            # batched (-2): time is in the first SPLIT record of the batch (path 2)
             s_bytes += 4.0 * p.rows * p.cols * (1 if fused else 2)
-            if not fused:
+            if spath >= 0:
                 s_ms += float(t)
-    streaming = {"bound": "hbm", "kernels": "ew_static(_split)_kernel, ew_vec/gen_kernel, split_h16_kernel",
+    streaming = {"bound": "hbm", "kernels": "ew_static(_split)_kernel, ew_vec/gen_kernel, split_h16(_batch)_kernel",
                  "achieved": s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else 0.0, "peak": hbm, "unit": "GB/s",
                  "frac": (s_bytes / (s_ms / 1e3) / 1e9 / hbm) if s_ms > 0 else 0.0,
                  "bytes_per_step": s_bytes, "ms_per_step_eager": s_ms,

@@ -78,6 +78,8 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws);
 int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch);
 void spx_gemm_h3_free(SpxGemmH3* g);
 int spx_launch_split(const spx_split_params& p, cudaStream_t s, int* nlaunch);
+int spx_launch_split_batch(const spx_split_params* const* p, int n, cudaStream_t s, int* nlaunch);
+int spx_split_batch_max(void);
 int spx_ew_split_match(const spx_ew_params& p, const spx_split_params& sp);
 int spx_launch_ew_static_split(int id, const spx_ew_params& p, const spx_split_params& sp, int which,
                                cudaStream_t s, int* nlaunch);

@@ -63,17 +63,13 @@ struct SplitArgs {
 // A cluster of H3_CL CTAs splits one 128 x 128 block (CTA rank r takes rows
 // 32r..32r+31): the block maximum is exchanged through distributed shared
 // memory, so a 1024 x 1024 operand spreads over 256 CTAs instead of 64.
-__global__ void __cluster_dims__(H3_CL, 1, 1) __launch_bounds__(256)
-split_h16_kernel(const __grid_constant__ SplitArgs a) {
+// split_block: block (by, bx) of operand `a` on device `dev`, this CTA's quarter.
+SPX_DEV void split_block(const SplitArgs& a, int bx, int by, int crank, int dev) {
   __shared__ float wmax[8];
   __shared__ float cmax[H3_CL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int dev = blockIdx.z;
-  const int crank = blockIdx.x % H3_CL;
-  const int bx = blockIdx.x / H3_CL;
-  const int r0 = blockIdx.y * HB + crank * H3_ROWS, c0 = bx * HB;
+  const int r0 = by * HB + crank * H3_ROWS, c0 = bx * HB;
   const float* src = reinterpret_cast<const float*>(a.src + (uint64_t)((int64_t)dev * a.src_dev));
-  SPX_PDL_ENTRY();
   const bool vec = ((a.src | (uint64_t)a.src_dev | (uint64_t)(a.ld * 4)) & 15) == 0 && c0 + HB <= a.cols;
   float4 v[H3_V];
   float m = 0.f;
@@ -100,7 +96,7 @@ split_h16_kernel(const __grid_constant__ SplitArgs a) {
   const int e = h3_scale_exp(m);
   const float up = h3_pow2(e);
   if (threadIdx.x == 0 && crank == 0)
-    reinterpret_cast<float*>(a.scl + (uint64_t)((int64_t)dev * a.scl_dev))[blockIdx.y * a.cb + bx] = h3_pow2(-e);
+    reinterpret_cast<float*>(a.scl + (uint64_t)((int64_t)dev * a.scl_dev))[by * a.cb + bx] = h3_pow2(-e);
   __half* hi = reinterpret_cast<__half*>(a.dst + (uint64_t)((int64_t)dev * a.dst_dev));
   __half* lo = hi + (int64_t)a.rows * a.pitch;
 #pragma unroll
@@ -109,6 +105,38 @@ split_h16_kernel(const __grid_constant__ SplitArgs a) {
     if (r >= a.rows || c >= a.cols) continue;
     h3_store4(hi, lo, (int64_t)r * a.pitch + c, v[i], up, min(4, a.cols - c));
   }
+}
+
+__global__ void __cluster_dims__(H3_CL, 1, 1) __launch_bounds__(256)
+split_h16_kernel(const __grid_constant__ SplitArgs a) {
+  SPX_PDL_ENTRY();
+  split_block(a, blockIdx.x / H3_CL, blockIdx.y, blockIdx.x % H3_CL, blockIdx.z);
+}
+
+// Several independent splits in one launch (consecutive SPX_K_SPLIT records
+// of a stream, e.g. the hoisted splits of every weight at the start of a
+// step): one grid over all their 128 x 128 blocks, so the per-launch ramp and
+// tail are paid once and the loads of one CTA overlap the stores of others.
+// Cluster c belongs to the job j with start[j] <= c < start[j + 1].
+constexpr int SPLIT_MAX_JOBS = 48;
+struct SplitBatch {
+  int n;
+  int start[SPLIT_MAX_JOBS + 1];       // first cluster of each job (start[n] = total)
+  SplitArgs job[SPLIT_MAX_JOBS];
+};
+
+__global__ void __cluster_dims__(H3_CL, 1, 1) __launch_bounds__(256)
+split_h16_batch_kernel(const __grid_constant__ SplitBatch b) {
+  const int cl = blockIdx.x / H3_CL;
+  int lo = 0, hi = b.n - 1;            // last j with start[j] <= cl
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.start[mid] <= cl) lo = mid; else hi = mid - 1;
+  }
+  const SplitArgs& a = b.job[lo];
+  const int c = cl - b.start[lo];
+  SPX_PDL_ENTRY();
+  split_block(a, c % a.cb, c / a.cb, blockIdx.x % H3_CL, blockIdx.y);
 }
 
 struct H3Args {
@@ -763,10 +791,9 @@ int spx_gemm_h3_launch(const SpxGemmH3* g, cudaStream_t s, int* nlaunch) {
   return 0;
 }
 
-int spx_launch_split(const spx_split_params& p, cudaStream_t s, int* nlaunch) {
+static int split_args(const spx_split_params& p, SplitArgs& a) {
   if (p.rows <= 0 || p.cols <= 0 || (p.pitch & 7) || p.pitch < p.cols)
     return spx_set_error("split: bad geometry %dx%d pitch %lld", p.rows, p.cols, (long long)p.pitch);
-  SplitArgs a;
   a.src = p.base + (uint64_t)(p.src_off * 4);
   a.src_dev = p.dev_stride;
   a.ld = p.ld;
@@ -778,7 +805,35 @@ int spx_launch_split(const spx_split_params& p, cudaStream_t s, int* nlaunch) {
   a.scl = p.base + (uint64_t)(p.scl_off * 4);
   a.scl_dev = p.dev_stride;
   a.cb = (p.cols + HB - 1) / HB;
+  return 0;
+}
+
+int spx_launch_split(const spx_split_params& p, cudaStream_t s, int* nlaunch) {
+  SplitArgs a;
+  if (split_args(p, a)) return -1;
   launch_split_args(a, p.ndev, s);
+  SPX_CHECK_LAUNCH();
+  if (nlaunch) ++*nlaunch;
+  return 0;
+}
+
+int spx_split_batch_max(void) { return SPLIT_MAX_JOBS; }
+
+int spx_launch_split_batch(const spx_split_params* const* p, int n, cudaStream_t s, int* nlaunch) {
+  if (n < 1 || n > SPLIT_MAX_JOBS) return spx_set_error("split batch: %d jobs (1..%d)", n, SPLIT_MAX_JOBS);
+  SplitBatch b;
+  memset(&b, 0, sizeof(b));
+  b.n = n;
+  int64_t total = 0;
+  for (int j = 0; j < n; ++j) {
+    if (p[j]->ndev != p[0]->ndev) return spx_set_error("split batch: device counts differ");
+    if (split_args(*p[j], b.job[j])) return -1;
+    b.start[j] = (int)total;
+    total += (int64_t)b.job[j].cb * ((p[j]->rows + HB - 1) / HB);
+  }
+  b.start[n] = (int)total;
+  if (total * H3_CL > INT32_MAX) return spx_set_error("split batch: grid too large");
+  spx_launch(split_h16_batch_kernel, dim3((unsigned)(total * H3_CL), p[0]->ndev, 1), dim3(256), 0, s, b);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
   return 0;

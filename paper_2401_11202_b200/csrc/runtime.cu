@@ -158,7 +158,9 @@ struct Record {
   int fused_split = -1;         // EW: the next record (SPX_K_SPLIT of output `split_out`) runs inside this launch
   int split_out = -1;
   std::vector<uint8_t> split_params;
-  bool fused = false;           // SPLIT done by the preceding EW record
+  bool fused = false;           // SPLIT done by the preceding EW record, or by an earlier SPLIT record's batch
+  std::vector<int> batch;       // SPLIT: later SPLIT records launched together with this one (path 2)
+  std::vector<spx_split_params> batch_params;   // this record's and theirs, in record order
   int stream = 0;               // 0 main, 1..SPX_SIDE_STREAMS side streams
   std::vector<int> waits;       // records on other streams to wait for
   bool signal = false;          // a later record on another stream waits for this one
@@ -199,10 +201,18 @@ static int run_record(Record& r, cudaStream_t s, int* nl) {
       return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
     case SPX_K_NCCL: return run_nccl(*reinterpret_cast<const spx_nccl_params*>(r.params.data()), s);
     case SPX_K_PEER: return spx_launch_peer(*reinterpret_cast<const spx_peer_params*>(r.params.data()), s, nl);
-    case SPX_K_SPLIT: return spx_launch_split(*reinterpret_cast<const spx_split_params*>(r.params.data()), s, nl);
+    case SPX_K_SPLIT:
+      if (!r.batch_params.empty()) {
+        std::vector<const spx_split_params*> ps;
+        for (auto& q : r.batch_params) ps.push_back(&q);
+        return spx_launch_split_batch(ps.data(), (int)ps.size(), s, nl);
+      }
+      return spx_launch_split(*reinterpret_cast<const spx_split_params*>(r.params.data()), s, nl);
   }
   return spx_set_error("unknown record kind %d", r.kind);
 }
+
+
 
 static size_t params_size(int kind) {
   switch (kind) {
@@ -404,6 +414,28 @@ int spx_plan_finalize(uint64_t plan) {
     a.split_params = b.params;
     b.fused = true;
     b.path = -1;                 // reported by spx_plan_record_info: runs inside record i
+  }
+  // consecutive standalone splits on one stream (the hoisted splits of the
+  // weights, ...): one batched launch at the first (gemm_h3.cu split_h16_batch_kernel)
+  const char* be = getenv("SPX_SPLIT_BATCH");
+  const int batch = be ? atoi(be) != 0 : 1;
+  for (size_t i = 0; batch && i < P->recs.size(); ++i) {
+    Record& a = P->recs[i];
+    if (a.kind != SPX_K_SPLIT || a.fused) continue;
+    size_t j = i + 1;
+    for (; j < P->recs.size() && (int)a.batch.size() + 1 < spx_split_batch_max(); ++j) {
+      Record& b = P->recs[j];
+      if (b.kind != SPX_K_SPLIT || b.fused || b.stream != a.stream || !b.waits.empty()) break;
+      a.batch.push_back((int)j);
+      b.fused = true;
+      b.path = -2;               // reported by spx_plan_record_info: runs inside the batch of record i
+    }
+    if (!a.batch.empty()) {
+      a.path = 2;
+      a.batch_params.push_back(*reinterpret_cast<const spx_split_params*>(a.params.data()));
+      for (int k : a.batch) a.batch_params.push_back(*reinterpret_cast<const spx_split_params*>(P->recs[k].params.data()));
+    }
+    i = j - 1;
   }
   for (int k = 0; k <= SPX_SIDE_STREAMS; ++k)
     if (h3need[k] && !P->h3ws[k]) SPX_CUDA(cudaMalloc(&P->h3ws[k], (size_t)h3need[k]));

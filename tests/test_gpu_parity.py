@@ -411,3 +411,48 @@ def test_gemm_inkernel_splitk(M, N, K, monkeypatch):
     sess.close()
     assert np.all(np.isfinite(a)) and O.relative_error(a, want) < TOL
     np.testing.assert_array_equal(a, b)
+
+
+@requires_gpu
+@pytest.mark.gpu
+def test_split_batch_bitexact(monkeypatch):
+    """Consecutive standalone operand splits (here the hoisted splits of the
+    batch and three weights, ragged sizes) run as one split_h16_batch_kernel
+    launch; the GEMM results are bit-identical to one launch per split and
+    within the fp32 bar of the oracle."""
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.session import Session
+    text = """func @main(%x: tensor<1024x520xf32>, %w1: tensor<520x384xf32>, %w2: tensor<384x640xf32>, %w3: tensor<640x328xf32>) -> tensor<1024x328xf32> {
+  %h1 = matmul %x, %w1 : tensor<1024x384xf32>
+  %h2 = matmul %h1, %w2 : tensor<1024x640xf32>
+  %h3 = matmul %h2, %w3 : tensor<1024x328xf32>
+  return %h3
+}
+"""
+    m = pkg.parse_module(text)
+    rng = np.random.default_rng(7)
+    ins = {"x": rng.standard_normal((1024, 520)).astype(np.float32),
+           "w1": (rng.standard_normal((520, 384)) * 1e-3).astype(np.float32),
+           "w2": (rng.standard_normal((384, 640)) * 30).astype(np.float32),
+           "w3": rng.standard_normal((640, 328)).astype(np.float32)}
+    monkeypatch.setenv("SPX_SPLITK_F", "100000")      # no split-K: every GEMM on the 3xFP16 path
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SPX_SPLIT_BATCH", mode)
+        sess = Session(m)
+        sess.load(ins)
+        sess.capture()
+        paths = [sess.ex.plan.record_info(i)[1] for i, (k, _) in enumerate(sess.ex._records) if k == R.K_SPLIT]
+        if mode == "1":
+            assert 2 in paths and paths.count(-2) >= 3, paths
+        else:
+            assert 2 not in paths and -2 not in paths, paths
+        sess.step()
+        sess.sync()
+        outs[mode] = sess.results()[0][0].copy()
+        sess.close()
+    assert np.all(np.isfinite(outs["1"]))
+    np.testing.assert_array_equal(outs["1"], outs["0"])
+    want = O.interpret(m, ins)[0]
+    assert O.relative_error(outs["1"], want) < TOL

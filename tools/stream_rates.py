@@ -6,7 +6,8 @@ launch list (tools/profile_step.py under `ncu --metrics gpu__time_duration.sum
 
 Bytes per record are algorithmic: every input once (broadcast operands at their
 own size), every output, and the fp16 pieces (4 B per element) a split writes
--- standalone splits also read their fp32 source.  ncu serialises kernels and
+-- standalone splits also read their fp32 source.  A batched split launch
+(split_h16_batch_kernel) carries the bytes of every record it runs.  ncu serialises kernels and
 flushes caches between them (cold L2), so these are DRAM-bound rates.
 """
 import collections
@@ -60,12 +61,29 @@ def main(path, program="c2_tf8_dense", steps=2):
                 and b.ld == b.cols and b.rows * b.cols == a.numel and b.cols % 4 == 0
                 and any(a.out_off[j] == b.src_off for j in range(a.n_out))):
             fused.add(i + 1)
+    # ... and runs consecutive standalone SPLITs of one stream as one batched launch
+    wt = {i: w for i, _, w in ex.sched}
+    batched = {}                      # member -> leader
+    i = 0
+    while i < len(recs):
+        if recs[i][0] == R.K_SPLIT and i not in fused:
+            j = i + 1
+            while (j < len(recs) and recs[j][0] == R.K_SPLIT and j not in fused and st.get(j, 0) == st.get(i, 0)
+                   and not wt.get(j) and j - i < 48):
+                batched[j] = i
+                j += 1
+            i = j
+        else:
+            i += 1
     L = launches(path)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     pos = 0
     for _ in range(steps):
         for i, (k, q) in enumerate(recs):
             if k == R.K_SPLIT and i in fused:
+                continue
+            if k == R.K_SPLIT and i in batched:
+                agg[last_split][2] += 8 * q.rows * q.cols
                 continue
             if k == R.K_REDUCE:
                 while pos < len(L) and L[pos][0].startswith("reduce"):
@@ -80,6 +98,7 @@ def main(path, program="c2_tf8_dense", steps=2):
                 a = agg[name]
                 a[0] += 1; a[1] += us; a[2] += b
             elif k == R.K_SPLIT:
+                last_split = name
                 a = agg[name]
                 a[0] += 1; a[1] += us; a[2] += 8 * q.rows * q.cols
     tb = tt = 0.0
