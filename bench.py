@@ -188,6 +188,9 @@ def main():
     if world != n and not (world == 1 and n == 1):
         raise SystemExit(f"--gpus {n} needs torchrun with {n} processes (WORLD_SIZE={world})")
     wl = WORKLOADS[args.config]
+    wl_env = wl.get("env", {}).get(n, {})
+    for k, v in wl_env.items():
+        os.environ.setdefault(k, v)        # before any plan is built; an explicit setting wins
     prog = load_program(args.program or wl["programs"][n])
     batch = prog.batch
     base = prog.dense
@@ -198,6 +201,8 @@ def main():
               ("none (unpartitioned)" if n == 1 else f"mesh {mesh}, one device per GPU"),
               "l2": "working set > 126 MB L2 (params+momenta alone exceed it); no flush needed",
               "inputs": f"synthetic N(0, {wl['scale']}^2) float32 (random_inputs generator, seed 0)"}
+    if wl_env:
+        config["env"] = {k: os.environ[k] for k in wl_env}
     dtype = "f32"
 
     if args.impl == "reference":
