@@ -53,6 +53,7 @@ class Executable:
         self.dry = dry
         self.device = None if dry else (device or R.Device(0))
         self.ndev = len(self.comp.devices)
+        self.mesh_size = module.mesh.device_count if getattr(module, "mesh", None) is not None else 1
         self.gemm_path = gemm_path
         self.comms = comms or {}
         import os
@@ -503,7 +504,11 @@ class Executable:
         for i, k in enumerate(ks):
             if k.kind == "split" and k.data["src"][0] in args:
                 side[i] = self.COMPUTE
-        if os.environ.get("SPX_CONCURRENT_GEMM", "1") != "0":
+        # side-stream GEMMs (whole-SM CTAs) only below 4 ranks: with spinning
+        # peer kernels on two streams they can close a cross-rank residency
+        # cycle (known issue); SPX_CONCURRENT_GEMM overrides
+        cg_default = "0" if c.comm_mode == "nccl" and self.mesh_size >= 4 else "1"
+        if os.environ.get("SPX_CONCURRENT_GEMM", cg_default) != "0":
             for i in reversed(range(len(ks))):
                 # in-kernel split-K GEMMs share one workspace: main stream only
                 if (ks[i].kind in ("gemm", "split") and not ks[i].data.get("sk_inkernel")

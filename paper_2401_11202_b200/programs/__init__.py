@@ -89,11 +89,7 @@ WORKLOADS = {
                                        8: "c3_tf32_bpz3_B8"}},
     "c4": {"desc": "unet_train(batch=128, 32x32, channels 64/256/512) U-Net analog (tools/unet_model.py), BP+Z2",
            "scale": 0.05, "programs": {1: "c4_unet_dense", 2: "c4_unet_bpz2_B2", 4: "c4_unet_bpz2_B4",
-                                       8: "c4_unet_bpz2_B8"},
-           # N>=4: no GEMMs on the compute side stream, so no whole-SM kernel can wait behind a
-           # spinning peer kernel of another stream (DESIGN.md §5 "Known issue": the
-           # cross-stream forward-progress cycle seen on C4 at N=4)
-           "env": {4: {"SPX_CONCURRENT_GEMM": "0"}, 8: {"SPX_CONCURRENT_GEMM": "0"}}},
+                                       8: "c4_unet_bpz2_B8"}},
     "c5": {"desc": "mini_transformer_train(blocks=8, batch=2048, d_model=1024, d_ff=4096), BP+MP+Z3+EMB",
            "scale": 0.02, "programs": {1: "c2_tf8_dense", 2: "c5_tf8_bpz3_B2", 4: "c5_tf8_bpmpz3_B2M2",
                                        8: "c5_tf8_bpmpz3emb_B2M2E2"}},

@@ -166,19 +166,17 @@ def test_gemm_epilogue_fusion_sim(epi, monkeypatch):
         assert relative_error(g, w) < TOL
 
 
-def test_c4_multi_gpu_env_keeps_gemms_off_side_streams(monkeypatch):
-    """C4 at N>=4 runs with SPX_CONCURRENT_GEMM=0 (DESIGN.md §5 known issue):
-    no whole-SM GEMM on a side stream, collectives only on the main and
-    collective streams."""
+def test_multi_gpu_keeps_gemms_off_side_streams_from_4_ranks(monkeypatch):
+    """From 4 ranks the NCCL-mode schedule puts no whole-SM GEMM on a side
+    stream (DESIGN.md §5 known issue); below 4 it does (overlap pays there);
+    collectives stay on the main and collective streams."""
     from record_sim import _dry_comms
     from paper_2401_11202_b200.executable import Executable
-    from paper_2401_11202_b200.programs import WORKLOADS, load_program
-    env = WORKLOADS["c4"]["env"][4]
-    assert env == {"SPX_CONCURRENT_GEMM": "0"}
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    p = load_program("c4_unet_bpz2_B4")
-    ex = Executable(p.local, devices=[0], comm_mode="nccl", dry=True, comm_factory=lambda e: _dry_comms(e, True))
-    streams = {(k.kind, ex.stream_of.get(i, 0)) for i, k in enumerate(ex.comp.kernels)}
-    assert ("gemm", ex.COMPUTE) not in streams
-    assert {s for kind, s in streams if kind == "coll"} <= {ex.MAIN, ex.COMM}
+    from paper_2401_11202_b200.programs import load_program
+    monkeypatch.delenv("SPX_CONCURRENT_GEMM", raising=False)
+    for name, side_gemm in (("c4_unet_bpz2_B4", False), ("c2_tf8_bpmp_B2M2", False), ("c2_tf8_bp_B2", True)):
+        p = load_program(name)
+        ex = Executable(p.local, devices=[0], comm_mode="nccl", dry=True, comm_factory=lambda e: _dry_comms(e, True))
+        streams = {(k.kind, ex.stream_of.get(i, 0)) for i, k in enumerate(ex.comp.kernels)}
+        assert (("gemm", ex.COMPUTE) in streams) == side_gemm, name
+        assert {s for kind, s in streams if kind == "coll"} <= {ex.MAIN, ex.COMM}, name
