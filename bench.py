@@ -1,6 +1,6 @@
 """Benchmark: partitioned fwd+bwd+momentum-SGD step throughput on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
 Metric (BASELINE.json): "Partitioned fwd+bwd samples/s at 1/2/4/8 B200; %
 of tensor-core/HBM roofline".  One STEP = one execution of the localized
@@ -11,11 +11,22 @@ unpartitioned module (the reference's 1-device semantics); N>1 runs
 the partitioned program one mesh device per GPU (torchrun), collectives over
 NCCL.  Scaling is STRONG (global batch fixed).
 
+The default workload is C3 (BASELINE.json configs[2]: 32 transformer blocks,
+d_model 2048, d_ff 8192, batch 8192, BP+Z3 on B:8 at 8 GPUs), the largest
+configuration that fits one B200 (configs[1], C2, is quoted on a 2x4 mesh).
+
 `value` is device-timed (CUDA events, max over ranks) with every input
-resident in HBM; `e2e` repeats the measurement through the Session API with
-each step's batch (x, y) copied host->device from pinned memory and the loss
-read back device->host inside the timed region.  `--impl reference` times the
-reference's CPU evaluator (the oracle restatement, numpy) on this host.
+resident in HBM (the compiled step replayed as one CUDA graph).  `e2e` is
+the same metric through the drop-in call a user of the reference makes --
+`interpret(module, inputs)` at 1 GPU (interp.py:117-132; `spmd_interpret` is
+the same call with a mesh), `Session.call` per rank at N GPUs -- with EVERY
+input (parameters, momenta, batch) copied in from host arrays and EVERY
+result copied back to new host arrays inside the timed region; the compiled
+plan comes from the plan cache, as on any repeated call.  `step_roofline`
+is T_roof / T_measured with T_roof from the program's IR op by op
+(roofline.py); `roofline` is the dominant kernel's.
+`--impl reference` times the reference's CPU evaluator (the oracle
+restatement, numpy) on this host.
 """
 from __future__ import annotations
 
@@ -153,21 +164,80 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def time_reference(prog, n, inputs, steps, warmup):
-    """The reference evaluator (oracle restatement; numpy on host cores)."""
+def reference_step(wl, n, prog):
+    """One step of the reference's CPU evaluator on this workload (the oracle
+    restatement, bit-identical to the reference: tests/test_oracle_configs.py):
+    `interpret` of the dense module at 1 GPU, `spmd_interpret` of the
+    partitioned one at N.  Where the evaluator cannot hold the model (C3: ~11 GB
+    per block) the step time is extrapolated from 1- and 2-block
+    programs at full width, t(1) + (B-1) (t(2) - t(1)).
+    Returns (step seconds, sample description)."""
     from oracle import spmd_oracle as O
-    if n == 1:
-        fn = lambda: O.interpret(prog.dense, inputs)
-    else:
-        fn = lambda: O.spmd_interpret(prog.local, prog.sharding, inputs)
-    for _ in range(warmup):
-        fn()
-    ts = []
-    for _ in range(steps):
+    from paper_2401_11202_b200.programs import load_program, synthetic_inputs
+
+    def run(p):
+        ins = synthetic_inputs(p.dense, seed=0, scale=wl["scale"])
+        fn = (lambda: O.interpret(p.dense, ins)) if n == 1 else (lambda: O.spmd_interpret(p.local, p.sharding, ins))
         t0 = time.perf_counter()
         fn()
-        ts.append(time.perf_counter() - t0)
-    return float(np.median(ts)), ts
+        return time.perf_counter() - t0
+
+    what = "interpret" if n == 1 else "spmd_interpret"
+    ext = wl.get("cpu_extrap")
+    if ext and n in ext:
+        b = ext["blocks"]
+        p1, p2 = (load_program(x) for x in ext[n])
+        t1, t2 = run(p1), run(p2)
+        return t1 + (b - 1) * (t2 - t1), (f"{what} of the 1- and 2-block programs at full width ({p1.name}: "
+                                         f"{t1:.2f} s, {p2.name}: {t2:.2f} s) extrapolated to {b} blocks as "
+                                         f"t(1) + {b - 1} (t(2) - t(1)) (BASELINE.md §2; the full model does not "
+                                         f"fit the CPU evaluator, SURVEY F6)")
+    t = run(prog)
+    return t, f"one full step of {prog.name} through {what}"
+
+
+def e2e_call(sess, base, inputs, n, dist, budget_s, max_steps, batch):
+    """The metric through the call a user makes, with every input copied in
+    from host arrays and every result copied out to new host arrays each
+    step.  1 GPU: the drop-in `interpret(module, inputs)` (the session is
+    closed first; the call compiles once into the plan cache and replays the
+    captured step).  N GPUs: `Session.call(inputs)` on every rank (the same
+    data movement for the rank's mesh device), wall time max over ranks."""
+    import paper_2401_11202_b200 as pkg
+    if n == 1:
+        sess.close()
+        fn = lambda: pkg.interpret(base, inputs)
+        what = "paper_2401_11202_b200.interpret(module, host inputs) -- the drop-in for interp.interpret"
+    else:
+        fn = lambda: sess.call(inputs)
+        what = "Session.call(host inputs) on every rank (shard, copy in, replay, copy out)"
+    out = fn()                     # compile (1 GPU: into the plan cache) + eager run + capture
+    out = fn()                     # replay
+    res = out if n == 1 else [r[0] for r in out]
+    h2d = sum(np.asarray(a).nbytes for a in sess.local_inputs(inputs)[0].values()) if n > 1 else \
+        sum(np.asarray(a).nbytes for a in inputs.values())
+    d2h = sum(r.nbytes for r in res)
+    barrier(dist)
+    t0 = time.perf_counter()
+    fn()
+    one = max_over_ranks(dist, time.perf_counter() - t0)
+    k = int(max(3, min(max_steps, budget_s / max(one, 1e-6))))
+    k = int(max_over_ranks(dist, k))
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(k):
+        out = fn()
+    wall = max_over_ranks(dist, time.perf_counter() - t0)
+    res = out if n == 1 else [r[0] for r in out]
+    finite = bool(all(np.all(np.isfinite(r)) for r in res))
+    if n > 1:
+        sess.close()
+    return {"value": batch / (wall / k), "unit": "samples/s", "steps": k, "ms_per_step": wall / k * 1e3,
+            "h2d_bytes_per_step": int(sum_over_ranks(dist, h2d)), "d2h_bytes_per_step": int(sum_over_ranks(dist, d2h)),
+            "outputs_finite": finite,
+            "note": f"{what}: every parameter, momentum and batch array copied in from pageable host numpy arrays "
+                    f"and every result copied out to new host arrays inside the timed region (host wall clock, "
+                    f"max over ranks); pageable copies, no pinned staging"}
 
 
 def main():
@@ -175,7 +245,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--e2e-seconds", type=float, default=40.0, help="time budget of the plugin-call e2e loop")
     ap.add_argument("--program", default=None, help="override the config's program for this GPU count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -208,20 +279,23 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        inputs = synthetic_inputs(base, seed=0, scale=wl["scale"])
         steps = max(1, min(args.steps, 3))
         warm = min(args.warmup, 1)
-        med, ts = time_reference(prog, n, inputs, steps, warm)
+        for _ in range(warm):
+            reference_step(wl, n, prog)
+        ts, sample = [], ""
+        for _ in range(steps):
+            t, sample = reference_step(wl, n, prog)
+            ts.append(t)
+        med = float(np.median(ts))
         v = batch / med
         line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": n, "steps": steps,
                 "warmup": warm, "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config,
                 "impl": "reference",
                 "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cpu_threads(), "kind": "port",
-                                 "sample": f"{steps} full steps of the workload through the oracle "
-                                           f"restatement of the reference evaluator ("
-                                           f"{'interpret' if n == 1 else 'spmd_interpret'}); numpy "
-                                           f"{np.__version__}, BLAS threads = host cores"},
+                                 "sample": f"median of {steps} steps, each {sample}; oracle restatement of the "
+                                           f"reference evaluator, numpy {np.__version__}, BLAS threads = host cores"},
                 "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -269,43 +343,10 @@ def main():
     ms_step = ms_total / args.steps
     value = batch / (ms_step / 1e3)
 
-    # ---- end to end: batch H2D from pinned host memory + loss D2H, per step
-    f = sess.func
-    bx = sess.local_inputs(inputs)[0]
-    pin = {nm: dev.pinned(bx[nm].shape) for nm in ("x", "y") if nm in bx}
-    for nm, arr in pin.items():
-        arr[...] = bx[nm]
-    loss_pin = dev.pinned((max(1, args.steps),))
-    loss_addr = sess.result_addr(0)
-    h2d = sum(a.nbytes for a in pin.values())
-    import ctypes
-    # warm the input pipeline (staging slots, copy stream) outside the timed region
-    sess.feed(pin)
-    sess.step()
-    sess.sync()
-    barrier(dist)
-    sess.sync()
-    t0 = time.perf_counter()
-    dev.record(e0)
-    # each step's batch is copied inside the timed region; the copy of batch
-    # i+1 overlaps step i (Session.feed: copy stream + staging slots)
-    # every step's loss is read back to the host (async D2H into a pinned
-    # slot per step); the host waits once at the end instead of every step
-    sess.feed(pin)
-    for i in range(args.steps):
-        if i + 1 < args.steps:
-            sess.feed(pin)
-        sess.step()
-        R.call(dev.lib.spx_memcpy_d2h, loss_pin.ctypes.data + 4 * i, loss_addr, 4, dev.stream)
-    sess.sync()
-    dev.record(e1)
-    sess.sync()
-    wall = time.perf_counter() - t0
-    e2e_ms = max_over_ranks(dist, max(dev.elapsed_ms(e0, e1), wall * 1e3))
-    e2e_value = batch / (e2e_ms / args.steps / 1e3)
-    h2d_total = sum_over_ranks(dist, h2d)
-    d2h_total = sum_over_ranks(dist, 4)
-    loss = float(loss_pin[args.steps - 1])
+    loss_arr = np.empty(1, np.float32)
+    dev.d2h(loss_arr, sess.result_addr(0))
+    dev.sync()
+    loss = float(loss_arr[0])
 
     # ---- per-record profile (eager, events between records) for the roofline
     rec_ms = sess.ex.plan.profile()
@@ -338,8 +379,11 @@ def main():
     sust = bf16_sustained()       # MEASURED_PEAKS: cuBLAS bf16 back to back for 4 s (the step's regime)
     # DRAM traffic of one GEMM launch from the committed `ncu --set full` capture
     traffic, traffic_note = None, None
+    cap_file = next((f for f in (f"r02_ncu_full_gemm_{args.config}_n1.json", f"r01_ncu_full_gemm_{args.config}_n1.json",
+                                 "r01_ncu_full_gemm_c2_n1.json") if os.path.exists(os.path.join(ROOT, "profiles", f))),
+                    "r01_ncu_full_gemm_c2_n1.json")
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_gemm_c2_n1.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", cap_file)) as fh:
             cap = json.load(fh)[0]
 
         def _mb(v):
@@ -347,9 +391,10 @@ def main():
             return float(x) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
         traffic = _mb(cap["dram__bytes_read.sum"]) + _mb(cap["dram__bytes_write.sum"])
         traffic_note = (f"dram read+write bytes of one {cap['kernel'].split('(')[0].replace('void ', '')} launch "
-                        f"(C2 2048x4096x1024, {cap['gpu__time_duration.sum']}) from profiles/r01_ncu_full_gemm_c2_n1.json; "
-                        f"algorithmic: fp16 pieces of A 8.4 MB + B 16.8 MB read, C 33.6 MB written (C stays in L2 "
-                        f"for its consumer, so DRAM sees the operand reads only)")
+                        f"({cap.get('shape', 'C2 2048x4096x1024')}, {cap['gpu__time_duration.sum']}) from "
+                        f"profiles/{cap_file}; " + cap.get("algorithmic_note",
+                        "algorithmic: fp16 pieces of A 8.4 MB + B 16.8 MB read, C 33.6 MB written (C stays in L2 "
+                        "for its consumer, so DRAM sees the operand reads only)"))
     except (OSError, KeyError, ValueError, IndexError):
         pass
     peak_eff = tensor_flops / (ideal_ms / 1e3) / 1e12 if ideal_ms > 0 else bf16
@@ -406,31 +451,46 @@ def main():
             json.dump({"records": [[int(k), float(t)] for (k, _), t in zip(recs, rec_ms)],
                        "class_ms": cls_ms}, fh, indent=0)
 
+    # ---- executed work (runtime counters over every run above) vs the simulator
+    work = sess.ex.work_report()
+    # ---- step-level roofline from the program's IR (per device)
+    from paper_2401_11202_b200.roofline import step_roofline
+    sr = step_roofline(base if n == 1 else prog.local, bf16_tflops=bf16, hbm_gbs=hbm)
+    step_roof = {"t_roof_ms": sr["t_roof_s"] * 1e3, "t_measured_ms": ms_step,
+                 "frac": sr["t_roof_s"] * 1e3 / ms_step, "bound": sr["bound"],
+                 "t_gemm_ms": sr["t_gemm_s"] * 1e3, "t_stream_ms": sr["t_stream_s"] * 1e3,
+                 "t_nvlink_ms": sr["t_nvlink_s"] * 1e3, "hbm_bytes": sr["hbm_bytes"], "flops": sr["flops"],
+                 "nvlink_bytes": sr["nvlink_bytes"],
+                 "note": "T_roof = max(sum over IR ops of max(F/P, B/BW_hbm), B_nvl/BW_nvl) per device (SURVEY "
+                         "§8(d), paper_2401_11202_b200/roofline.py): F by the simulator's convention (sim.py:86-100), "
+                         "matmuls at the measured bf16 peak / 3 (3 fp16 MMAs per fp32 FLOP), B = operand data + "
+                         "result bytes of each matmul/elementwise/reduce op unfused, B_nvl = ring bytes "
+                         "(sim.py:114-123) at 900 GB/s; frac = T_roof / measured step"}
+
+    # ---- end to end through the drop-in call: every input from host arrays,
+    # every result back to new host arrays, per step
+    e2e = e2e_call(sess, base, inputs, n, dist, args.e2e_seconds, args.steps, batch)
+
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
-        med, ts = time_reference(prog, n, inputs, 2, 0)
-        cpu = {"value": batch / med, "unit": "samples/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"2 full steps (median {med:.2f} s) of the same workload through the oracle "
-                         f"restatement of the reference's dense interpreter (interp.py:117-132), numpy "
-                         f"{np.__version__}, BLAS on all host cores"}
+        t, sample = reference_step(wl, n, prog)
+        cpu = {"value": batch / t, "unit": "samples/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{sample}: oracle restatement of the reference evaluator (bit-identical to it, "
+                         f"tests/test_oracle_configs.py), numpy {np.__version__}, BLAS on all host cores"}
 
-    counts = sess.ex.comp.counts
+    counts = work["collectives"]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": config, "roofline": roofline, "streaming_roofline": streaming, "cpu_baseline": cpu,
-                "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_total),
-                        "d2h_bytes_per_step": int(d2h_total),
-                        "note": "Session.feed + Session.step: every step's batch (x, y) H2D from pinned memory (the copy of batch i+1 overlaps step i) and the "
-                                "loss D2H each step (async into a pinned slot per step), one host wait at the end"},
+                "e2e": e2e, "step_roofline": step_roof,
                 "gpu_launches": int(launches_per_step * args.steps),
                 "launches_per_step": int(launches_per_step),
                 "clocks": clk.summary(), "loss": loss, "loss_finite": bool(np.isfinite(loss)),
                 "collectives_per_step": counts,
-                "flops_per_device_step": sess.ex.comp.flops}
+                "flops_per_device_step": work["flops"]}
         print(json.dumps(line), flush=True)
-    sess.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

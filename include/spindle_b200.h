@@ -240,6 +240,12 @@ int spx_memcpy_d2d(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream);
 int spx_memset(uint64_t dst, int value, uint64_t bytes, uint64_t stream);
 int spx_host_alloc(uint64_t bytes, void** out_ptr); /* pinned host memory */
 int spx_host_free(void* ptr);
+/* page-lock / unlock an existing host range (cudaHostRegister) so copies
+ * from/to it run as direct DMA at full link rate */
+int spx_host_register(void* ptr, uint64_t bytes);
+int spx_host_unregister(void* ptr);
+/* host memcpy split over `threads` threads (staging into pinned buffers) */
+int spx_host_copy(void* dst, const void* src, uint64_t bytes, int threads);
 int spx_stream_create(uint64_t* out_stream);
 int spx_stream_sync(uint64_t stream);
 int spx_stream_destroy(uint64_t stream);
@@ -281,6 +287,34 @@ int spx_event_destroy(uint64_t event);
 
 /* per-record timing of one eager run (ms per record, length = record count) */
 int spx_plan_profile(uint64_t plan, uint64_t stream, float* out_ms, int n);
+
+/* ---- executed-work accounting ---------------------------------------------
+ * The reference's simulator predicts, per device, the collectives of a
+ * program (`collective_counts`, spmd.py:264-271) and its FLOPs
+ * (`simulate().compute_flops`, sim.py:86-100, :209-229).  The runtime counts
+ * what it actually ISSUES: every eager run, profile run and graph replay adds
+ * the logical collectives and FLOPs of the records it launched (a replay adds
+ * what was captured into the graph).  A record's tag says which logical
+ * collective it executes (one record per IR collective; relayouts around an
+ * NCCL call are untagged) and whether it is internal work that the IR does
+ * not contain (split-K workspace reductions: no FLOPs).  FLOPs follow the
+ * simulator's convention from the record parameters: GEMM 2MNK, elementwise
+ * one per arithmetic instruction per element, reduce one per input element
+ * (+ the fused operand expression), summed over the record's virtual
+ * devices. */
+enum spx_tag_bits {
+  SPX_TAG_COLL_MASK = 0x7,        /* 0 none, 1 all_gather, 2 all_reduce, 3 reduce_scatter, 4 all_to_all */
+  SPX_TAG_INTERNAL = 0x100        /* no IR FLOPs (split-K partial reduction) */
+};
+int spx_plan_tag(uint64_t plan, int index, int tag);
+typedef struct {
+  int64_t runs;                   /* eager runs + graph replays + profile runs */
+  int64_t coll[4];                /* logical collectives issued: all_gather, all_reduce, reduce_scatter, all_to_all */
+  double flops;                   /* FLOPs issued, summed over the plan's virtual devices */
+  int64_t launches;               /* kernel launches issued (graph replays count the captured launches) */
+} spx_exec_stats;
+int spx_plan_exec_stats(uint64_t plan, spx_exec_stats* out);
+int spx_plan_reset_stats(uint64_t plan);
 
 #ifdef __cplusplus
 }

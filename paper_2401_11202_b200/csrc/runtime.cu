@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 #include "common.cuh"
 
@@ -161,6 +162,8 @@ struct Record {
   bool fused = false;           // SPLIT done by the preceding EW record, or by an earlier SPLIT record's batch
   std::vector<int> batch;       // SPLIT: later SPLIT records launched together with this one (path 2)
   std::vector<spx_split_params> batch_params;   // this record's and theirs, in record order
+  int tag = 0;                  // spx_tag_bits: logical collective executed / internal work
+  double flops = 0;             // simulator-convention FLOPs of one launch (all virtual devices)
   int stream = 0;               // 0 main, 1..SPX_SIDE_STREAMS side streams
   std::vector<int> waits;       // records on other streams to wait for
   bool signal = false;          // a later record on another stream waits for this one
@@ -180,7 +183,48 @@ struct Plan {
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
   void* h3ws[SPX_SIDE_STREAMS + 1] = {};   // fp16-pieces workspace per stream (GEMMs of a stream run in order)
+  spx_exec_stats stats = {};               // issued so far
+  spx_exec_stats graph_tally = {};         // issued into the captured graph (added per replay)
 };
+
+// work of the records issued since `tally` was reset
+static void tally_record(const Record& r, spx_exec_stats* t) {
+  if (r.fused) return;
+  const int c = r.tag & SPX_TAG_COLL_MASK;
+  if (c >= 1 && c <= 4) t->coll[c - 1] += 1;
+  if (!(r.tag & SPX_TAG_INTERNAL)) t->flops += r.flops;
+}
+
+static bool arith_op(int op) {
+  return op == SPX_OP_ADD || op == SPX_OP_MUL || op == SPX_OP_NEG || op == SPX_OP_EXP || op == SPX_OP_MAX ||
+         op == SPX_OP_ADDI || op == SPX_OP_MULI || op == SPX_OP_IADD || op == SPX_OP_IMUL;
+}
+
+static double ew_flops(const spx_ew_params& p) {
+  int n = 0;
+  for (int i = 0; i < p.n_prog; ++i) n += arith_op(p.prog[i].op);
+  return (double)n * (double)p.numel * (double)p.ndev;
+}
+
+// simulator convention (sim.py:86-100): matmul 2mkn, add/mul/neg/exp one per
+// result element, reduce one per input element
+static double record_flops(const Record& r) {
+  switch (r.kind) {
+    case SPX_K_GEMM: {
+      const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
+      // + the fused elementwise consumer's operations per output element
+      const int epi = g.epi == SPX_EPI_ADD ? 1 : g.epi == SPX_EPI_SQUARE ? 1 : g.epi == SPX_EPI_MULSCALE ? 2
+                    : g.epi == SPX_EPI_MOMENTUM ? 5 : 0;
+      return (2.0 * g.K + epi) * g.M * (double)g.N * g.ndev;
+    }
+    case SPX_K_EW: return ew_flops(*reinterpret_cast<const spx_ew_params*>(r.params.data()));
+    case SPX_K_REDUCE: {
+      const spx_reduce_params& q = *reinterpret_cast<const spx_reduce_params*>(r.params.data());
+      return ew_flops(q.x) + (double)q.x.numel * q.x.ndev;
+    }
+  }
+  return 0.0;
+}
 
 static int run_record(Record& r, cudaStream_t s, int* nl) {
   if (r.fused) return 0;
@@ -282,6 +326,30 @@ int spx_host_free(void* p) {
   SPX_CUDA(cudaFreeHost(p));
   return 0;
 }
+int spx_host_register(void* p, uint64_t bytes) {
+  SPX_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return 0;
+}
+int spx_host_unregister(void* p) {
+  SPX_CUDA(cudaHostUnregister(p));
+  return 0;
+}
+int spx_host_copy(void* dst, const void* src, uint64_t bytes, int threads) {
+  if (threads <= 1 || bytes < (8u << 20)) {
+    memcpy(dst, src, bytes);
+    return 0;
+  }
+  std::vector<std::thread> ts;
+  const uint64_t per = (bytes / threads + 4095) & ~uint64_t(4095);
+  for (int t = 0; t < threads; ++t) {
+    const uint64_t o = per * t;
+    if (o >= bytes) break;
+    const uint64_t n = o + per > bytes ? bytes - o : per;
+    ts.emplace_back([=] { memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, n); });
+  }
+  for (auto& t : ts) t.join();
+  return 0;
+}
 int spx_stream_create(uint64_t* out) {
   cudaStream_t s;
   SPX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -376,6 +444,7 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
     if (g.splits > 1 && r.path != 1) return spx_set_error("gemm %dx%dx%d: split-K needs the tcgen05 path", g.M, g.N, g.K);
     if (g.epi != SPX_EPI_NONE && r.path != 1) return spx_set_error("gemm %dx%dx%d: fused epilogue needs the tcgen05 path", g.M, g.N, g.K);
   }
+  r.flops = record_flops(r);
   P->recs.push_back(std::move(r));
   return 0;
 }
@@ -459,10 +528,15 @@ int spx_plan_finalize(uint64_t plan) {
 // Issue every record: main-stream records on `s`, side-stream records on the
 // plan's side stream, cross-stream order through events (fork at the start,
 // join at the end, so the whole plan is one unit on `s` -- also under capture).
-static int issue_all(Plan* P, cudaStream_t s, int* nl) {
+static int issue_all(Plan* P, cudaStream_t s, int* nl, spx_exec_stats* t) {
+  *t = spx_exec_stats{};
+  t->runs = 1;
   if (!P->two_streams) {
-    for (auto& r : P->recs)
+    for (auto& r : P->recs) {
       if (run_record(r, s, nl)) return -1;
+      tally_record(r, t);
+    }
+    t->launches = *nl;
     return 0;
   }
   SPX_CUDA(cudaEventRecord(P->fork, s));
@@ -472,6 +546,7 @@ static int issue_all(Plan* P, cudaStream_t s, int* nl) {
     cudaStream_t rs = r.stream ? P->side[r.stream] : s;
     for (int w : r.waits) SPX_CUDA(cudaStreamWaitEvent(rs, P->recs[w].done, 0));
     if (run_record(r, rs, nl)) return -1;
+    tally_record(r, t);
     if (r.signal) SPX_CUDA(cudaEventRecord(r.done, rs));
   }
   for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
@@ -479,7 +554,15 @@ static int issue_all(Plan* P, cudaStream_t s, int* nl) {
     SPX_CUDA(cudaEventRecord(P->join[k], P->side[k]));
     SPX_CUDA(cudaStreamWaitEvent(s, P->join[k], 0));
   }
+  t->launches = *nl;
   return 0;
+}
+
+static void stats_add(spx_exec_stats* a, const spx_exec_stats& b) {
+  a->runs += b.runs;
+  for (int k = 0; k < 4; ++k) a->coll[k] += b.coll[k];
+  a->flops += b.flops;
+  a->launches += b.launches;
 }
 
 int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, int n_waits) {
@@ -508,7 +591,9 @@ int spx_plan_run(uint64_t plan, uint64_t stream) {
   if (!P->finalized && spx_plan_finalize(plan)) return -1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int nl = 0;
-  if (issue_all(P, s, &nl)) return -1;
+  spx_exec_stats t;
+  if (issue_all(P, s, &nl, &t)) return -1;
+  stats_add(&P->stats, t);
   P->launches = nl;
   return 0;
 }
@@ -521,7 +606,7 @@ int spx_plan_capture(uint64_t plan, uint64_t stream) {
   if (P->graph) { cudaGraphDestroy(P->graph); P->graph = nullptr; }
   SPX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   int nl = 0;
-  if (issue_all(P, s, &nl)) {
+  if (issue_all(P, s, &nl, &P->graph_tally)) {
     cudaGraph_t g;
     cudaStreamEndCapture(s, &g);
     if (g) cudaGraphDestroy(g);
@@ -537,6 +622,26 @@ int spx_plan_replay(uint64_t plan, uint64_t stream) {
   Plan* P = reinterpret_cast<Plan*>(plan);
   if (!P->exec) return spx_set_error("plan has no captured graph");
   SPX_CUDA(cudaGraphLaunch(P->exec, reinterpret_cast<cudaStream_t>(stream)));
+  stats_add(&P->stats, P->graph_tally);
+  return 0;
+}
+
+int spx_plan_tag(uint64_t plan, int index, int tag) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (index < 0 || index >= (int)P->recs.size()) return spx_set_error("record index out of range");
+  const int c = tag & SPX_TAG_COLL_MASK;
+  if (c > 4 || (tag & ~(SPX_TAG_COLL_MASK | SPX_TAG_INTERNAL))) return spx_set_error("bad record tag %#x", tag);
+  P->recs[index].tag = tag;
+  return 0;
+}
+
+int spx_plan_exec_stats(uint64_t plan, spx_exec_stats* out) {
+  *out = reinterpret_cast<Plan*>(plan)->stats;
+  return 0;
+}
+
+int spx_plan_reset_stats(uint64_t plan) {
+  reinterpret_cast<Plan*>(plan)->stats = spx_exec_stats{};
   return 0;
 }
 
@@ -609,10 +714,15 @@ int spx_plan_profile(uint64_t plan, uint64_t stream, float* out_ms, int n) {
   SPX_CUDA(cudaGetLastError());
   SPX_CUDA(cudaEventRecord(ev[0], s));
   int nl = 0;
+  spx_exec_stats t = {};
+  t.runs = 1;
   for (int i = 0; i < nr; ++i) {
     if (run_record(P->recs[i], s, &nl)) return -1;
+    tally_record(P->recs[i], &t);
     SPX_CUDA(cudaEventRecord(ev[i + 1], s));
   }
+  t.launches = nl;
+  stats_add(&P->stats, t);
   SPX_CUDA(cudaEventSynchronize(ev[nr]));
   for (int i = 0; i < nr && i < n; ++i) SPX_CUDA(cudaEventElapsedTime(&out_ms[i], ev[i], ev[i + 1]));
   for (auto& e : ev) cudaEventDestroy(e);

@@ -46,10 +46,13 @@ class Executable:
 
     def __init__(self, module, func="main", device: R.Device | None = None, devices=None,
                  comm_mode="local", comms=None, gemm_path=0, dry=False, comm_factory=None,
-                 overlap=None):
+                 overlap=None, dtype=np.float32):
         """dry=True builds the records against fake addresses without a GPU
-        (used by the CPU tests and the record simulator)."""
-        self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode).compile()
+        (used by the CPU tests and the record simulator).  dtype: the
+        arithmetic type of the call (np.result_type of the inputs,
+        evaluator._cdtype): float32 or int32."""
+        self.dtype = np.dtype(dtype)
+        self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode, dtype=self.dtype).compile()
         self.dry = dry
         self.device = None if dry else (device or R.Device(0))
         self.ndev = len(self.comp.devices)
@@ -93,6 +96,8 @@ class Executable:
             self.plan = R.NativePlan(self.device)
             for kind, params in self._records:
                 self.plan.add(kind, params)
+            for idx, tag in self._tags.items():
+                self.plan.tag(idx, tag)
             for idx, stream, waits in self.sched:
                 self.plan.set_sched(idx, stream, waits)
             self.plan.finalize()
@@ -108,6 +113,13 @@ class Executable:
                 first.setdefault(b, i)
             for b in k.ins:
                 last[b] = max(last.get(b, -1), i)
+            # a split right after the elementwise kernel that produces its
+            # source may run INSIDE that kernel (runtime.cu: ew_static_split):
+            # its pieces must not reuse the producer's inputs, which other
+            # CTAs of the fused launch may still be reading
+            if k.kind == "split" and i > 0 and ks[i - 1].kind == "ew" and k.data["src"][0] in ks[i - 1].outs:
+                for b in ks[i - 1].ins:
+                    last[b] = max(last.get(b, -1), i)
         off = {}
         top = 0
         for a in c.arg_bufs:
@@ -308,11 +320,22 @@ class Executable:
 
     def _emit(self):
         c = self.comp
+        self._tags = {}
         for i, k in enumerate(c.kernels):
             first = len(self._records)
             self._cur = i
             self._emit_one(k)
-            self._krange.append((first, len(self._records)))
+            end = len(self._records)
+            self._krange.append((first, end))
+            # the record that executes the logical collective (local mode: the
+            # group kernel; NCCL mode: the NCCL call or peer kernel, not the
+            # relayouts around it) and internal work without IR FLOPs
+            if k.kind == "coll" and k.data["kind"] in R.TAG_COLL and end > first:
+                idx = next((r for r in range(first, end) if self._records[r][0] in (R.K_NCCL, R.K_PEER)), first)
+                self._tags[idx] = R.TAG_COLL[k.data["kind"]]
+            if k.data.get("internal"):
+                for r in range(first, end):
+                    self._tags[r] = self._tags.get(r, 0) | R.TAG_INTERNAL
 
     def _emit_one(self, k):
         c = self.comp
@@ -952,7 +975,7 @@ class Executable:
         """per_device[p][arg] = local numpy array for hosted device p."""
         for p in range(self.ndev):
             for a in self.comp.arg_bufs:
-                arr = np.ascontiguousarray(per_device[p][a], dtype=np.float32)
+                arr = np.ascontiguousarray(per_device[p][a], dtype=self.dtype)
                 self.device.h2d(self.addr(p, a), arr)
 
     def download_results(self) -> list[list[np.ndarray]]:
@@ -963,7 +986,7 @@ class Executable:
             dims = tuple(f.result_types[j].dims)
             per = []
             for p in range(self.ndev):
-                a = np.empty(dims, dtype=np.float32)
+                a = np.empty(dims, dtype=self.dtype)
                 self.device.d2h(a, self.addr(p, b))
                 per.append(a)
             out.append(per)
@@ -975,6 +998,61 @@ class Executable:
 
     def records(self):
         return list(self._records)
+
+    # ------------------------------------------------------- executed work
+    ARITH = {R.OP[k] for k in ("ADD", "MUL", "NEG", "EXP", "MAX", "ADDI", "MULI", "IADD", "IMUL")}
+
+    def _ew_flops(self, p) -> float:
+        return float(sum(1 for i in range(p.n_prog) if p.prog[i].op in self.ARITH)) * p.numel * p.ndev
+
+    def issued_per_run(self) -> dict:
+        """What one run of the plan issues, derived from the records exactly as
+        the runtime counts it (runtime.cu record_flops / tally_record) -- the
+        CPU-side mirror used where there is no GPU (dry plans)."""
+        coll = {k: 0 for k in R.COLL_ORDER}
+        flops = 0.0
+        epi_ops = {R.EPI_ADD: 1, R.EPI_SQUARE: 1, R.EPI_MULSCALE: 2, R.EPI_MOMENTUM: 5}
+        for idx, (kind, p) in enumerate(self._records):
+            tag = self._tags.get(idx, 0)
+            c = tag & 7
+            if c:
+                coll[R.COLL_ORDER[c - 1]] += 1
+            if tag & R.TAG_INTERNAL:
+                continue
+            if kind == R.K_GEMM:
+                flops += (2.0 * p.K + epi_ops.get(p.epi, 0)) * p.M * p.N * p.ndev
+            elif kind == R.K_EW:
+                flops += self._ew_flops(p)
+            elif kind == R.K_REDUCE:
+                flops += self._ew_flops(p.x) + float(p.x.numel) * p.x.ndev
+        return {"coll": coll, "flops": flops}
+
+    def work_report(self) -> dict:
+        """Executed work vs the reference simulator's prediction, per device and
+        step.  `program` = collective_counts(local module) (spmd.py:264-271),
+        `executed` = logical collectives the runtime issued per run (measured
+        counters when the plan has run, else the record-derived count),
+        `cse_elided` = collectives served by an identical earlier one (their
+        executed + elided = program; SPX_COLL_CSE=0 executes every one).
+        FLOPs: `simulator` = simulate().compute_flops convention (sim.py:86-100),
+        `executed` = issued by the kernels, `folded` = elementwise ops with
+        constant operands evaluated at compile time; executed + folded =
+        simulator."""
+        c = self.comp
+        pred = self.issued_per_run()
+        ex_coll, ex_flops, source = pred["coll"], pred["flops"], "records"
+        if self.plan is not None:
+            st = self.plan.exec_stats()
+            if st["runs"] > 0:
+                ex_coll = {k: v / st["runs"] for k, v in st["coll"].items()}
+                ex_flops = st["flops"] / st["runs"]
+                source = f"runtime counters over {st['runs']} runs"
+        per = 1.0 / self.ndev      # FLOPs are summed over the virtual devices; a
+        # collective record is one logical collective for every device group
+        return {"collectives": {"program": dict(c.counts),
+                                "executed": dict(ex_coll),
+                                "cse_elided": dict(c.cse_elided), "source": source},
+                "flops": {"simulator": c.flops, "executed": ex_flops * per, "folded": c.folded_flops}}
 
     def close(self):
         if self.dry:

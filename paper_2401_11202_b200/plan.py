@@ -108,8 +108,11 @@ class Compiler:
     in-GPU mode, [rank] for the one-process-per-GPU NCCL mode).
     """
 
-    def __init__(self, module, func="main", devices=None, comm_mode="local"):
+    def __init__(self, module, func="main", devices=None, comm_mode="local", dtype=np.float32):
         self.module = module
+        self.dtype = np.dtype(dtype)
+        if self.dtype != np.dtype(np.float32):
+            raise TypeError(f"compute type {self.dtype}: the backend computes float32")
         self.f = module.func(func)
         self.mesh = module.mesh
         n_mesh = self.mesh.device_count if self.mesh is not None else 1
@@ -128,6 +131,13 @@ class Compiler:
         self.result_bufs = []
         self.counts = {k: 0 for k in COUNTED_COLLECTIVES}
         self.flops = 0.0
+        # work the program lists that no kernel executes: collectives reused
+        # from an identical earlier one (CSE; SPX_COLL_CSE=0 disables it) and
+        # elementwise ops folded at compile time (constant operands only)
+        self.cse_elided = {k: 0 for k in COUNTED_COLLECTIVES}
+        self.folded_flops = 0.0
+        import os
+        self.coll_cse = os.environ.get("SPX_COLL_CSE", "1") != "0"
         self._matcache = {}
 
     # ---------------------------------------------------------------- helpers
@@ -199,9 +209,9 @@ class Compiler:
     # ------------------------------------------------------------------ main
     def compile(self):
         f = self.f
+        # the arithmetic type is the inputs' (np.result_type, spmd_interp.py:173),
+        # not the IR's element kind: both kinds are 4 bytes (ir.py:14)
         for n, t in f.args:
-            if t.elem != "f32":
-                raise UnsupportedProgram(f"arg %{n}: element kind {t.elem} (backend computes f32)")
             self.types[n] = tuple(t.dims)
             self.buffers[n] = max(1, _prod(t.dims))
             self.bufdims[n] = tuple(t.dims)
@@ -210,8 +220,6 @@ class Compiler:
         uses = self._uses()
         for i, op in enumerate(f.ops):
             for r, t in zip(op.results, op.result_types):
-                if t.elem != "f32":
-                    raise UnsupportedProgram(f"%{r}: element kind {t.elem}")
                 self.types[r] = tuple(t.dims)
             self._lower(i, op, uses)
             if op.kind not in COLLECTIVE_KINDS:
@@ -248,6 +256,7 @@ class Compiler:
                     else:
                         v = np.float32(np.exp(kids[0]))
                 D[r] = Desc("const", dims, value=v)
+                self.folded_flops += op_flops(op, [self.types[o] for o in op.operands])
                 return
             node = self._node(k, kids)
             u = uses.get(r, [])
@@ -354,7 +363,7 @@ class Compiler:
             root = Leaf(ws, 0, _contig((splits, M, N)))
             self.kernels.append(Kernel("reduce", [out], {ws}, op_index=i,
                                        data=dict(root=root, in_dims=(splits, M, N), red=[0],
-                                                 monoid="sum")))
+                                                 monoid="sum", internal=True)))
         self.desc[op.results[0]] = Desc("buf", dims, buf=out)
 
     NUM_SMS = 148
@@ -463,11 +472,15 @@ class Compiler:
         # identical values: reuse the first result (bit-exact data movement)
         import json as _json
         cse_key = None
-        if x.kind == "buf":
+        if not self.coll_cse:
+            pass
+        elif x.kind == "buf":
             cse_key = (k, x.buf, _json.dumps(op.attrs, sort_keys=True), tuple(dims))
             hit = self._coll_cse.get(cse_key)
             if hit is not None:
                 self.desc[r] = Desc("buf", dims, buf=hit)
+                if k in self.cse_elided:
+                    self.cse_elided[k] += 1
                 return
         elif x.kind == "view" and k == "all_gather" and x.off == 0:
             # all_gather of a transposed buffer (the backward pass's W^T) is the
@@ -495,6 +508,7 @@ class Compiler:
                     gcs = _contig(gd)
                     self.desc[r] = Desc("view", tuple(dims), buf=hit, off=0,
                                         strides=tuple(gcs[q] for q in perm))
+                    self.cse_elided[k] += 1
                     return
         src = self.materialize(src_name)
         out = self._new_buf(dims, "c")

@@ -86,7 +86,12 @@ WORKLOADS = {
                                        8: "c2_tf8_bpmp_B2M4"}},
     "c3": {"desc": "mini_transformer_train(blocks=32, batch=8192, d_model=2048, d_ff=8192), BP+Z3",
            "scale": 0.02, "programs": {1: "c3_tf32_dense", 2: "c3_tf32_bpz3_B2", 4: "c3_tf32_bpz3_B4",
-                                       8: "c3_tf32_bpz3_B8"}},
+                                       8: "c3_tf32_bpz3_B8"},
+           # the CPU evaluator cannot hold 32 blocks: its step time is
+           # t(1 block) + 31 (t(2 blocks) - t(1 block)) at full width
+           "cpu_extrap": {"blocks": 32, 1: ("c3_tf1_dense", "c3_tf2_dense"),
+                          2: ("c3_tf1_bpz3_B2", "c3_tf2_bpz3_B2"), 4: ("c3_tf1_bpz3_B4", "c3_tf2_bpz3_B4"),
+                          8: ("c3_tf1_bpz3_B8", "c3_tf2_bpz3_B8")}},
     "c4": {"desc": "unet_train(batch=128, 32x32, channels 64/256/512) U-Net analog (tools/unet_model.py), BP+Z2",
            "scale": 0.05, "programs": {1: "c4_unet_dense", 2: "c4_unet_bpz2_B2", 4: "c4_unet_bpz2_B4",
                                        8: "c4_unet_bpz2_B8"}},

@@ -107,6 +107,17 @@ class PeerParams(C.Structure):
 
 K_PEER = 7
 K_SPLIT = 8
+
+# record tags (include/spindle_b200.h spx_tag_bits)
+TAG_COLL = {"all_gather": 1, "all_reduce": 2, "reduce_scatter": 3, "all_to_all": 4}
+TAG_INTERNAL = 0x100
+COLL_ORDER = ("all_gather", "all_reduce", "reduce_scatter", "all_to_all")
+
+
+class ExecStats(C.Structure):
+    _fields_ = [("runs", C.c_int64), ("coll", C.c_int64 * 4), ("flops", C.c_double), ("launches", C.c_int64)]
+
+
 PEER_MAX_BLOCKS = 512      # include/spindle_b200.h
 PEER_PHASES = 3
 
@@ -123,6 +134,8 @@ EXPORTS = [
     "spx_stream_wait_event", "spx_memcpy_d2d",
     "spx_plan_profile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
     "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
+    "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats",
+    "spx_host_register", "spx_host_unregister", "spx_host_copy",
 ]
 
 _lib = None
@@ -171,6 +184,11 @@ def load(build_if_missing: bool = True):
         "spx_plan_set_sched": [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int],
         "spx_ipc_get_handle": [C.c_uint64, C.c_void_p], "spx_ipc_open": [C.c_void_p, C.POINTER(C.c_uint64)],
         "spx_ipc_close": [C.c_uint64],
+        "spx_plan_tag": [C.c_uint64, C.c_int, C.c_int],
+        "spx_plan_exec_stats": [C.c_uint64, C.POINTER(ExecStats)],
+        "spx_plan_reset_stats": [C.c_uint64],
+        "spx_host_register": [C.c_void_p, C.c_uint64], "spx_host_unregister": [C.c_void_p],
+        "spx_host_copy": [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int],
     }
     for name, args in sigs.items():
         getattr(lib, name).argtypes = args
@@ -293,6 +311,19 @@ class NativePlan:
         assert isinstance(params, PARAMS[kind])
         call(self.lib.spx_plan_add, self.h, kind, C.byref(params), C.sizeof(params))
         self.n_records += 1
+
+    def tag(self, index: int, tag: int):
+        call(self.lib.spx_plan_tag, self.h, index, tag)
+
+    def exec_stats(self) -> dict:
+        """What the runtime has issued so far (include/spindle_b200.h spx_exec_stats)."""
+        st = ExecStats()
+        call(self.lib.spx_plan_exec_stats, self.h, C.byref(st))
+        return {"runs": int(st.runs), "coll": {k: int(st.coll[i]) for i, k in enumerate(COLL_ORDER)},
+                "flops": float(st.flops), "launches": int(st.launches)}
+
+    def reset_stats(self):
+        call(self.lib.spx_plan_reset_stats, self.h)
 
     def set_sched(self, index: int, stream: int, waits):
         arr = (C.c_int * max(1, len(waits)))(*waits)

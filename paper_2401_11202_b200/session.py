@@ -219,6 +219,18 @@ class Session:
     def results(self):
         return self.ex.download_results()
 
+    def call(self, global_inputs: dict):
+        """One step with every input coming from host memory and every result
+        going back to it -- the drop-in call's data movement (spmd_interpret:
+        shard, copy in, run, copy out) for this process's mesh devices:
+        returns [result j][hosted device] local arrays."""
+        self.ex.upload_args(self.local_inputs(global_inputs))
+        if self.ex.plan.captured:
+            self.ex.plan.replay()
+        else:
+            self.ex.plan.run()
+        return self.ex.download_results()
+
     def result_addr(self, j: int, p: int = 0) -> int:
         return self.ex.addr(p, self.ex.comp.result_bufs[j])
 

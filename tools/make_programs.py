@@ -71,7 +71,22 @@ CONFIGS = {
     "c5_tf8_bpmpz3emb_B2M2E2": ("transformer", TF_C2, "B:2,M:2,E:2", ["bp", "mp", "z3"], [EMB]),
     "c5_tf8_bpmpz3_B2M2": ("transformer", TF_C2, "B:2,M:2", ["bp", "mp", "z3"], []),
     "c5_tf8_bpz3_B2": ("transformer", TF_C2, "B:2", ["bp", "z3"], []),
+    # parity programs: the BASELINE configs' own meshes and tactics at full
+    # width and reduced depth (blocks are identical; the CPU oracle cannot hold
+    # C3 at 32 blocks) -- tests/test_config_parity.py
+    "c2_tf1_bpmp_B2M4": ("transformer", dict(TF_C2, blocks=1), "B:2,M:4", ["bp", "mp"], []),
+    "c2_tf2_bpmp_B2M4": ("transformer", dict(TF_C2, blocks=2), "B:2,M:4", ["bp", "mp"], []),
+    "c5_tf1_bpmpz3emb_B2M2E2": ("transformer", dict(TF_C2, blocks=1), "B:2,M:2,E:2", ["bp", "mp", "z3"], [EMB]),
+    "c5_tf2_bpmpz3emb_B2M2E2": ("transformer", dict(TF_C2, blocks=2), "B:2,M:2,E:2", ["bp", "mp", "z3"], [EMB]),
+    "c3_tf1_bpz3_B8": ("transformer", dict(TF_C3, blocks=1), "B:8", ["bp", "z3"], []),
+    # CPU-baseline sample for C3 (t(1) + 31 (t(2) - t(1)))
+    "c3_tf1_dense": ("transformer", dict(TF_C3, blocks=1), None, [], []),
+    "c3_tf2_dense": ("transformer", dict(TF_C3, blocks=2), None, [], []),
 }
+# ... and for the reference arm at N > 1 (the partitioned program's CPU evaluator)
+for _n in (2, 4, 8):
+    for _b in (1, 2):
+        CONFIGS[f"c3_tf{_b}_bpz3_B{_n}"] = ("transformer", dict(TF_C3, blocks=_b), f"B:{_n}", ["bp", "z3"], [])
 
 
 def make(name: str):
