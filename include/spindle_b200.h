@@ -79,6 +79,7 @@ typedef struct {
   uint64_t base;                  /* device 0 arena base address              */
   int64_t dev_stride;             /* bytes between virtual devices            */
   int32_t ndev, rank, n_in, n_out, n_prog, vec;  /* vec: 1 = float4 fast path */
+  int32_t dtype, dtype_pad;       /* SPX_DT_F32 / SPX_DT_I32 (imm[] then holds int32 bits) */
   int64_t dims[SPX_MAX_RANK];     /* logical output shape (row-major)         */
   int64_t numel;
   spx_view in[SPX_MAX_IN];
@@ -87,6 +88,11 @@ typedef struct {
   spx_insn prog[SPX_MAX_PROG];
   float imm[SPX_MAX_PROG];
 } spx_ew_params;
+
+/* Arithmetic type of a record (the reference computes in np.result_type of the
+ * inputs, spmd_interp.py:173; the IR's element kinds are f32 and i32,
+ * ir.py:14).  i32 arithmetic wraps modulo 2^32 like numpy's int32 ufuncs. */
+enum spx_dtype { SPX_DT_F32 = 0, SPX_DT_I32 = 1 };
 
 /* ---- reductions ---------------------------------------------------------- */
 typedef struct {
@@ -149,6 +155,7 @@ typedef struct {
   int32_t h3_shared;
   int32_t h3_splitk;              /* path 3 split-K of few-tile GEMMs: <= 1 off (default), n = at most n splits */
   int64_t h3_a_off, h3_a_scl, h3_b_off, h3_b_scl;
+  int32_t dtype, dtype_pad;       /* SPX_DT_I32: wrapping int32 GEMM (SIMT) */
 } spx_gemm_params;
 
 /* ---- operand split for the block-scaled 3xFP16 GEMM ------------------------
@@ -195,6 +202,7 @@ typedef struct {
   uint64_t members;               /* const int32_t* [ndev * n_members]          */
   uint64_t base_off;              /* const int64_t* [ndev]                      */
   uint64_t dst;                   /* float** [ndev]                             */
+  int32_t dtype, dtype_pad;
 } spx_creduce_params;
 
 /* ---- NCCL collective across processes (one mesh device per GPU) --------- */
@@ -246,6 +254,12 @@ int spx_host_register(void* ptr, uint64_t bytes);
 int spx_host_unregister(void* ptr);
 /* host memcpy split over `threads` threads (staging into pinned buffers) */
 int spx_host_copy(void* dst, const void* src, uint64_t bytes, int threads);
+/* copies between PAGEABLE host memory and the device through a ring of pinned
+ * chunks filled/drained by a host thread pool while the copy engine moves the
+ * previous chunk (ordered on `stream`).  h2d returns once the source may be
+ * reused; d2h returns once the data is in `dst`. */
+int spx_h2d_staged(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream);
+int spx_d2h_staged(void* dst, uint64_t src, uint64_t bytes, uint64_t stream);
 int spx_stream_create(uint64_t* out_stream);
 int spx_stream_sync(uint64_t stream);
 int spx_stream_destroy(uint64_t stream);
@@ -259,6 +273,14 @@ int spx_ipc_close(uint64_t ptr);
 int spx_nccl_get_unique_id(uint8_t out_id[128]);
 int spx_comm_init(const uint8_t id[128], int nranks, int rank, int* out_comm);
 int spx_comm_destroy(int comm);
+/* failure detection: NCCL asynchronous error of a communicator (0 = none),
+ * abort, a peer-collective barrier that gave up (0 = none, else 1 + phase),
+ * and a stream wait that watches for both (timeout_s 0 = no limit) */
+int spx_comm_async_error(int comm, int* out_err);
+int spx_comm_abort(int comm);
+int spx_peer_error(int* out);
+int spx_peer_error_clear(void);
+int spx_stream_sync_watch(uint64_t stream, double timeout_s);
 
 /* plans: a sequence of records [kind, param struct] executed in order on a stream */
 int spx_plan_create(uint64_t* out_plan);

@@ -63,6 +63,11 @@ int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_creduce(const spx_creduce_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_gemm_simt(const spx_gemm_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch);
+// int32 arithmetic records (int32.cu)
+int spx_launch_ew_i32(const spx_ew_params& p, cudaStream_t s, int* nlaunch);
+int spx_launch_reduce_i32(const spx_reduce_params& p, cudaStream_t s, int* nlaunch);
+int spx_launch_creduce_i32(const spx_creduce_params& p, cudaStream_t s, int* nlaunch);
+int spx_launch_gemm_i32(const spx_gemm_params& p, cudaStream_t s, int* nlaunch);
 
 struct SpxGemmTC;  // prepared tcgen05 GEMM (tensor maps), see gemm_tc.cu
 int spx_gemm_tc_prepare(const spx_gemm_params& p, SpxGemmTC** out);

@@ -236,7 +236,7 @@ const Entry kCatalog[] = {
 
 // Catalog index for a program, or -1.  Also requires the vector-path layout.
 int spx_ew_static_match(const spx_ew_params& p) {
-  if (!p.vec || p.numel % 4 || p.rank > 2 || p.numel >= (int64_t(1) << 31)) return -1;
+  if (p.dtype != SPX_DT_F32 || !p.vec || p.numel % 4 || p.rank > 2 || p.numel >= (int64_t(1) << 31)) return -1;
   for (int i = 0; i < (int)(sizeof(kCatalog) / sizeof(kCatalog[0])); ++i) {
     const Entry& c = kCatalog[i];
     if (c.n_in != p.n_in || c.n_out != p.n_out || c.n_prog != p.n_prog) continue;

@@ -30,24 +30,47 @@
 // SM while every variant fits two per SM (__launch_bounds__(256, 2)), so a
 // second peer kernel -- or an NCCL kernel -- always finds room.
 #include <cstdlib>
+#include <cstring>
 #include "common.cuh"
 
 namespace {
 
-// Flags are relaxed (volatile) system-scope accesses: a release/acquire pair
-// costs ~5 us per barrier across NVLink, and neither side needs one -- the
-// inputs were completed by earlier kernels (kernel boundaries make them
-// visible to peer reads), the depart flag is stored after __syncthreads, when
-// every load of the block has returned its value, and the kernel reads each
-// peer element exactly once (no stale L1 line can be hit).
-SPX_DEV void st_flag(uint32_t* p, uint32_t v) {
-  asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Flag protocol and memory ordering.  Flags are written with system-scope
+// stores into the members' arenas and polled with relaxed system-scope loads.
+// Where a barrier publishes data written IN THE SAME KERNEL (the two-shot
+// all-reduce's reduced segments, read by the peers after phase 1) the
+// arriving thread issues the flag store with release semantics after the
+// block's __syncthreads, and the waiting thread follows its successful poll
+// with an acquire fence before the block's __syncthreads: the PTX
+// message-passing pattern at system scope (bar.sync makes the other threads'
+// writes/reads part of the release/acquire).  The arrive barrier of phase 0
+// publishes inputs completed by EARLIER kernels (kernel boundaries) and the
+// depart barrier orders only reads before a later overwrite (every load of
+// the block has returned when __syncthreads completes), so those use relaxed
+// flags unless SPX_PEER_ORDER=2 asks for release/acquire everywhere
+// (SPX_PEER_ORDER=0: relaxed everywhere, the round-1 protocol).
+SPX_DEV void st_flag(uint32_t* p, uint32_t v, bool release) {
+  if (release) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 SPX_DEV uint32_t ld_flag(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+SPX_DEV uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Set when a barrier gave up waiting (a member never arrived within the
+// timeout): the kernel abandons the wait -- its results are garbage -- and the
+// host raises (spx_peer_error, polled while the host waits for the stream)
+// instead of the context dying on a trap.  The word lives in mapped pinned host
+// memory, so the host reads it without any CUDA call.
+uint32_t* g_err_host = nullptr;
+uint32_t* g_err_dev = nullptr;
 
 // flag word of (slot, phase, block, member) inside a member's flag region
 SPX_DEV uint32_t* flag_at(uint64_t region, int slot, int phase, int block, int member) {
@@ -55,17 +78,30 @@ SPX_DEV uint32_t* flag_at(uint64_t region, int slot, int phase, int block, int m
          (((int64_t)(slot * SPX_PEER_PHASES + phase) * SPX_PEER_MAX_BLOCKS + block) * 8 + member);
 }
 
-SPX_DEV void block_barrier(const spx_peer_params& p, int phase, uint32_t epoch) {
+struct PeerSync {
+  uint64_t timeout_ns;   // 0: wait forever
+  int order;             // SPX_PEER_ORDER
+  uint32_t* err;         // mapped host error word
+};
+
+// publish: this barrier makes data written by this kernel visible to the peers
+SPX_DEV void block_barrier(const spx_peer_params& p, int phase, uint32_t epoch, PeerSync ps, bool publish) {
   const int t = threadIdx.x;
+  const bool ra = ps.order >= 2 || (ps.order == 1 && publish);
   if (t < p.n) {
-    st_flag(flag_at(p.flags[t], p.slot, phase, blockIdx.x, p.me), epoch);
+    st_flag(flag_at(p.flags[t], p.slot, phase, blockIdx.x, p.me), epoch, ra);
     const uint32_t* mine = flag_at(p.flags[p.me], p.slot, phase, blockIdx.x, t);
     if (ld_flag(mine) < epoch) {
-      const long long t0 = clock64();
+      const uint64_t t0 = globaltimer();
       while (ld_flag(mine) < epoch) {
-        if (clock64() - t0 > 20000000000LL) __trap();     // ~10 s: a peer never arrived
+        if (ps.timeout_ns && globaltimer() - t0 > ps.timeout_ns) {
+          *reinterpret_cast<volatile uint32_t*>(ps.err) = 1u + (uint32_t)phase;
+          __threadfence_system();
+          break;
+        }
       }
     }
+    if (ra) asm volatile("fence.acq_rel.sys;" ::: "memory");
   }
   __syncthreads();
 }
@@ -91,13 +127,13 @@ struct PeerU { static constexpr int value = N >= 8 ? 2 : 4; };
 // N > 0: member count known at compile time (all loads issued before folding)
 template <int N>
 __global__ void __launch_bounds__(256, 2) peer_allreduce(const __grid_constant__ spx_peer_params p, int64_t per_block,
-                                                      int dbg) {
+                                                      int dbg, PeerSync ps) {
   SPX_PEER_ENTRY();
   constexpr int U = PeerU<N>::value;
   const int n = N > 0 ? N : p.n;
   uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
   const uint32_t epoch = *counter + 1u;
-  if (!(dbg & 1)) block_barrier(p, 0, epoch);
+  if (!(dbg & 1)) block_barrier(p, 0, epoch, ps, false);
   if (dbg & 4) per_block = 0;
 
   const int64_t n4 = p.count >> 2;
@@ -144,7 +180,7 @@ __global__ void __launch_bounds__(256, 2) peer_allreduce(const __grid_constant__
     reinterpret_cast<float*>(p.dst)[i] = acc;
   }
   __syncthreads();
-  if (!(dbg & 2)) block_barrier(p, 1, epoch);
+  if (!(dbg & 2)) block_barrier(p, 1, epoch, ps, false);
   if (threadIdx.x == 0) *counter = epoch;
   SPX_PEER_EXIT();
 }
@@ -159,12 +195,12 @@ __global__ void __launch_bounds__(256, 2) peer_allreduce(const __grid_constant__
 // (and so every replica's bits) is the same as the one-shot kernel's.
 template <int N>
 __global__ void __launch_bounds__(256, 2) peer_allreduce_2shot(const __grid_constant__ spx_peer_params p,
-                                                            int64_t seg4, int64_t per_block) {
+                                                            int64_t seg4, int64_t per_block, PeerSync ps) {
   SPX_PEER_ENTRY();
   constexpr int U = PeerU<N>::value;
   uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
   const uint32_t epoch = *counter + 1u;
-  block_barrier(p, 0, epoch);
+  block_barrier(p, 0, epoch, ps, false);
   // phase A: my segment's chunk b
   {
     const int64_t s0 = (int64_t)p.me * seg4;
@@ -192,7 +228,7 @@ __global__ void __launch_bounds__(256, 2) peer_allreduce_2shot(const __grid_cons
     }
   }
   __syncthreads();
-  block_barrier(p, 1, epoch);
+  block_barrier(p, 1, epoch, ps, true);     // my reduced segment is read by the peers next
   // phase B: the other members' chunk b, from their outputs (same arena offset)
   {
     float4* dst = reinterpret_cast<float4*>(p.dst);
@@ -216,7 +252,7 @@ __global__ void __launch_bounds__(256, 2) peer_allreduce_2shot(const __grid_cons
     }
   }
   __syncthreads();
-  block_barrier(p, 2, epoch);
+  block_barrier(p, 2, epoch, ps, false);
   if (threadIdx.x == 0) *counter = epoch;
   SPX_PEER_EXIT();
 }
@@ -226,12 +262,13 @@ __global__ void __launch_bounds__(256, 2) peer_allreduce_2shot(const __grid_cons
 // same arrive / depart barriers: inputs complete before anyone reads, nobody
 // leaves while a peer still reads its input.
 template <int N>
-__global__ void __launch_bounds__(256, 2) peer_allgather(const __grid_constant__ spx_peer_params p, int64_t per_block) {
+__global__ void __launch_bounds__(256, 2) peer_allgather(const __grid_constant__ spx_peer_params p, int64_t per_block,
+                                                      PeerSync ps) {
   SPX_PEER_ENTRY();
   constexpr int U = PeerU<N>::value;
   uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS + blockIdx.x;
   const uint32_t epoch = *counter + 1u;
-  block_barrier(p, 0, epoch);
+  block_barrier(p, 0, epoch, ps, false);
   const int64_t n4 = p.count >> 2;
   const int64_t b0 = (int64_t)blockIdx.x * per_block, b1 = min(n4, b0 + per_block);
   float4* dst = reinterpret_cast<float4*>(p.dst);
@@ -253,12 +290,35 @@ __global__ void __launch_bounds__(256, 2) peer_allgather(const __grid_constant__
       }
   }
   __syncthreads();
-  block_barrier(p, 1, epoch);
+  block_barrier(p, 1, epoch, ps, false);
   if (threadIdx.x == 0) *counter = epoch;
   SPX_PEER_EXIT();
 }
 
 }  // namespace
+
+static int peer_err_init() {
+  if (g_err_host) return 0;
+  void* h = nullptr;
+  SPX_CUDA(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(h, 0, 64);
+  void* d = nullptr;
+  SPX_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+  g_err_host = static_cast<uint32_t*>(h);
+  g_err_dev = static_cast<uint32_t*>(d);
+  return 0;
+}
+
+// 0: no peer barrier has timed out; else 1 + the phase that gave up
+extern "C" int spx_peer_error(int* out) {
+  *out = g_err_host ? (int)*reinterpret_cast<volatile uint32_t*>(g_err_host) : 0;
+  return 0;
+}
+
+extern "C" int spx_peer_error_clear(void) {
+  if (g_err_host) *reinterpret_cast<volatile uint32_t*>(g_err_host) = 0;
+  return 0;
+}
 
 int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if (p.n < 1 || p.n > 8) return spx_set_error("peer collective: group size %d", p.n);
@@ -278,6 +338,16 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const int64_t per_block = (n4 + blocks - 1) / blocks;
+  static PeerSync ps = {~0ull, -1, nullptr};
+  if (ps.order < 0) {
+    if (peer_err_init()) return -1;
+    ps.err = g_err_dev;
+    const char* e = getenv("SPX_PEER_ORDER");
+    ps.order = e ? atoi(e) : 1;
+    const char* t = getenv("SPX_PEER_TIMEOUT_S");
+    const double sec = t ? atof(t) : 300.0;
+    ps.timeout_ns = sec > 0 ? (uint64_t)(sec * 1e9) : 0;
+  }
   static int dbg = -1, two = -1;
   if (dbg < 0) { const char* e = getenv("SPX_PEER_DBG"); dbg = e ? atoi(e) : 0; }
   if (two < 0) { const char* e = getenv("SPX_PEER_TWOSHOT"); two = e ? atoi(e) : 1; }
@@ -285,10 +355,10 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   // one-shot; 1 MB: 14.4 vs 11.2), when every segment is whole float4s
   if (p.kind == 1) {
     switch (p.n) {
-      case 2: spx_launch(peer_allgather<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
-      case 3: spx_launch(peer_allgather<3>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
-      case 4: spx_launch(peer_allgather<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
-      case 8: spx_launch(peer_allgather<8>, dim3((unsigned)blocks), 256, 0, s, p, per_block); break;
+      case 2: spx_launch(peer_allgather<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block, ps); break;
+      case 3: spx_launch(peer_allgather<3>, dim3((unsigned)blocks), 256, 0, s, p, per_block, ps); break;
+      case 4: spx_launch(peer_allgather<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block, ps); break;
+      case 8: spx_launch(peer_allgather<8>, dim3((unsigned)blocks), 256, 0, s, p, per_block, ps); break;
       default: return spx_set_error("peer all-gather: group size %d", p.n);
     }
     SPX_CHECK_LAUNCH();
@@ -303,17 +373,17 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
     if (b2 > cap) b2 = cap;
     if (b2 < 1) b2 = 1;
     const int64_t pb = (seg4 + b2 - 1) / b2;
-    if (p.n == 4) spx_launch(peer_allreduce_2shot<4>, dim3((unsigned)b2), 256, 0, s, p, seg4, pb);
-    else spx_launch(peer_allreduce_2shot<8>, dim3((unsigned)b2), 256, 0, s, p, seg4, pb);
+    if (p.n == 4) spx_launch(peer_allreduce_2shot<4>, dim3((unsigned)b2), 256, 0, s, p, seg4, pb, ps);
+    else spx_launch(peer_allreduce_2shot<8>, dim3((unsigned)b2), 256, 0, s, p, seg4, pb, ps);
     SPX_CHECK_LAUNCH();
     if (nlaunch) ++*nlaunch;
     return 0;
   }
   switch (p.n) {
-    case 2: spx_launch(peer_allreduce<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
-    case 4: spx_launch(peer_allreduce<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
-    case 8: spx_launch(peer_allreduce<8>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg); break;
-    default: spx_launch(peer_allreduce<0>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg);
+    case 2: spx_launch(peer_allreduce<2>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg, ps); break;
+    case 4: spx_launch(peer_allreduce<4>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg, ps); break;
+    case 8: spx_launch(peer_allreduce<8>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg, ps); break;
+    default: spx_launch(peer_allreduce<0>, dim3((unsigned)blocks), 256, 0, s, p, per_block, dbg, ps);
   }
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;

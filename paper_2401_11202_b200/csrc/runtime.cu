@@ -6,6 +6,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -68,6 +71,8 @@ typedef int (*fn_sendrecv)(const void*, size_t, int, int, nccl_comm_t, cudaStrea
 typedef int (*fn_group)(void);
 typedef const char* (*fn_errstr)(int);
 typedef int (*fn_count)(nccl_comm_t, int*);
+typedef int (*fn_async)(nccl_comm_t, int*);
+typedef int (*fn_abort)(nccl_comm_t);
 
 static struct {
   void* h = nullptr;
@@ -81,6 +86,8 @@ static struct {
   fn_group gstart, gend;
   fn_errstr errstr;
   fn_count count;
+  fn_async async_error;
+  fn_abort abort;
 } N;
 static std::vector<nccl_comm_t> g_comms;
 
@@ -109,6 +116,8 @@ static int nccl_load() {
   LOADSYM(gend, "ncclGroupEnd");
   LOADSYM(errstr, "ncclGetErrorString");
   LOADSYM(count, "ncclCommCount");
+  LOADSYM(async_error, "ncclCommGetAsyncError");
+  LOADSYM(abort, "ncclCommAbort");
 #undef LOADSYM
   return 0;
 }
@@ -230,16 +239,25 @@ static int run_record(Record& r, cudaStream_t s, int* nl) {
   if (r.fused) return 0;
   switch (r.kind) {
     case SPX_K_EW:
+      if (reinterpret_cast<const spx_ew_params*>(r.params.data())->dtype == SPX_DT_I32)
+        return spx_launch_ew_i32(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
       if (r.fused_split >= 0)
         return spx_launch_ew_static_split(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()),
                                           *reinterpret_cast<const spx_split_params*>(r.split_params.data()),
                                           r.split_out, s, nl);
       if (r.path > 0) return spx_launch_ew_static(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
       return spx_launch_ew(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
-    case SPX_K_REDUCE: return spx_launch_reduce(*reinterpret_cast<const spx_reduce_params*>(r.params.data()), s, nl);
+    case SPX_K_REDUCE: {
+      const spx_reduce_params& q = *reinterpret_cast<const spx_reduce_params*>(r.params.data());
+      return q.x.dtype == SPX_DT_I32 ? spx_launch_reduce_i32(q, s, nl) : spx_launch_reduce(q, s, nl);
+    }
     case SPX_K_GATHER: return spx_launch_gather(*reinterpret_cast<const spx_gather_params*>(r.params.data()), s, nl);
-    case SPX_K_CREDUCE: return spx_launch_creduce(*reinterpret_cast<const spx_creduce_params*>(r.params.data()), s, nl);
+    case SPX_K_CREDUCE: {
+      const spx_creduce_params& q = *reinterpret_cast<const spx_creduce_params*>(r.params.data());
+      return q.dtype == SPX_DT_I32 ? spx_launch_creduce_i32(q, s, nl) : spx_launch_creduce(q, s, nl);
+    }
     case SPX_K_GEMM:
+      if (r.path == 4) return spx_launch_gemm_i32(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
       if (r.path == 3) return spx_gemm_h3_launch(r.h3, s, nl);
       if (r.path == 1) return spx_gemm_tc_launch(r.tc, s, nl);
       return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
@@ -334,6 +352,157 @@ int spx_host_unregister(void* p) {
   SPX_CUDA(cudaHostUnregister(p));
   return 0;
 }
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Staged host<->device copies for pageable host arrays (the drop-in call's
+// inputs and results): a persistent pool of memcpy threads moves chunks
+// between the user's memory and a ring of pinned buffers while the copy
+// engine moves the previous chunk over PCIe -- pageable cudaMemcpy runs at
+// ~11 GB/s H2D and ~5 GB/s D2H into fresh pages on this box, pinned DMA at
+// ~55 GB/s and a 16-thread host memcpy at ~86 GB/s (tools/h2d_bench.py).
+// ---------------------------------------------------------------------------
+namespace {
+
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 1; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+    n_ = n;
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  // memcpy split over the pool (the calling thread takes part)
+  void copy(void* dst, const void* src, size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void part(int i) {
+    const size_t per = ((bytes_ + n_ - 1) / n_ + 4095) & ~size_t(4095);
+    const size_t o = per * i;
+    if (o < bytes_) memcpy(dst_ + o, src_ + o, o + per > bytes_ ? bytes_ - o : per);
+  }
+  void loop(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      part(i);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        --pending_;
+      }
+      done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+  int n_ = 1, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+struct Staging {
+  static constexpr int R = 4;
+  static constexpr size_t CHUNK = 32u << 20;
+  void* buf[R] = {};
+  cudaEvent_t ev[R] = {};
+  CopyPool* pool = nullptr;
+  std::mutex m;
+};
+Staging g_stage;
+
+int staging_init() {
+  if (g_stage.pool) return 0;
+  for (int i = 0; i < Staging::R; ++i) {
+    SPX_CUDA(cudaHostAlloc(&g_stage.buf[i], Staging::CHUNK, cudaHostAllocPortable));
+    SPX_CUDA(cudaEventCreateWithFlags(&g_stage.ev[i], cudaEventDisableTiming));
+  }
+  int n = (int)std::thread::hardware_concurrency();
+  const char* e = getenv("SPX_COPY_THREADS");
+  if (e) n = atoi(e);
+  if (n < 1) n = 1;
+  if (n > 32) n = 32;
+  g_stage.pool = new CopyPool(n);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spx_h2d_staged(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (bytes < (4u << 20)) return spx_memcpy_h2d(dst, src, bytes, stream);
+  std::lock_guard<std::mutex> g(g_stage.m);
+  if (staging_init()) return -1;
+  int k = 0;
+  for (uint64_t o = 0; o < bytes; o += Staging::CHUNK, k = (k + 1) % Staging::R) {
+    const uint64_t n = bytes - o < Staging::CHUNK ? bytes - o : Staging::CHUNK;
+    SPX_CUDA(cudaEventSynchronize(g_stage.ev[k]));          // the slot's previous DMA is done
+    g_stage.pool->copy(g_stage.buf[k], static_cast<const char*>(src) + o, n);
+    SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst + o), g_stage.buf[k], n, cudaMemcpyHostToDevice, s));
+    SPX_CUDA(cudaEventRecord(g_stage.ev[k], s));
+  }
+  return 0;
+}
+
+int spx_d2h_staged(void* dst, uint64_t src, uint64_t bytes, uint64_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (bytes < (4u << 20)) {
+    if (spx_memcpy_d2h(dst, src, bytes, stream)) return -1;
+    SPX_CUDA(cudaStreamSynchronize(s));
+    return 0;
+  }
+  std::lock_guard<std::mutex> g(g_stage.m);
+  if (staging_init()) return -1;
+  const uint64_t nchunks = (bytes + Staging::CHUNK - 1) / Staging::CHUNK;
+  auto issue = [&](uint64_t c) -> int {
+    const uint64_t o = c * Staging::CHUNK, n = bytes - o < Staging::CHUNK ? bytes - o : Staging::CHUNK;
+    const int k = (int)(c % Staging::R);
+    SPX_CUDA(cudaMemcpyAsync(g_stage.buf[k], reinterpret_cast<const void*>(src + o), n, cudaMemcpyDeviceToHost, s));
+    SPX_CUDA(cudaEventRecord(g_stage.ev[k], s));
+    return 0;
+  };
+  uint64_t issued = 0;
+  for (; issued < nchunks && issued < (uint64_t)Staging::R; ++issued)
+    if (issue(issued)) return -1;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    const uint64_t o = c * Staging::CHUNK, n = bytes - o < Staging::CHUNK ? bytes - o : Staging::CHUNK;
+    const int k = (int)(c % Staging::R);
+    SPX_CUDA(cudaEventSynchronize(g_stage.ev[k]));
+    g_stage.pool->copy(static_cast<char*>(dst) + o, g_stage.buf[k], n);
+    if (issued < nchunks && issue(issued++)) return -1;        // the slot is free again
+  }
+  return 0;
+}
+
 int spx_host_copy(void* dst, const void* src, uint64_t bytes, int threads) {
   if (threads <= 1 || bytes < (8u << 20)) {
     memcpy(dst, src, bytes);
@@ -408,6 +577,60 @@ int spx_comm_destroy(int comm) {
   return 0;
 }
 
+int spx_comm_async_error(int comm, int* out) {
+  *out = 0;
+  if (comm < 0 || comm >= (int)g_comms.size() || !g_comms[comm]) return 0;
+  int e = 0;
+  SPX_NCCL(N.async_error(g_comms[comm], &e));
+  *out = e;
+  return 0;
+}
+
+int spx_comm_abort(int comm) {
+  if (comm < 0 || comm >= (int)g_comms.size() || !g_comms[comm]) return 0;
+  N.abort(g_comms[comm]);
+  g_comms[comm] = nullptr;
+  return 0;
+}
+
+int spx_peer_error(int* out);
+
+// Wait for `stream` while watching for failures: an NCCL asynchronous error on
+// any live communicator (ncclCommGetAsyncError; the communicators are then
+// aborted so their kernels return), a peer-collective barrier that gave up
+// (spx_peer_error), or no completion within timeout_s (0: none).  Returns 0
+// when the stream completed cleanly.
+int spx_stream_sync_watch(uint64_t stream, double timeout_s) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int it = 0;; ++it) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return spx_set_error("stream: %s", cudaGetErrorString(q));
+    if (N.h && (it & 15) == 0) {
+      for (size_t c = 0; c < g_comms.size(); ++c) {
+        if (!g_comms[c]) continue;
+        int e = 0;
+        if (N.async_error(g_comms[c], &e) == 0 && e != 0 && e != 7 /* ncclInProgress */) {
+          for (size_t k = 0; k < g_comms.size(); ++k) spx_comm_abort((int)k);
+          return spx_set_error("NCCL asynchronous error %d (%s) on communicator %zu; communicators aborted", e,
+                               N.errstr(e), c);
+        }
+      }
+    }
+    int pe = 0;
+    spx_peer_error(&pe);
+    if (pe) return spx_set_error("peer collective barrier (phase %d) timed out: a member never arrived", pe - 1);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s > 0 && el > timeout_s) return spx_set_error("stream did not complete within %.0f s", timeout_s);
+    std::this_thread::sleep_for(std::chrono::microseconds(it < 100 ? 20 : 500));
+  }
+  int pe = 0;
+  spx_peer_error(&pe);
+  if (pe) return spx_set_error("peer collective barrier (phase %d) timed out: a member never arrived", pe - 1);
+  return 0;
+}
+
 int spx_plan_create(uint64_t* out) {
   *out = reinterpret_cast<uint64_t>(new Plan());
   return 0;
@@ -425,10 +648,15 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
   r.params.assign(static_cast<const uint8_t*>(params), static_cast<const uint8_t*>(params) + bytes);
   if (kind == SPX_K_EW) {
     const char* e = getenv("SPX_EW_STATIC");
-    if (!(e && e[0] == '0'))
+    if (!(e && e[0] == '0') && reinterpret_cast<const spx_ew_params*>(r.params.data())->dtype == SPX_DT_F32)
       r.path = 1 + spx_ew_static_match(*reinterpret_cast<const spx_ew_params*>(r.params.data()));
   }
-  if (kind == SPX_K_GEMM) {
+  if (kind == SPX_K_GEMM && reinterpret_cast<const spx_gemm_params*>(r.params.data())->dtype == SPX_DT_I32) {
+    const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
+    if (g.splits > 1 || g.epi != SPX_EPI_NONE || g.h3_shared || (g.path != 0 && g.path != 2))
+      return spx_set_error("gemm %dx%dx%d: int32 GEMMs run on the SIMT path only", g.M, g.N, g.K);
+    r.path = 4;
+  } else if (kind == SPX_K_GEMM) {
     const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
     const bool tc_ok = spx_gemm_tc_supported(g);
     if (g.path == 1 && !tc_ok) return spx_set_error("gemm %dx%dx%d: tcgen05 path requested but operands unsupported", g.M, g.N, g.K);

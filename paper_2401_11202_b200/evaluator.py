@@ -168,7 +168,9 @@ def fingerprint(module, func="main") -> str:
 
 class PlanCache:
     """LRU of compiled Executables.  Bounded by entry count (SPX_PLAN_CACHE,
-    default 4) and by arena bytes (SPX_PLAN_CACHE_BYTES, default 64 GiB);
+    default 4) and by arena bytes (SPX_PLAN_CACHE_BYTES, default 160 GiB of
+    the B200's 180 GB: one C3-sized plan, 96 GB, must stay resident; a build
+    that runs out of memory evicts everything and retries once);
     SPX_PLAN_CACHE=0 disables caching (every call builds and frees its plan)."""
 
     def __init__(self):
@@ -178,7 +180,7 @@ class PlanCache:
     @staticmethod
     def limits():
         return (int(os.environ.get("SPX_PLAN_CACHE", "4")),
-                int(os.environ.get("SPX_PLAN_CACHE_BYTES", str(64 << 30))))
+                int(os.environ.get("SPX_PLAN_CACHE_BYTES", str(160 << 30))))
 
     def bytes(self) -> int:
         return sum(ex.dev_stride * ex.ndev for ex in self.entries.values())

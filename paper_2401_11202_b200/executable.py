@@ -52,6 +52,9 @@ class Executable:
         arithmetic type of the call (np.result_type of the inputs,
         evaluator._cdtype): float32 or int32."""
         self.dtype = np.dtype(dtype)
+        self.dt = R.DT_I32 if self.dtype == np.dtype(np.int32) else R.DT_F32
+        if self.dt == R.DT_I32 and comm_mode != "local":
+            raise TypeError("int32 programs run in local mode (the drop-in spmd_interpret / interpret)")
         self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode, dtype=self.dtype).compile()
         self.dry = dry
         self.device = None if dry else (device or R.Device(0))
@@ -59,6 +62,7 @@ class Executable:
         self.mesh_size = module.mesh.device_count if getattr(module, "mesh", None) is not None else 1
         self.gemm_path = gemm_path
         self.comms = comms or {}
+        self._own_comms = False
         import os
         if overlap is None:
             overlap = os.environ.get("SPX_OVERLAP", "1") != "0"
@@ -83,6 +87,7 @@ class Executable:
         self._alloc()
         if comm_mode == "nccl" and comm_factory is not None:
             self.comms = comm_factory(self)
+            self._own_comms = not dry
         self._tables = []
         self._records = []
         self._krange = []          # per compiler kernel: [first record, end record)
@@ -314,9 +319,17 @@ class Executable:
         p.n_prog = len(prog.insns)
         for i, (op, a, b, dst, imm) in enumerate(prog.insns):
             p.prog[i].op, p.prog[i].a, p.prog[i].b, p.prog[i].dst = op, a, b, dst
-            p.imm[i] = imm
+            p.imm[i] = self._imm(imm)
         p.vec = vec
+        p.dtype = self.dt
         return p
+
+    def _imm(self, v) -> float:
+        """Immediate as stored in the record: the f32 value, or the int32 bits
+        (SPX_DT_I32 records reinterpret imm[])."""
+        if self.dt == R.DT_I32:
+            return float(np.array([v], dtype=np.int32).view(np.float32)[0])
+        return float(v)
 
     def _emit(self):
         c = self.comp
@@ -359,7 +372,7 @@ class Executable:
         """The block-scaled 3xFP16 kernel takes this GEMM (runtime.cu h3_default,
         gemm_h3.cu spx_gemm_h3_supported, gemm_tc.cu spx_gemm_tc_supported)."""
         import os
-        if self.gemm_path != 0 or os.environ.get("SPX_GEMM_H3", "1") == "0":
+        if self.gemm_path != 0 or os.environ.get("SPX_GEMM_H3", "1") == "0" or self.dt != R.DT_F32:
             return False
         if d.get("splits", 1) != 1 or d.get("epi") is not None or d.get("sk_inkernel") or not d.get("tc_ok"):
             return False
@@ -509,16 +522,23 @@ class Executable:
         side: dict = {}
         crit_coll = os.environ.get("SPX_SIDE_ALL_COLLECTIVES", "0") == "1"
         prefetch = os.environ.get("SPX_PREFETCH", "1") != "0"
+        # Forward progress by construction: every cross-rank
+        # collective of a rank -- peer kernels and NCCL calls alike -- is issued
+        # on ONE stream, in program order, identical on every rank.  A rank then
+        # holds at most one spinning collective at a time, and the k-th
+        # collective of every member is launched only after all its members
+        # completed their earlier ones and its local producers finished (which
+        # need no remote progress), so no cycle of SM residency and cross-stream
+        # waits can form, whatever the compute streams run (side-stream GEMMs
+        # included).  SPX_COLL_ONE_STREAM=0 restores the round-1 placement
+        # (critical-path collectives on the main stream).
+        one = c.comm_mode == "nccl" and os.environ.get("SPX_COLL_ONE_STREAM", "1") != "0"
         args = set(c.arg_bufs)
         if c.comm_mode == "nccl":
-            # activation collectives on the critical path stay on the main
-            # stream (a cross-stream hop only adds latency); collectives of
-            # function arguments (ZeRO-3 parameter all-gathers) depend on no
-            # compute and are prefetched on the collective stream
             for i in reversed(range(len(ks))):
                 k = ks[i]
                 if k.kind == "coll" and k.data["kind"] != "all_slice":
-                    if (crit_coll or off_critical(i, side)
+                    if (one or crit_coll or off_critical(i, side)
                             or (prefetch and k.data["kind"] == "all_gather" and k.ins
                                 and all(b in args for b in k.ins))):
                         side[i] = self.COMM
@@ -527,10 +547,10 @@ class Executable:
         for i, k in enumerate(ks):
             if k.kind == "split" and k.data["src"][0] in args:
                 side[i] = self.COMPUTE
-        # side-stream GEMMs (whole-SM CTAs) only below 4 ranks: with spinning
-        # peer kernels on two streams they can close a cross-rank residency
-        # cycle (known issue); SPX_CONCURRENT_GEMM overrides
-        cg_default = "0" if c.comm_mode == "nccl" and self.mesh_size >= 4 else "1"
+        # side-stream GEMMs (whole-SM CTAs): with every collective on one stream
+        # they cannot close a cross-rank residency cycle; under the round-1
+        # placement (SPX_COLL_ONE_STREAM=0) only below 4 ranks
+        cg_default = "0" if c.comm_mode == "nccl" and not one and self.mesh_size >= 4 else "1"
         if os.environ.get("SPX_CONCURRENT_GEMM", cg_default) != "0":
             for i in reversed(range(len(ks))):
                 # in-kernel split-K GEMMs share one workspace: main stream only
@@ -566,6 +586,12 @@ class Executable:
                 sc = (self.scratch_off, self.zero_off)
                 r.append(sc)
                 w.append(sc)
+            if k.data.get("stage"):
+                # NCCL relayouts share the staging region: order
+                # every collective that uses it
+                st_iv = (self.stage_a, self.stage_b + self.stage_elems)
+                r.append(st_iv)
+                w.append(st_iv)
             kin.append(r)
             kout.append(w)
 
@@ -627,7 +653,8 @@ class Executable:
         x.n_prog = len(prog.insns)
         for i, (op, a, b, dst, imm) in enumerate(prog.insns):
             x.prog[i].op, x.prog[i].a, x.prog[i].b, x.prog[i].dst = op, a, b, dst
-            x.imm[i] = imm
+            x.imm[i] = self._imm(imm)
+        x.dtype = self.dt
         p.monoid = 0 if k.data["monoid"] == "sum" else 1
         p.n_kept, p.n_red = len(kd), len(rd)
         p.n_out = _prod(in_dims[d] for d in kept)
@@ -707,6 +734,7 @@ class Executable:
             p.h3_b_scl = p.h3_b_off + d["h3b_scl"]
         # with collectives overlapped on a side stream, leave SMs for NCCL's CTAs
         p.reserve_sms = self.reserve_sms
+        p.dtype = self.dt
         self._records.append((R.K_GEMM, p))
 
     # ---- in-GPU collectives (spmd_interp.py:74-123 as group kernels) ----
@@ -794,6 +822,7 @@ class Executable:
             for p in range(self.ndev):
                 base[p] = sum(c._chunk_index(coords[p], apd[j]) * out_dims[j] * S[j]
                               for j in range(len(out_dims)))
+        r.dtype = self.dt
         r.src = self._tref(self._ptrs(src))
         r.members = self._tref(members.reshape(-1))
         r.base_off = self._tref(base)
@@ -928,6 +957,7 @@ class Executable:
             if direct:
                 self._nccl(R.NCCL_ALLGATHER, comm, src_a, out_a, nloc)
                 return
+            k.data["stage"] = True
             self._nccl(R.NCCL_ALLGATHER, comm, src_a, sa, nloc)
             table = [self.base + self.zero_off * 4] * _prod(nper)
             for j, cb in enumerate(combo_of):
@@ -946,6 +976,7 @@ class Executable:
                 self._nccl(R.NCCL_REDUCESCATTER, comm, src_a, out_a, nout, monoid)
                 return
             # relayout send buffer as [member j][chunk of member j]
+            k.data["stage"] = True
             self._gather1(sa, [n] + out_dims, [1] + out_dims, [1] + [0] * len(out_dims),
                           [0] + list(S), [src_a + o * 4 for o in offs])
             self._nccl(R.NCCL_REDUCESCATTER, comm, sa, out_a, nout, monoid)
@@ -955,6 +986,7 @@ class Executable:
             piece = list(in_dims)
             piece[sd] = out_dims[sd]
             npiece = _prod(piece)
+            k.data["stage"] = True
             chunk = [c._chunk_index(coords[m], list(attrs["axes"])) for m in grp]
             self._gather1(sa, [n] + piece, [1] + piece, [1] + [0] * len(piece), [0] + list(S),
                           [src_a + ch * out_dims[sd] * S[sd] * 4 for ch in chunk])
@@ -972,11 +1004,17 @@ class Executable:
 
     # --------------------------------------------------------------- host I/O
     def upload_args(self, per_device: list[dict]):
-        """per_device[p][arg] = local numpy array for hosted device p."""
+        """per_device[p][arg] = local numpy array for hosted device p.  Arrays
+        in pinned memory (results of an earlier call, runtime.PinnedPool) go
+        by direct async DMA; pageable ones through the pinned staging ring."""
+        pool = R.pinned_pool()
         for p in range(self.ndev):
             for a in self.comp.arg_bufs:
                 arr = np.ascontiguousarray(per_device[p][a], dtype=self.dtype)
-                self.device.h2d(self.addr(p, a), arr)
+                if pool.contains(arr):
+                    self.device.h2d(self.addr(p, a), arr)
+                else:
+                    self.device.h2d_staged(self.addr(p, a), arr)
 
     def download_results(self) -> list[list[np.ndarray]]:
         """[result j][device p] local arrays."""
@@ -986,8 +1024,12 @@ class Executable:
             dims = tuple(f.result_types[j].dims)
             per = []
             for p in range(self.ndev):
-                a = np.empty(dims, dtype=self.dtype)
-                self.device.d2h(a, self.addr(p, b))
+                a = R.pinned_pool().array(dims, self.dtype)
+                if a is None:
+                    a = np.empty(dims, dtype=self.dtype)
+                    self.device.d2h_staged(a, self.addr(p, b))
+                else:
+                    self.device.d2h(a, self.addr(p, b))       # direct async DMA, one sync below
                 per.append(a)
             out.append(per)
         self.device.sync()
@@ -1058,6 +1100,11 @@ class Executable:
         if self.dry:
             return
         self.plan.destroy()
+        if self._own_comms:
+            for cm in set(self.comms.values()):
+                R.call(R.load().spx_comm_destroy, int(cm))
+            self.comms = {}
+            self._own_comms = False
         for ptr in self._peer_handles:
             R.call(R.load().spx_ipc_close, ptr)
         self._peer_handles = []

@@ -111,8 +111,9 @@ class Compiler:
     def __init__(self, module, func="main", devices=None, comm_mode="local", dtype=np.float32):
         self.module = module
         self.dtype = np.dtype(dtype)
-        if self.dtype != np.dtype(np.float32):
-            raise TypeError(f"compute type {self.dtype}: the backend computes float32")
+        if self.dtype not in (np.dtype(np.float32), np.dtype(np.int32)):
+            raise TypeError(f"compute type {self.dtype}: the backend computes float32 or int32")
+        self.is_int = self.dtype == np.dtype(np.int32)
         self.f = module.func(func)
         self.mesh = module.mesh
         n_mesh = self.mesh.device_count if self.mesh is not None else 1
@@ -238,23 +239,28 @@ class Compiler:
         dims = tuple(op.result_types[0].dims) if op.result_types else ()
         D = self.desc
         if k == "constant":
-            D[r] = Desc("const", dims, value=np.float32(op.attrs["value"]))
+            # np.full(dims, value, cdtype) (interp.py:39-41): the value cast by numpy itself
+            D[r] = Desc("const", dims, value=np.full((1,), op.attrs["value"], dtype=self.dtype)[0])
             return
         if k == "tag":
             D[r] = D[op.operands[0]]
             return
         if k in EW_KINDS:
+            if k == "exp" and self.is_int:
+                raise TypeError("exp of int32 computes in float64 in the reference (np.exp); "
+                                "the backend computes float32 or int32")
             kids = [self._leaf_of(D[o]) for o in op.operands]
-            if all(isinstance(c, np.float32) for c in kids):          # constant folding
+            if all(_is_const(c) for c in kids):          # constant folding (numpy's own arithmetic)
                 with np.errstate(all="ignore"):
+                    a = np.array(kids, dtype=self.dtype)
                     if k == "add":
-                        v = np.float32(kids[0] + kids[1])
+                        v = (a[:1] + a[1:2])[0]
                     elif k == "mul":
-                        v = np.float32(kids[0] * kids[1])
+                        v = (a[:1] * a[1:2])[0]
                     elif k == "neg":
-                        v = np.float32(-kids[0])
+                        v = (-a[:1])[0]
                     else:
-                        v = np.float32(np.exp(kids[0]))
+                        v = np.exp(a[:1])[0]
                 D[r] = Desc("const", dims, value=v)
                 self.folded_flops += op_flops(op, [self.types[o] for o in op.operands])
                 return
@@ -340,8 +346,8 @@ class Compiler:
         out = self._new_buf(dims, "mm")
         M, K = a_dims
         N = b_dims[1]
-        splits = self._splitk(M, N, K, aoff, lda, boff, ldb)
-        sk = self._splitk_inkernel(M, N, K, aoff, lda, boff, ldb) if splits == 1 and not at else 1
+        splits = 1 if self.is_int else self._splitk(M, N, K, aoff, lda, boff, ldb)
+        sk = self._splitk_inkernel(M, N, K, aoff, lda, boff, ldb) if splits == 1 and not at and not self.is_int else 1
         if sk > 1:
             # few-tile activation GEMM on the critical path: partials reduced
             # inside the kernel (no workspace reduction launch)
@@ -351,7 +357,7 @@ class Compiler:
         elif splits == 1:
             k = Kernel("gemm", [out], {ab, bb}, op_index=i,
                        data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt), splits=1,
-                                 tc_ok=self._tc_ok(M, N, K, aoff, lda, boff, ldb)))
+                                 tc_ok=not self.is_int and self._tc_ok(M, N, K, aoff, lda, boff, ldb)))
             self.kernels.append(k)
         else:
             # split-K: partial products into a [splits, M, N] workspace, summed
@@ -417,6 +423,9 @@ class Compiler:
 
     # ----------------------------------------------------------------- reduce
     def _lower_reduce(self, i, op, dims):
+        if self.is_int and op.attrs.get("monoid", "sum") == "sum":
+            raise TypeError("reduce sum of int32 widens to int64 in the reference (np.sum); "
+                            "the backend computes float32 or int32")
         x = self.desc[op.operands[0]]
         in_dims = self.types[op.operands[0]]
         root = self._leaf_of(x)
@@ -533,7 +542,7 @@ class Compiler:
         bandwidth with so little memory-level parallelism per SM).  See
         DESIGN.md, "GEMM epilogue fusion"."""
         import os
-        if os.environ.get("SPX_EPILOGUE", "0") == "0":
+        if os.environ.get("SPX_EPILOGUE", "0") == "0" or self.is_int:
             return
         kinds = {int(x) for x in os.environ.get("SPX_EPILOGUE_KINDS", "1,2,3,4").split(",") if x}
         ks = self.kernels
@@ -645,7 +654,7 @@ class Compiler:
 
 
 def _is_const(e):
-    return isinstance(e, (np.float32, float))
+    return isinstance(e, (np.float32, np.int32, float))
 
 
 def _match_epilogue(exprs: dict, outs: list, C: str, M: int, N: int):
@@ -764,13 +773,13 @@ class Program:
         def val(x):
             if isinstance(x, Leaf):
                 return leaf(x)
-            if isinstance(x, (np.float32, float)):
+            if _is_const(x):
                 return emit(R.OP["IMM"], None, None, x)
             if x.uid in memo:
                 return memo[x.uid]
             if x.op in ("add", "mul"):
                 a, b = x.kids
-                ca, cb = isinstance(a, (np.float32, float)), isinstance(b, (np.float32, float))
+                ca, cb = _is_const(a), _is_const(b)
                 if cb and not ca:
                     r = emit(R.OP["ADDI" if x.op == "add" else "MULI"], val(a), None, b)
                 elif ca and not cb:

@@ -36,6 +36,7 @@ class EwParams(C.Structure):
     _fields_ = [("base", C.c_uint64), ("dev_stride", C.c_int64),
                 ("ndev", C.c_int32), ("rank", C.c_int32), ("n_in", C.c_int32),
                 ("n_out", C.c_int32), ("n_prog", C.c_int32), ("vec", C.c_int32),
+                ("dtype", C.c_int32), ("dtype_pad", C.c_int32),
                 ("dims", I64R), ("numel", C.c_int64),
                 ("inp", View * MAX_IN),
                 ("out_off", C.c_int64 * MAX_OUT), ("out_reg", C.c_int32 * MAX_OUT),
@@ -66,7 +67,8 @@ class GemmParams(C.Structure):
                 ("sk_mode", C.c_int32), ("sk_pad", C.c_int32),
                 ("ws_off", C.c_int64), ("flag_off", C.c_int64),
                 ("h3_shared", C.c_int32), ("h3_splitk", C.c_int32),
-                ("h3_a_off", C.c_int64), ("h3_a_scl", C.c_int64), ("h3_b_off", C.c_int64), ("h3_b_scl", C.c_int64)]
+                ("h3_a_off", C.c_int64), ("h3_a_scl", C.c_int64), ("h3_b_off", C.c_int64), ("h3_b_scl", C.c_int64),
+                ("dtype", C.c_int32), ("dtype_pad", C.c_int32)]
 
 
 class SplitParams(C.Structure):
@@ -76,6 +78,7 @@ class SplitParams(C.Structure):
                 ("dst_off", C.c_int64), ("pitch", C.c_int64), ("scl_off", C.c_int64)]
 
 
+DT_F32, DT_I32 = 0, 1
 EPI_NONE, EPI_ADD, EPI_SQUARE, EPI_MULSCALE, EPI_MOMENTUM = 0, 1, 2, 3, 4
 
 
@@ -90,7 +93,7 @@ class CreduceParams(C.Structure):
     _fields_ = [("ndev", C.c_int32), ("rank", C.c_int32), ("n_members", C.c_int32),
                 ("monoid", C.c_int32), ("dims", I64R), ("sstride", I64R), ("numel", C.c_int64),
                 ("src", C.c_uint64), ("members", C.c_uint64), ("base_off", C.c_uint64),
-                ("dst", C.c_uint64)]
+                ("dst", C.c_uint64), ("dtype", C.c_int32), ("dtype_pad", C.c_int32)]
 
 
 class NcclParams(C.Structure):
@@ -136,6 +139,8 @@ EXPORTS = [
     "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
     "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats",
     "spx_host_register", "spx_host_unregister", "spx_host_copy",
+    "spx_h2d_staged", "spx_d2h_staged",
+    "spx_comm_async_error", "spx_comm_abort", "spx_peer_error", "spx_peer_error_clear", "spx_stream_sync_watch",
 ]
 
 _lib = None
@@ -189,6 +194,11 @@ def load(build_if_missing: bool = True):
         "spx_plan_reset_stats": [C.c_uint64],
         "spx_host_register": [C.c_void_p, C.c_uint64], "spx_host_unregister": [C.c_void_p],
         "spx_host_copy": [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int],
+        "spx_h2d_staged": [C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64],
+        "spx_d2h_staged": [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64],
+        "spx_comm_async_error": [C.c_int, C.POINTER(C.c_int)], "spx_comm_abort": [C.c_int],
+        "spx_peer_error": [C.POINTER(C.c_int)], "spx_peer_error_clear": [],
+        "spx_stream_sync_watch": [C.c_uint64, C.c_double],
     }
     for name, args in sigs.items():
         getattr(lib, name).argtypes = args
@@ -243,11 +253,29 @@ class Device:
         assert arr.flags.c_contiguous
         call(self.lib.spx_memcpy_d2h, arr.ctypes.data, src, arr.nbytes, self.stream)
 
+    def h2d_staged(self, dst: int, arr: np.ndarray):
+        """Pageable host array -> device through pinned staging (spx_h2d_staged)."""
+        arr = np.ascontiguousarray(arr)
+        call(self.lib.spx_h2d_staged, dst, arr.ctypes.data, arr.nbytes, self.stream)
+
+    def d2h_staged(self, arr: np.ndarray, src: int):
+        """Device -> pageable host array through pinned staging; returns when
+        `arr` holds the data (spx_d2h_staged)."""
+        assert arr.flags.c_contiguous
+        call(self.lib.spx_d2h_staged, arr.ctypes.data, src, arr.nbytes, self.stream)
+
     def memset(self, dst: int, nbytes: int, value: int = 0):
         call(self.lib.spx_memset, dst, value, nbytes, self.stream)
 
     def sync(self):
         call(self.lib.spx_stream_sync, self.stream)
+
+    def sync_watch(self, timeout_s: float | None = None):
+        """Wait for the stream while watching for NCCL asynchronous errors and
+        peer-collective timeouts (spx_stream_sync_watch); raises BackendError."""
+        if timeout_s is None:
+            timeout_s = float(os.environ.get("SPX_SYNC_TIMEOUT_S", "900"))
+        call(self.lib.spx_stream_sync_watch, self.stream, timeout_s)
 
     def event(self) -> int:
         e = C.c_uint64()
@@ -293,6 +321,81 @@ class Device:
         for p in self._pinned:
             self.lib.spx_host_free(C.c_void_p(p))
         self._pinned = []
+
+
+class PinnedPool:
+    """Page-locked host arrays for the drop-in call's results.
+
+    `array()` hands out a NEW numpy array (owned by the caller) backed by a
+    pinned buffer; when the caller drops the last reference the buffer goes
+    back to the pool (weakref finalizer) and serves a later result of the same
+    size.  Results then come back by direct DMA (~57 GB/s on this box) instead
+    of pageable copies into freshly faulted pages (~5 GB/s), and a result fed
+    back as the next call's input -- a training loop's parameters and momenta
+    -- goes in by direct DMA too (`contains`).  Bounded by
+    SPX_PINNED_POOL_BYTES (default 64 GiB); beyond it callers get ordinary
+    arrays.  SPX_PINNED_POOL=0 disables it."""
+
+    def __init__(self, lib):
+        import threading
+        self.lib = lib
+        self.limit = int(os.environ.get("SPX_PINNED_POOL_BYTES", str(64 << 30)))
+        self.enabled = os.environ.get("SPX_PINNED_POOL", "1") != "0"
+        self.free: dict[int, list[int]] = {}
+        self.ranges: dict[int, int] = {}       # ptr -> nbytes of every pinned buffer
+        self._starts: list[int] = []
+        self.total = 0
+        self.lock = threading.Lock()
+
+    def _release(self, ptr: int, nbytes: int):
+        with self.lock:
+            self.free.setdefault(nbytes, []).append(ptr)
+
+    def array(self, shape, dtype) -> np.ndarray | None:
+        dtype = np.dtype(dtype)
+        nbytes = max(16, int(np.prod(shape)) * dtype.itemsize)
+        if not self.enabled:
+            return None
+        with self.lock:
+            lst = self.free.get(nbytes)
+            ptr = lst.pop() if lst else None
+            if ptr is None:
+                if self.total + nbytes > self.limit:
+                    return None
+                p = C.c_void_p()
+                call(self.lib.spx_host_alloc, nbytes, C.byref(p))
+                ptr = p.value
+                self.total += nbytes
+                self.ranges[ptr] = nbytes
+                import bisect
+                bisect.insort(self._starts, ptr)
+        import weakref
+        buf = (C.c_uint8 * nbytes).from_address(ptr)
+        weakref.finalize(buf, self._release, ptr, nbytes)
+        n = int(np.prod(shape))
+        return np.frombuffer(buf, dtype=dtype, count=n).reshape(shape)
+
+    def contains(self, arr: np.ndarray) -> bool:
+        """Is `arr` (contiguous) inside a pinned buffer of this pool?"""
+        if not self._starts:
+            return False
+        import bisect
+        a = arr.ctypes.data
+        i = bisect.bisect_right(self._starts, a) - 1
+        if i < 0:
+            return False
+        s = self._starts[i]
+        return a + arr.nbytes <= s + self.ranges[s]
+
+
+_POOL = None
+
+
+def pinned_pool() -> PinnedPool:
+    global _POOL
+    if _POOL is None:
+        _POOL = PinnedPool(load())
+    return _POOL
 
 
 class NativePlan:

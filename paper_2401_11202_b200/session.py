@@ -211,7 +211,10 @@ class Session:
         self.ex.plan.replay()
 
     def sync(self):
-        self.device.sync()
+        if self.mode == "nccl":
+            self.device.sync_watch()      # NCCL async errors / peer timeouts raise instead of hanging
+        else:
+            self.device.sync()
 
     def launch_count(self) -> int:
         return self.ex.plan.launch_count()
@@ -224,7 +227,11 @@ class Session:
         going back to it -- the drop-in call's data movement (spmd_interpret:
         shard, copy in, run, copy out) for this process's mesh devices:
         returns [result j][hosted device] local arrays."""
-        self.ex.upload_args(self.local_inputs(global_inputs))
+        return self.call_local(self.local_inputs(global_inputs))
+
+    def call_local(self, local_inputs: list[dict]):
+        """`call` with inputs already sharded: local_inputs[hosted device][arg]."""
+        self.ex.upload_args(local_inputs)
         if self.ex.plan.captured:
             self.ex.plan.replay()
         else:

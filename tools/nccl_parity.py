@@ -67,6 +67,56 @@ def main():
                 except DivergenceError as e:
                     if case.get("error") != "DivergenceError":
                         fails.append((case["key"], str(e)))
+    # the BASELINE configs' own programs at this world size, default knobs:
+    # eager run and graph replay vs the oracle, executed collectives vs the
+    # simulator's counts (runtime counters)
+    from oracle import spmd_oracle as O
+    from paper_2401_11202_b200.programs import load_program, synthetic_inputs
+    cfg = {2: [("c1_mlp_bp_B2", 0.25), ("c2_tf8_bp_B2", 0.02), ("c3_tf1_bpz3_B2", 0.02), ("c4_unet_bpz2_B2", 0.05),
+               ("c5_tf8_bpz3_B2", 0.02)],
+           4: [("c2_tf8_bpmp_B2M2", 0.02), ("c3_tf1_bpz3_B4", 0.02), ("c4_unet_bpz2_B4", 0.05),
+               ("c5_tf8_bpmpz3_B2M2", 0.02)],
+           8: [("c2_tf1_bpmp_B2M4", 0.02), ("c3_tf1_bpz3_B8", 0.02), ("c4_unet_bpz2_B8", 0.05),
+               ("c5_tf1_bpmpz3emb_B2M2E2", 0.02)]}.get(world, [])
+    only = os.environ.get("PARITY_CONFIGS")
+    for name, scale in cfg:
+        if only and name not in only.split(","):
+            continue
+        prog = load_program(name)
+        m, spec = prog.local, prog.sharding
+        ins = synthetic_inputs(prog.dense, seed=0, scale=scale)
+        sess = Session(m, spec, mode="nccl", device=dev, rank=rank, world=world, local_rank=local)
+        sess.load(ins)
+        sess.run()
+        sess.sync()
+        eager = [r[0] for r in sess.results()]
+        sess.capture()
+        sess.step()
+        sess.sync()
+        replay = [r[0] for r in sess.results()]
+        work = sess.ex.work_report()
+        pred = sess.ex.issued_per_run()["coll"]
+        sess.close()
+        same = all(np.array_equal(a, b) for a, b in zip(eager, replay))
+        allres = [None] * world
+        dist.all_gather_object(allres, (replay, same, work["collectives"]["executed"] == pred))
+        if rank == 0:
+            n += 1
+            coords = m.mesh.coords()
+            want = O.spmd_interpret(m, spec, ins)
+            try:
+                got = [unshard([allres[r][0][j] for r in range(world)], spec.results[j], m.mesh, coords,
+                               1e-5, f"result {j}") for j in range(len(want))]
+                worst = max(relative_error(g, w) for g, w in zip(got, want))
+                fin = all(np.all(np.isfinite(g)) for g in got)
+                print(f"{name}: worst rel err {worst:.3e} finite {fin} replay==eager "
+                      f"{all(a[1] for a in allres)} counters==records {all(a[2] for a in allres)} "
+                      f"executed {work['collectives']['executed']} program {work['collectives']['program']}",
+                      flush=True)
+                if not worst < 1e-5 or not fin or not all(a[1] and a[2] for a in allres):
+                    fails.append((name, worst))
+            except DivergenceError as e:
+                fails.append((name, str(e)))
     # large all_reduce over every rank (the peer-memory kernels: one-shot for 2
     # members, two-shot for 4 / 8): bit-identical to the member-order fold
     for rows in (1024, 257):

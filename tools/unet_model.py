@@ -11,8 +11,10 @@ The reference IR has no convolution (ir.py:18-21), so this is a
   * activation      = square (like the model zoo, models.py:73-77)
 with the backward pass written by hand (as models.py does; no autodiff) and
 the momentum-SGD update of models._Grad.momentum_update (models.py:79-85).
-Gradients are validated against central finite differences with the
-reference's own `grads_by_finite_difference` (tests/test_unet_model.py).
+Gradients are validated against central finite differences in float64 by
+tests/test_unet_model.py (the method of the reference's
+`grads_by_finite_difference`, conftest.py:99-139, at unit input scale and
+per-tensor relative error -- see that test for why).
 
 Needs the reference importable (PYTHONPATH=/root/reference/pkg/src).
 """
