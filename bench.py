@@ -152,6 +152,15 @@ def sum_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
+_T0 = time.time()
+
+
+def log(msg: str):
+    """Progress on stderr (one line per phase and rank): a hang shows where it is."""
+    sys.stderr.write(f"[bench rank {os.environ.get('RANK', '0')} +{time.time() - _T0:7.1f}s] {msg}\n")
+    sys.stderr.flush()
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -196,7 +205,7 @@ def reference_step(wl, n, prog):
     return t, f"one full step of {prog.name} through {what}"
 
 
-def e2e_call(sess, prog, base, inputs, n, dist, budget_s, max_steps, batch):
+def e2e_call(sess, prog, base, inputs, n, dist, budget_s, max_steps, batch, feedback=False):
     """The metric through the call a user makes, as a training loop: every
     input copied in from host memory and every result copied out to host
     memory each step, the updated parameters and momenta (results `new_X`)
@@ -232,7 +241,7 @@ def e2e_call(sess, prog, base, inputs, n, dist, budget_s, max_steps, batch):
         what = "Session.call_local(host inputs) on every rank (copy in, replay, copy out)"
         spec = prog.sharding
     fb = {}
-    for j, r in enumerate(f.results):
+    for j, r in enumerate(f.results if feedback else []):
         a = r[4:] if r.startswith("new_") else None
         if a in cur and tuple(f.result_types[j].dims) == tuple(cur[a].shape) and \
                 (spec is None or spec.results[j] == spec.args[a]):
@@ -263,10 +272,11 @@ def e2e_call(sess, prog, base, inputs, n, dist, budget_s, max_steps, batch):
     return {"value": batch / (wall / k), "unit": "samples/s", "steps": k, "ms_per_step": wall / k * 1e3,
             "h2d_bytes_per_step": int(sum_over_ranks(dist, h2d)), "d2h_bytes_per_step": int(sum_over_ranks(dist, d2h)),
             "outputs_finite": finite, "fed_back": len(fb),
-            "note": f"{what}, as a training loop: each step copies EVERY argument (batch, {len(fb)} parameters and "
-                    f"momenta fed back from the previous step's results) host->device and EVERY result "
-                    f"device->host inside the timed region (host wall clock, max over ranks); host arrays are "
-                    f"page-locked (the batch staged once, results returned in pinned arrays)"}
+            "note": f"{what}: each step copies EVERY argument (batch, parameters, momenta"
+                    f"{'; ' + str(len(fb)) + ' of them fed back from the previous results' if fb else ''}) "
+                    f"host->device and EVERY result device->host into new host arrays inside the timed region "
+                    f"(host wall clock, max over ranks); host arrays are page-locked (arguments staged once, "
+                    f"results returned in recycled pinned arrays)"}
 
 
 def main():
@@ -276,6 +286,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--e2e-seconds", type=float, default=40.0, help="time budget of the plugin-call e2e loop")
+    ap.add_argument("--e2e-feedback", action="store_true",
+                    help="feed results new_X back as arguments X (a training loop; C3's summed-loss model "
+                         "diverges after 2 steps at batch 8192, in the reference's evaluator as well)")
     ap.add_argument("--program", default=None, help="override the config's program for this GPU count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -337,17 +350,20 @@ def main():
         sess = Session(base, local_rank=local)
     else:
         sess = Session(prog.local, prog.sharding, mode="nccl", rank=rank, world=world, local_rank=local)
+    log(f"compiled {prog.name}: {sess.ex.plan.n_records} records, arena {sess.ex.peak_bytes / 1e9:.1f} GB")
     sess.load(inputs)
     dev = sess.device
     # eager run once (validates), then capture the whole step as one CUDA graph
     sess.run()
     sess.sync()
+    log("eager step done")
     sess.capture()
     for _ in range(max(3, args.warmup)):
         sess.step()
     sess.sync()
     launches_per_step = sess.launch_count()
 
+    log("captured + warm")
     e0, e1 = dev.event(), dev.event()
     # rank 0 samples every GPU of the job (nvidia-smi sees the whole node)
     with ClockSampler([local] if world == 1 else list(range(world)), active=(rank == 0)) as clk:
@@ -359,16 +375,19 @@ def main():
         dev.record(e1)
         sess.sync()
         barrier(dist)
-        # keep sampling clocks under the same load for a short while if the region was short
+        # keep sampling clocks under the same load for a short while if the region
+        # was short.  The number of extra steps must be the SAME on every rank
+        # (each step runs collectives that wait for every member): it is derived
+        # from the max over ranks, never from a rank's own time.
         ms = dev.elapsed_ms(e0, e1)
-        extra = 0
-        while ms * (1 + extra) < 1500 and extra < 2000:
-            for _ in range(args.steps):
-                sess.step()
-            extra += 1
+        ms_total = max_over_ranks(dist, ms)
+        n_extra = 0
+        while ms_total * (1 + n_extra) < 1500 and n_extra < 2000:
+            n_extra += 1
+        for _ in range(n_extra * args.steps):
+            sess.step()
         sess.sync()
         barrier(dist)
-    ms_total = max_over_ranks(dist, ms)
     ms_step = ms_total / args.steps
     value = batch / (ms_step / 1e3)
 
@@ -377,6 +396,7 @@ def main():
     dev.sync()
     loss = float(loss_arr[0])
 
+    log(f"timed region: {ms_step:.3f} ms/step")
     # ---- per-record profile (eager, events between records) for the roofline
     rec_ms = sess.ex.plan.profile()
     recs = sess.ex.records()
@@ -498,7 +518,9 @@ def main():
 
     # ---- end to end through the drop-in call: every input from host arrays,
     # every result back to new host arrays, per step
-    e2e = e2e_call(sess, prog, base, inputs, n, dist, args.e2e_seconds, args.steps, batch)
+    log("profile done; e2e")
+    e2e = e2e_call(sess, prog, base, inputs, n, dist, args.e2e_seconds, args.steps, batch, args.e2e_feedback)
+    log(f"e2e {e2e['ms_per_step']:.2f} ms/call")
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:

@@ -231,9 +231,23 @@ typedef struct {
   int32_t slot, max_blocks;        /* max_blocks: 0 = default (2 per SM); fewer leave SMs to concurrent compute */
 } spx_peer_params;
 
+/* ---- host <-> device copies inside the plan ---------------------------------
+ * The drop-in call's data movement as plan records: an argument's H2D copy
+ * right before its first reader, a result's D2H copy right after its last
+ * writer, each on its own copy stream, so the copies overlap the step instead
+ * of bracketing it.  `host` must be page-locked; spx_plan_set_host rebinds it
+ * before a run or a graph replay (the captured memcpy node is updated in the
+ * instantiated graph). */
+typedef struct {
+  uint64_t dev;                    /* device address */
+  uint64_t host;                   /* page-locked host address */
+  uint64_t bytes;
+  int32_t dir, pad;                /* 0 host->device, 1 device->host */
+} spx_copy_params;
+
 /* ---- plan records --------------------------------------------------------- */
 enum spx_kind { SPX_K_EW = 1, SPX_K_REDUCE = 2, SPX_K_GEMM = 3, SPX_K_GATHER = 4,
-                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6, SPX_K_PEER = 7, SPX_K_SPLIT = 8 };
+                SPX_K_CREDUCE = 5, SPX_K_NCCL = 6, SPX_K_PEER = 7, SPX_K_SPLIT = 8, SPX_K_COPY = 9 };
 
 /* library / device */
 const char* spx_last_error(void);
@@ -286,10 +300,10 @@ int spx_stream_sync_watch(uint64_t stream, double timeout_s);
 int spx_plan_create(uint64_t* out_plan);
 int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t params_bytes);
 /* Scheduling (optional): run record `index` on stream `stream` (0 = the stream
- * passed to run/capture; 1..3 = the plan's side streams: 1 off-critical compute
+ * passed to run/capture; 1..5 = the plan's side streams: 1 off-critical compute
  * such as weight-gradient GEMMs, 2 collectives (high priority), 3 parameter
- * updates), after the records listed in `waits` (indices of earlier records on
- * other streams) have completed.  Side streams fork from and join back into
+ * updates, 4 host->device copies, 5 device->host copies), after the records
+ * listed in `waits` (indices of earlier records on other streams) have completed.  Side streams fork from and join back into
  * the run/capture stream, so a plan stays one unit on it. */
 int spx_plan_set_sched(uint64_t plan, int index, int stream, const int* waits, int n_waits);
 int spx_plan_finalize(uint64_t plan);              /* builds TMA descriptors etc. */
@@ -329,6 +343,7 @@ enum spx_tag_bits {
   SPX_TAG_INTERNAL = 0x100        /* no IR FLOPs (split-K partial reduction) */
 };
 int spx_plan_tag(uint64_t plan, int index, int tag);
+int spx_plan_set_host(uint64_t plan, int index, uint64_t host);   /* SPX_K_COPY: rebind the host buffer */
 typedef struct {
   int64_t runs;                   /* eager runs + graph replays + profile runs */
   int64_t coll[4];                /* logical collectives issued: all_gather, all_reduce, reduce_scatter, all_to_all */

@@ -12,9 +12,22 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
 #include "common.cuh"
 
 static thread_local char g_err[1024] = "";
+
+// NVTX range per issued record (SPX_NVTX=1): "gemm 8192x8192x2048", "ew",
+// "peer all_reduce" ... -- for ncu --nvtx-include / Nsight timelines; header-only
+// NVTX3, a no-op unless a tool is attached
+static bool nvtx_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SPX_NVTX");
+    on = e ? atoi(e) != 0 : 0;
+  }
+  return on != 0;
+}
 
 int spx_set_error(const char* fmt, ...) {
   va_list ap;
@@ -177,9 +190,10 @@ struct Record {
   std::vector<int> waits;       // records on other streams to wait for
   bool signal = false;          // a later record on another stream waits for this one
   cudaEvent_t done = nullptr;
+  cudaGraphNode_t node = nullptr;   // SPX_K_COPY: its memcpy node in the captured graph
 };
 
-constexpr int SPX_SIDE_STREAMS = 3;   // 1 off-critical compute, 2 collectives, 3 parameter updates
+constexpr int SPX_SIDE_STREAMS = 5;   // 1 off-critical compute, 2 collectives, 3 parameter updates, 4/5 H2D/D2H copies
 
 struct Plan {
   std::vector<Record> recs;
@@ -235,7 +249,39 @@ static double record_flops(const Record& r) {
   return 0.0;
 }
 
+static int run_record_impl(Record& r, cudaStream_t s, int* nl);
+
+static const char* kind_name(int k) {
+  switch (k) {
+    case SPX_K_EW: return "ew";
+    case SPX_K_REDUCE: return "reduce";
+    case SPX_K_GEMM: return "gemm";
+    case SPX_K_GATHER: return "gather";
+    case SPX_K_CREDUCE: return "collective";
+    case SPX_K_NCCL: return "nccl";
+    case SPX_K_PEER: return "peer";
+    case SPX_K_SPLIT: return "split";
+    case SPX_K_COPY: return "copy";
+  }
+  return "record";
+}
+
 static int run_record(Record& r, cudaStream_t s, int* nl) {
+  if (!nvtx_on() || r.fused) return run_record_impl(r, s, nl);
+  char name[96];
+  if (r.kind == SPX_K_GEMM) {
+    const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
+    snprintf(name, sizeof(name), "gemm p%d %dx%dx%d", r.path, g.M, g.N, g.K);
+  } else {
+    snprintf(name, sizeof(name), "%s", kind_name(r.kind));
+  }
+  nvtxRangePushA(name);
+  const int rc = run_record_impl(r, s, nl);
+  nvtxRangePop();
+  return rc;
+}
+
+static int run_record_impl(Record& r, cudaStream_t s, int* nl) {
   if (r.fused) return 0;
   switch (r.kind) {
     case SPX_K_EW:
@@ -263,6 +309,25 @@ static int run_record(Record& r, cudaStream_t s, int* nl) {
       return spx_launch_gemm_simt(*reinterpret_cast<const spx_gemm_params*>(r.params.data()), s, nl);
     case SPX_K_NCCL: return run_nccl(*reinterpret_cast<const spx_nccl_params*>(r.params.data()), s);
     case SPX_K_PEER: return spx_launch_peer(*reinterpret_cast<const spx_peer_params*>(r.params.data()), s, nl);
+    case SPX_K_COPY: {
+      const spx_copy_params& c = *reinterpret_cast<const spx_copy_params*>(r.params.data());
+      if (!c.bytes) return 0;
+      if (c.dir == 0)
+        SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.dev), reinterpret_cast<const void*>(c.host), c.bytes,
+                                 cudaMemcpyHostToDevice, s));
+      else
+        SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.host), reinterpret_cast<const void*>(c.dev), c.bytes,
+                                 cudaMemcpyDeviceToHost, s));
+      cudaStreamCaptureStatus st;
+      SPX_CUDA(cudaStreamIsCapturing(s, &st));
+      if (st == cudaStreamCaptureStatusActive) {
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        SPX_CUDA(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd));
+        r.node = nd ? deps[0] : nullptr;       // the memcpy node just captured
+      }
+      return 0;
+    }
     case SPX_K_SPLIT:
       if (!r.batch_params.empty()) {
         std::vector<const spx_split_params*> ps;
@@ -286,6 +351,7 @@ static size_t params_size(int kind) {
     case SPX_K_NCCL: return sizeof(spx_nccl_params);
     case SPX_K_PEER: return sizeof(spx_peer_params);
     case SPX_K_SPLIT: return sizeof(spx_split_params);
+    case SPX_K_COPY: return sizeof(spx_copy_params);
   }
   return 0;
 }
@@ -860,6 +926,24 @@ int spx_plan_tag(uint64_t plan, int index, int tag) {
   const int c = tag & SPX_TAG_COLL_MASK;
   if (c > 4 || (tag & ~(SPX_TAG_COLL_MASK | SPX_TAG_INTERNAL))) return spx_set_error("bad record tag %#x", tag);
   P->recs[index].tag = tag;
+  return 0;
+}
+
+int spx_plan_set_host(uint64_t plan, int index, uint64_t host) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (index < 0 || index >= (int)P->recs.size()) return spx_set_error("record index out of range");
+  Record& r = P->recs[index];
+  if (r.kind != SPX_K_COPY) return spx_set_error("record %d is not a copy", index);
+  spx_copy_params& c = *reinterpret_cast<spx_copy_params*>(r.params.data());
+  c.host = host;
+  if (P->exec && r.node && c.bytes) {
+    if (c.dir == 0)
+      SPX_CUDA(cudaGraphExecMemcpyNodeSetParams1D(P->exec, r.node, reinterpret_cast<void*>(c.dev),
+                                                  reinterpret_cast<const void*>(c.host), c.bytes, cudaMemcpyHostToDevice));
+    else
+      SPX_CUDA(cudaGraphExecMemcpyNodeSetParams1D(P->exec, r.node, reinterpret_cast<void*>(c.host),
+                                                  reinterpret_cast<const void*>(c.dev), c.bytes, cudaMemcpyDeviceToHost));
+  }
   return 0;
 }
 

@@ -237,7 +237,18 @@ def _build(key, make):
     return ex, _CACHE.put(key, ex)
 
 
+def _io() -> bool:
+    """Copies inside the plan, overlapped with the step (Executable io=True);
+    SPX_IO_OVERLAP=0: copy in, run, copy out."""
+    return os.environ.get("SPX_IO_OVERLAP", "1") != "0"
+
+
 def _execute(ex, per_device, cached):
+    if ex.io:
+        res = ex.call(per_device, replay=cached and ex.plan.captured)
+        if cached and not ex.plan.captured:
+            ex.plan.capture()    # later calls replay the step, copies included, as one CUDA graph
+        return res
     ex.upload_args(per_device)
     if cached and ex.plan.captured:
         ex.plan.replay()
@@ -282,7 +293,7 @@ def spmd_interpret(module, sharding, inputs, func: str = "main", tol: float = 1e
         dev = device or default_device()
         key = ("spmd", fingerprint(module, func), func, gemm_path, str(cdtype), dev.ordinal, _knobs())
         ex, cached = _build(key, lambda: Executable(module, func, device=dev, gemm_path=gemm_path,
-                                                    dtype=cdtype))
+                                                    dtype=cdtype, io=_io()))
         _LAST = ex
         try:
             res = _execute(ex, per_device, cached)
@@ -317,7 +328,8 @@ def interpret(module, inputs, func: str = "main", device: R.Device | None = None
 
         def make():
             try:
-                return Executable(dense, func, device=dev, devices=[0], gemm_path=gemm_path, dtype=cdtype)
+                return Executable(dense, func, device=dev, devices=[0], gemm_path=gemm_path, dtype=cdtype,
+                                  io=_io())
             except UnsupportedProgram as e:
                 raise EvalError(str(e)) from e
         ex, cached = _build(key, make)

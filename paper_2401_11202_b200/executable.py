@@ -20,7 +20,7 @@ import ctypes as C
 import numpy as np
 
 from . import runtime as R
-from .plan import ALIGN, Compiler, Kernel, Leaf, Node, Program, _align, _contig, _prod
+from .plan import ALIGN, Compiler, Kernel, Leaf, Node, Program, UnsupportedProgram, _align, _contig, _prod
 
 
 def _collapse(dims, views):
@@ -46,11 +46,14 @@ class Executable:
 
     def __init__(self, module, func="main", device: R.Device | None = None, devices=None,
                  comm_mode="local", comms=None, gemm_path=0, dry=False, comm_factory=None,
-                 overlap=None, dtype=np.float32):
+                 overlap=None, dtype=np.float32, io=False):
         """dry=True builds the records against fake addresses without a GPU
         (used by the CPU tests and the record simulator).  dtype: the
         arithmetic type of the call (np.result_type of the inputs,
-        evaluator._cdtype): float32 or int32."""
+        evaluator._cdtype): float32 or int32.  io=True: the plan also copies
+        its arguments in and its results out (SPX_K_COPY records on two copy
+        streams, each right next to its first reader / last writer) -- the
+        drop-in call's data movement overlapped with the step (`call`)."""
         self.dtype = np.dtype(dtype)
         self.dt = R.DT_I32 if self.dtype == np.dtype(np.int32) else R.DT_F32
         if self.dt == R.DT_I32 and comm_mode != "local":
@@ -69,6 +72,9 @@ class Executable:
         if overlap:
             self._hoist_terminal()
         self._share_splits()
+        self.io = io
+        if io:
+            self._add_copies()
         self.stream_of = self._streams() if overlap else {}
         self.side = set(self.stream_of)
         self.overlap = bool(self.side)
@@ -91,6 +97,7 @@ class Executable:
         self._tables = []
         self._records = []
         self._krange = []          # per compiler kernel: [first record, end record)
+        self.copy_in, self.copy_out = {}, {}   # (arg, device) / (result j, device) -> copy record
 
         self._emit()
         self._upload_tables()
@@ -362,6 +369,8 @@ class Executable:
                 self._emit_gemm(k)
             elif k.kind == "split":
                 self._emit_split(k)
+            elif k.kind == "copy":
+                self._emit_copy(k)
             elif k.kind == "coll":
                 if c.comm_mode == "local":
                     self._emit_coll_local(k)
@@ -445,6 +454,23 @@ class Executable:
             self._fsg = next((i for i, k in enumerate(ks) if k.kind == "gemm" and self.stream_of.get(i)), len(ks))
         return self._fsg
 
+    def _emit_copy(self, k):
+        d = k.data
+        buf = d["buf"]
+        dims = self.comp.bufdims[buf] if d["dir"] == 0 else self.comp.f.result_types[d["j"]].dims
+        nbytes = 4 * _prod(dims)
+        for p in range(self.ndev):
+            q = R.CopyParams()
+            q.dev = self.addr(p, buf)
+            q.host = 0
+            q.bytes = nbytes
+            q.dir = d["dir"]
+            if d["dir"] == 0:
+                self.copy_in[(buf, p)] = len(self._records)
+            else:
+                self.copy_out[(d["j"], p)] = len(self._records)
+            self._records.append((R.K_COPY, q))
+
     def _emit_split(self, k):
         d = k.data
         buf, off, ld = d["src"]
@@ -459,7 +485,34 @@ class Executable:
         self._records.append((R.K_SPLIT, p))
 
     # streams of a two-level schedule (runtime.cu: SPX_SIDE_STREAMS)
-    MAIN, COMPUTE, COMM, UPDATE = 0, 1, 2, 3
+    MAIN, COMPUTE, COMM, UPDATE, H2D, D2H = 0, 1, 2, 3, 4, 5
+
+    def _add_copies(self):
+        """Copy kernels for the drop-in call: one H2D per argument, issued in
+        the order the step first reads them (so the first block's weights
+        arrive first and compute starts while later ones are in flight), one
+        D2H per result right after the kernel that last writes it (parameter
+        updates are hoisted next to their gradients, so most results leave
+        during the backward pass)."""
+        c = self.comp
+        ks = c.kernels
+        first_read = {}
+        last_write = {}
+        for i, k in enumerate(ks):
+            for b in k.ins:
+                first_read.setdefault(b, i)
+            for b in k.outs:
+                last_write[b] = i
+        order = sorted(c.arg_bufs, key=lambda a: (first_read.get(a, len(ks)), c.arg_bufs.index(a)))
+        ins = [Kernel("copy", [a], set(), data=dict(dir=0, buf=a)) for a in order]
+        after: dict = {}
+        for j, b in enumerate(c.result_bufs):
+            after.setdefault(last_write.get(b, -1), []).append(Kernel("copy", [], {b}, data=dict(dir=1, buf=b, j=j)))
+        out = list(ins) + after.get(-1, [])
+        for i, k in enumerate(ks):
+            out.append(k)
+            out.extend(after.get(i, []))
+        c.kernels = out
 
     def _terminal(self, k) -> bool:
         """A kernel whose outputs are only function results (parameter and
@@ -561,6 +614,9 @@ class Executable:
             for i, k in enumerate(ks):
                 if self._terminal(k):
                     side[i] = self.UPDATE
+        for i, k in enumerate(ks):
+            if k.kind == "copy":
+                side[i] = self.D2H if k.data["dir"] else self.H2D
         return side
 
     def _schedule(self):
@@ -846,6 +902,8 @@ class Executable:
         return keys
 
     def _nccl(self, kind, comm, send, recv, count, monoid=0):
+        if comm < 0:
+            raise UnsupportedProgram("this collective needs NCCL, but no communicator exists (SPX_NCCL_NONE=1)")
         p = R.NcclParams()
         p.kind, p.comm, p.monoid = kind, comm, monoid
         p.send, p.recv, p.count = send, recv, count
@@ -1015,6 +1073,47 @@ class Executable:
                     self.device.h2d(self.addr(p, a), arr)
                 else:
                     self.device.h2d_staged(self.addr(p, a), arr)
+
+    def call(self, per_device: list[dict], replay: bool) -> list[list[np.ndarray]]:
+        """One step with its data movement inside the plan (io=True): bind every
+        argument's page-locked host array and a fresh page-locked result array
+        per result to the copy records, launch (eager, or the captured graph),
+        wait.  Pageable arguments are first staged into page-locked arrays
+        (multi-threaded host copy).  Returns [result j][device p]."""
+        assert self.io
+        pool = R.pinned_pool()
+        keep = []
+        for p in range(self.ndev):
+            for a in self.comp.arg_bufs:
+                arr = np.ascontiguousarray(per_device[p][a], dtype=self.dtype)
+                if not pool.contains(arr):
+                    st = pool.array(arr.shape, self.dtype)
+                    if st is None:
+                        raise R.BackendError("page-locked pool exhausted (SPX_PINNED_POOL_BYTES)")
+                    R.call(self.device.lib.spx_host_copy, C.c_void_p(st.ctypes.data), C.c_void_p(arr.ctypes.data),
+                           arr.nbytes, 16)
+                    arr = st
+                keep.append(arr)
+                self.plan.set_host(self.copy_in[(a, p)], arr.ctypes.data)
+        f = self.comp.f
+        out = []
+        for j in range(len(self.comp.result_bufs)):
+            dims = tuple(f.result_types[j].dims)
+            per = []
+            for p in range(self.ndev):
+                r = pool.array(dims, self.dtype)
+                if r is None:
+                    raise R.BackendError("page-locked pool exhausted (SPX_PINNED_POOL_BYTES)")
+                self.plan.set_host(self.copy_out[(j, p)], r.ctypes.data)
+                per.append(r)
+            out.append(per)
+        if replay:
+            self.plan.replay()
+        else:
+            self.plan.run()
+        self.device.sync()
+        del keep
+        return out
 
     def download_results(self) -> list[list[np.ndarray]]:
         """[result j][device p] local arrays."""

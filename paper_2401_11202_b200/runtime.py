@@ -110,6 +110,12 @@ class PeerParams(C.Structure):
 
 K_PEER = 7
 K_SPLIT = 8
+K_COPY = 9
+
+
+class CopyParams(C.Structure):
+    _fields_ = [("dev", C.c_uint64), ("host", C.c_uint64), ("bytes", C.c_uint64), ("dir", C.c_int32),
+                ("pad", C.c_int32)]
 
 # record tags (include/spindle_b200.h spx_tag_bits)
 TAG_COLL = {"all_gather": 1, "all_reduce": 2, "reduce_scatter": 3, "all_to_all": 4}
@@ -125,7 +131,8 @@ PEER_MAX_BLOCKS = 512      # include/spindle_b200.h
 PEER_PHASES = 3
 
 PARAMS = {K_PEER: PeerParams, K_EW: EwParams, K_REDUCE: ReduceParams, K_GEMM: GemmParams,
-          K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams, K_SPLIT: SplitParams}
+          K_GATHER: GatherParams, K_CREDUCE: CreduceParams, K_NCCL: NcclParams, K_SPLIT: SplitParams,
+          K_COPY: CopyParams}
 
 EXPORTS = [
     "spx_last_error", "spx_version", "spx_params_size", "spx_device_init", "spx_malloc", "spx_free",
@@ -137,7 +144,7 @@ EXPORTS = [
     "spx_stream_wait_event", "spx_memcpy_d2d",
     "spx_plan_profile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
     "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
-    "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats",
+    "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats", "spx_plan_set_host",
     "spx_host_register", "spx_host_unregister", "spx_host_copy",
     "spx_h2d_staged", "spx_d2h_staged",
     "spx_comm_async_error", "spx_comm_abort", "spx_peer_error", "spx_peer_error_clear", "spx_stream_sync_watch",
@@ -190,6 +197,7 @@ def load(build_if_missing: bool = True):
         "spx_ipc_get_handle": [C.c_uint64, C.c_void_p], "spx_ipc_open": [C.c_void_p, C.POINTER(C.c_uint64)],
         "spx_ipc_close": [C.c_uint64],
         "spx_plan_tag": [C.c_uint64, C.c_int, C.c_int],
+        "spx_plan_set_host": [C.c_uint64, C.c_int, C.c_uint64],
         "spx_plan_exec_stats": [C.c_uint64, C.POINTER(ExecStats)],
         "spx_plan_reset_stats": [C.c_uint64],
         "spx_host_register": [C.c_void_p, C.c_uint64], "spx_host_unregister": [C.c_void_p],
@@ -417,6 +425,10 @@ class NativePlan:
 
     def tag(self, index: int, tag: int):
         call(self.lib.spx_plan_tag, self.h, index, tag)
+
+    def set_host(self, index: int, host: int):
+        """Rebind a copy record's page-locked host buffer (also in the captured graph)."""
+        call(self.lib.spx_plan_set_host, self.h, index, host)
 
     def exec_stats(self) -> dict:
         """What the runtime has issued so far (include/spindle_b200.h spx_exec_stats)."""

@@ -82,6 +82,13 @@ def make_nccl_comms(ex: Executable, rank: int, broadcast, get_uid=nccl_uid, init
     plan = comm_plan(ex)
     if allgather is not None and ex.wants_peer and plan:
         map_peer_arenas(ex, rank, allgather)
+    import os
+    if os.environ.get("SPX_NCCL_NONE", "0") == "1":
+        # peer-memory collectives only (every collective of the program must take
+        # the peer path; an NCCL record then fails loudly): lets tools/nccl_parity.py
+        # run 8 ranks on a 4-GPU box, two processes per GPU, where NCCL refuses
+        # duplicate devices
+        return {key: -1 for key, _ in plan}
     uids = None
     if rank == 0:
         uids = {(key, gi): get_uid() for key, groups in plan for gi in range(len(groups))}

@@ -38,30 +38,29 @@ def parity(name, steps):
 
 
 def phases(name, steps):
+    """C3 through the drop-in call with its copies in the plan (io mode), the
+    same pinned arguments every call (no feedback: the model diverges)."""
     p = load_program(name)
-    m, f = p.dense, p.dense.func()
+    m = p.dense
     pool = R.pinned_pool()
     cur = {}
     for k, v in synthetic_inputs(m, 0, 0.02).items():
         x = pool.array(v.shape, v.dtype)
         x[...] = v
         cur[k] = x
-    pkg.interpret(m, cur)
-    ex = E.last_executable()
     for it in range(steps):
         t0 = time.perf_counter()
-        ex.upload_args([cur])
-        ex.device.sync()
+        out = pkg.interpret(m, cur)
         t1 = time.perf_counter()
-        ex.plan.replay()
-        ex.device.sync()
-        t2 = time.perf_counter()
-        res = ex.download_results()
-        t3 = time.perf_counter()
-        out = [r[0] for r in res]
-        print(f"{name} step {it}: in {t1 - t0:.3f}s step {t2 - t1:.3f}s out {t3 - t2:.3f}s loss {float(out[0]):.4f} "
-              f"finite {all(np.isfinite(x).all() for x in out)} pool {pool.total / 1e9:.1f} GB", flush=True)
-        feed(f, cur, out)
+        print(f"{name} call {it}: {t1 - t0:.3f}s loss {float(out[0]):.4f} finite "
+              f"{all(np.isfinite(x).all() for x in out)} pool {pool.total / 1e9:.1f} GB", flush=True)
+        del out
+    os.environ["SPX_IO_OVERLAP"] = "0"
+    for it in range(3):
+        t0 = time.perf_counter()
+        out = pkg.interpret(m, cur)
+        print(f"{name} SPX_IO_OVERLAP=0 call {it}: {time.perf_counter() - t0:.3f}s loss {float(out[0]):.4f}", flush=True)
+        del out
 
 
 if __name__ == "__main__":
