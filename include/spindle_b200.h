@@ -256,6 +256,7 @@ int spx_params_size(int kind);                     /* ABI check: sizeof(record p
 int spx_device_init(int ordinal);                  /* select + check sm_100 */
 int spx_malloc(uint64_t bytes, uint64_t* out_ptr);  /* arena (cudaMalloc) */
 int spx_free(uint64_t ptr);
+int spx_mem_info(uint64_t* free_bytes, uint64_t* total_bytes);   /* cudaMemGetInfo of the current device */
 int spx_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream);
 int spx_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, uint64_t stream);
 int spx_memcpy_d2d(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream);

@@ -33,6 +33,7 @@
 //                     kind::f16 MMAs (A collector reused by hi.lo / hi.hi),
 //                     warps 4-7 fold TMEM chunks with their scale and store C
 //                     through TMA.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <cuda_fp16.h>
@@ -143,6 +144,7 @@ struct H3Args {
   int M, N, K;
   int a_mn_major, b_k_major;
   int tiles_m, tiles_n, tiles;
+  int group_m;                         // tile raster: groups of group_m M-tiles, M fastest inside a group
   int tma_store;
   uint64_t c_base;
   int64_t dev_stride;                  // bytes (C)
@@ -270,12 +272,22 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     c0 = (int)(((long long)nch * sp) / args.splits);
     ncu = (int)(((long long)nch * (sp + 1)) / args.splits) - c0;
   };
+  // Tile raster: groups of group_m M-tiles (row panels of A), M fastest inside
+  // a group, groups in order.  The pairs working at the same time then cover a
+  // ~group_m x (pairs / group_m) rectangle of tiles whose A and B panels stay in
+  // L2 together (the host picks group_m ~ sqrt(pairs * BN / 256), the
+  // footprint minimum); group_m = tiles_m is plain M-fastest order.
   auto tile_of = [&](int t, int& m0, int& n0, int& dev) {
     const int per_dev = args.tiles_m * args.tiles_n;
     dev = t / per_dev;
-    const int r = t - dev * per_dev;
-    const int n_blk = r / args.tiles_m;        // M fastest: concurrent pairs share B panels
-    m0 = (r - n_blk * args.tiles_m) * (HB * H_CG);
+    int r = t - dev * per_dev;
+    const int gsz = args.group_m * args.tiles_n;
+    const int g = r / gsz;
+    r -= g * gsz;
+    const int mf = g * args.group_m;
+    const int gm = min(args.group_m, args.tiles_m - mf);
+    const int n_blk = r / gm;
+    m0 = (mf + (r - n_blk * gm)) * (HB * H_CG);
     n0 = n_blk * BN;
   };
 
@@ -700,6 +712,17 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   a_.tiles_m = (p.M + HB * H_CG - 1) / (HB * H_CG);
   a_.tiles_n = (p.N + g->bn - 1) / g->bn;
   a_.tiles = a_.tiles_m * a_.tiles_n * p.ndev;
+  {
+    // concurrent tiles ~ pairs: a group_m x (pairs / group_m) rectangle, A panels
+    // 256 rows, B panels BN columns (same K): footprint minimal at
+    // group_m = sqrt(pairs * BN / 256).  SPX_H3_GROUP_M=n forces n (0: M fastest)
+    int sms = spx_num_sms() - (p.reserve_sms > 0 ? p.reserve_sms : 0);
+    const double pairs = sms / H_CG > 0 ? sms / H_CG : 1;
+    int gm = (int)(sqrt(pairs * g->bn / 256.0) + 0.5);
+    if (const char* e = getenv("SPX_H3_GROUP_M")) gm = atoi(e);
+    if (gm <= 0 || gm > a_.tiles_m) gm = a_.tiles_m;
+    a_.group_m = gm;
+  }
   a_.c_base = p.base + (uint64_t)(p.c_off * 4);
   a_.dev_stride = p.dev_stride;
   a_.ldc = p.ldc;

@@ -383,6 +383,13 @@ int spx_free(uint64_t ptr) {
   SPX_CUDA(cudaFree(reinterpret_cast<void*>(ptr)));
   return 0;
 }
+int spx_mem_info(uint64_t* free_bytes, uint64_t* total_bytes) {
+  size_t f = 0, t = 0;
+  SPX_CUDA(cudaMemGetInfo(&f, &t));
+  *free_bytes = f;
+  *total_bytes = t;
+  return 0;
+}
 int spx_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, uint64_t stream) {
   SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice,
                            reinterpret_cast<cudaStream_t>(stream)));

@@ -222,6 +222,18 @@ def _knobs():
     return tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("SPX_")))
 
 
+def _make_room(dev):
+    """before_alloc hook: evict cached plans (LRU) until the new arena fits in
+    the device's free memory with a margin for launches and workspaces."""
+    margin = int(os.environ.get("SPX_PLAN_MARGIN_BYTES", str(6 << 30)))
+
+    def hook(nbytes):
+        while _CACHE.entries and dev.mem_info()[0] < nbytes + margin:
+            _, old = _CACHE.entries.popitem(last=False)
+            old.close()
+    return hook
+
+
 def _build(key, make):
     """Executable for `key` from the cache, or built by make() and cached."""
     ex = _CACHE.get(key)
@@ -293,7 +305,7 @@ def spmd_interpret(module, sharding, inputs, func: str = "main", tol: float = 1e
         dev = device or default_device()
         key = ("spmd", fingerprint(module, func), func, gemm_path, str(cdtype), dev.ordinal, _knobs())
         ex, cached = _build(key, lambda: Executable(module, func, device=dev, gemm_path=gemm_path,
-                                                    dtype=cdtype, io=_io()))
+                                                    dtype=cdtype, io=_io(), before_alloc=_make_room(dev)))
         _LAST = ex
         try:
             res = _execute(ex, per_device, cached)
@@ -329,7 +341,7 @@ def interpret(module, inputs, func: str = "main", device: R.Device | None = None
         def make():
             try:
                 return Executable(dense, func, device=dev, devices=[0], gemm_path=gemm_path, dtype=cdtype,
-                                  io=_io())
+                                  io=_io(), before_alloc=_make_room(dev))
             except UnsupportedProgram as e:
                 raise EvalError(str(e)) from e
         ex, cached = _build(key, make)

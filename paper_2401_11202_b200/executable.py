@@ -46,7 +46,7 @@ class Executable:
 
     def __init__(self, module, func="main", device: R.Device | None = None, devices=None,
                  comm_mode="local", comms=None, gemm_path=0, dry=False, comm_factory=None,
-                 overlap=None, dtype=np.float32, io=False):
+                 overlap=None, dtype=np.float32, io=False, before_alloc=None):
         """dry=True builds the records against fake addresses without a GPU
         (used by the CPU tests and the record simulator).  dtype: the
         arithmetic type of the call (np.result_type of the inputs,
@@ -90,6 +90,8 @@ class Executable:
         self.peer_bases = None          # [arena base of rank r, mapped here]
         self._peer_handles = []
         self._layout()
+        if before_alloc is not None and not dry:
+            before_alloc(self.slice_elems * 4 * self.ndev)    # e.g. the plan cache evicting to make room
         self._alloc()
         if comm_mode == "nccl" and comm_factory is not None:
             self.comms = comm_factory(self)

@@ -147,6 +147,7 @@ EXPORTS = [
     "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats", "spx_plan_set_host",
     "spx_host_register", "spx_host_unregister", "spx_host_copy",
     "spx_h2d_staged", "spx_d2h_staged",
+    "spx_mem_info",
     "spx_comm_async_error", "spx_comm_abort", "spx_peer_error", "spx_peer_error_clear", "spx_stream_sync_watch",
 ]
 
@@ -198,6 +199,7 @@ def load(build_if_missing: bool = True):
         "spx_ipc_close": [C.c_uint64],
         "spx_plan_tag": [C.c_uint64, C.c_int, C.c_int],
         "spx_plan_set_host": [C.c_uint64, C.c_int, C.c_uint64],
+        "spx_mem_info": [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
         "spx_plan_exec_stats": [C.c_uint64, C.POINTER(ExecStats)],
         "spx_plan_reset_stats": [C.c_uint64],
         "spx_host_register": [C.c_void_p, C.c_uint64], "spx_host_unregister": [C.c_void_p],
@@ -247,6 +249,12 @@ class Device:
         call(self.lib.spx_malloc, int(nbytes), C.byref(p))
         self._allocs.append(p.value)
         return p.value
+
+    def mem_info(self) -> tuple[int, int]:
+        """(free, total) device bytes."""
+        f, t = C.c_uint64(), C.c_uint64()
+        call(self.lib.spx_mem_info, C.byref(f), C.byref(t))
+        return f.value, t.value
 
     def free(self, ptr: int):
         if ptr in self._allocs:
