@@ -237,8 +237,14 @@ def e2e_call(sess, prog, base, inputs, n, dist, budget_s, max_steps, batch, feed
         spec = None
     else:
         cur = {a: pinned(x) for a, x in sess.local_inputs(inputs)[0].items()}
+        # a session whose plan carries the copies (io), like the drop-in call's
+        from paper_2401_11202_b200.session import Session
+        rank, world, local = sess.rank, dist.get_world_size(), int(os.environ.get("LOCAL_RANK", "0"))
+        sess.close()
+        sess = Session(prog.local, prog.sharding, mode="nccl", rank=rank, world=world, local_rank=local, io=True)
         fn = lambda: [r[0] for r in sess.call_local([cur])]
-        what = "Session.call_local(host inputs) on every rank (copy in, replay, copy out)"
+        what = ("Session.call_local(host inputs) on every rank, copies inside the plan overlapped with the step "
+                "(the drop-in call's data movement per mesh device)")
         spec = prog.sharding
     fb = {}
     for j, r in enumerate(f.results if feedback else []):

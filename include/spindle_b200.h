@@ -166,11 +166,16 @@ typedef struct {
 typedef struct {
   uint64_t base;
   int64_t dev_stride;             /* bytes */
-  int32_t ndev, rows, cols, pad;
+  int32_t ndev, rows, cols;
+  int32_t flags;                  /* SPX_SPLIT_PIECES_ONLY: when this split runs inside the elementwise
+                                     launch producing its source, that launch need not store the fp32
+                                     source (every reader takes the pieces) */
   int64_t src_off, ld;            /* elements */
   int64_t dst_off, pitch;         /* pieces: elements from the device base; pitch in halves (multiple of 8) */
   int64_t scl_off;                /* elements */
 } spx_split_params;
+
+#define SPX_SPLIT_PIECES_ONLY 1
 
 enum spx_epilogue { SPX_EPI_NONE = 0, SPX_EPI_ADD = 1, SPX_EPI_SQUARE = 2, SPX_EPI_MULSCALE = 3,
                     SPX_EPI_MOMENTUM = 4 };

@@ -100,6 +100,7 @@ struct EwSplit {
   int64_t dev_stride, pitch;
   int rows, cols, cb, which;
   int nb;                   // row blocks per cluster (pipelined)
+  int skip;                 // 1: output `which` is read only through its pieces -- no fp32 store
 };
 
 // The same program over 128 x 128 output blocks, a cluster of H3_CL CTAs per
@@ -164,10 +165,10 @@ ew_static_split_kernel(const __grid_constant__ spx_ew_params p, const __grid_con
       const int64_t e = (int64_t)row * q.cols + c;
       run_static<I...>(r[i], p.imm, std::make_integer_sequence<int, (int)sizeof...(I)>{});
       const float4 y0 = make_float4(r[i][O0].v[0], r[i][O0].v[1], r[i][O0].v[2], r[i][O0].v[3]);
-      *reinterpret_cast<float4*>(out0 + e) = y0;
+      if (!(q.skip && q.which == 0)) *reinterpret_cast<float4*>(out0 + e) = y0;
       if (NOUT > 1) {
         const float4 y1 = make_float4(r[i][O1].v[0], r[i][O1].v[1], r[i][O1].v[2], r[i][O1].v[3]);
-        *reinterpret_cast<float4*>(out1 + e) = y1;
+        if (!(q.skip && q.which == 1)) *reinterpret_cast<float4*>(out1 + e) = y1;
         keep[i] = q.which ? y1 : y0;
       } else {
         keep[i] = y0;
@@ -288,6 +289,12 @@ int spx_launch_ew_static_split(int id, const spx_ew_params& p, const spx_split_p
   q.cols = sp.cols;
   q.cb = (sp.cols + H3_BLOCK - 1) / H3_BLOCK;
   q.which = which;
+  static int po = -1;
+  if (po < 0) {
+    const char* e = getenv("SPX_PIECES_ONLY");
+    po = e ? atoi(e) != 0 : 1;
+  }
+  q.skip = po && (sp.flags & SPX_SPLIT_PIECES_ONLY) ? 1 : 0;
   const int rbs = (sp.rows + H3_BLOCK - 1) / H3_BLOCK;
   // two row blocks per cluster once the grid still covers every SM twice
   static int nbe = -1;

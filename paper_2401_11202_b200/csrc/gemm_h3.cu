@@ -163,6 +163,13 @@ struct H3Args {
   int64_t flag_dev;                    // bytes
   uint64_t ws_base;                    // device-0 address of the partials
   int64_t ws_dev;                      // bytes
+  // dynamic unit scheduling (dyn = 1): pairs take units from a global counter
+  // (sched[0]; sched[1] counts pairs that ran dry -- the last one resets both
+  // for the next launch), so pairs that become resident late (SMs held by a
+  // concurrent kernel on another stream) find fewer units instead of holding
+  // back a static share
+  int dyn;
+  uint64_t sched;                      // uint32[2], zero between launches
 };
 
 template <bool LEADER_BAR>
@@ -231,6 +238,10 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   uint64_t* tfull = raw_empty + RS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr int UQ = 4;                       // unit queue (dynamic scheduling)
+  uint64_t* uq_full = tempty + 4;             // 8 B after tmem_slot
+  uint64_t* uq_empty = uq_full + UQ;
+  volatile int* uq = reinterpret_cast<volatile int*>(uq_empty + UQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (args.K + HBK - 1) / HBK;
@@ -248,6 +259,11 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4 * S::NDG * H_CG);
+    }
+    for (int q = 0; q < UQ; ++q) {
+      mbar_init(&uq_full[q], 1);
+      // consumers: the leader's MMA warp and drain warps, the peer's producer and drain warps
+      mbar_init(&uq_empty[q], 2 + 2 * 4 * S::NDG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -291,6 +307,50 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     n0 = n_blk * BN;
   };
 
+  // The j-th unit of this pair (static: pair0 + j * npairs).  Dynamic: the
+  // leader's producer warp fetches it from the global counter and publishes it
+  // in both CTAs' queue slot (the peer's through distributed shared memory);
+  // every other consumer warp reads its own CTA's slot and releases it on the
+  // leader's empty barrier.  A unit >= units ends every role's loop.
+  auto get_unit = [&](int j, bool fetcher) -> int {
+    if (!args.dyn) return pair0 + j * npairs;
+    const int slot = j & (UQ - 1);
+    const uint32_t ph = (uint32_t)((j / UQ) & 1);
+    int u = 0;
+    if (fetcher) {
+      mbar_wait<true>(&uq_empty[slot], ph ^ 1u);
+      if (lane == 0) {
+        uint32_t* cnt = reinterpret_cast<uint32_t*>(args.sched);
+        u = (int)atomicAdd(cnt, 1u);
+        uq[slot] = u;
+        uint32_t r_uq, r_full;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(r_uq) : "r"(smem_u32((const void*)&uq[slot])));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(r_full) : "r"(smem_u32(&uq_full[slot])));
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_uq), "r"(u) : "memory");
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r_full) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&uq_full[slot])) : "memory");
+        if (u >= args.units) {
+          // this pair ran dry; the last pair to do so resets the counters for the next launch
+          if (atomicAdd(cnt + 1, 1u) == (uint32_t)(npairs - 1)) {
+            atomicExch(cnt, 0u);
+            atomicExch(cnt + 1, 0u);
+          }
+        }
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+    } else {
+      mbar_wait<true>(&uq_full[slot], ph);
+      u = uq[slot];
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t r;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(&uq_empty[slot])));
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+      }
+    }
+    return u;
+  };
+
   if (warp < 4) {
     if (BN > 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
@@ -298,7 +358,9 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       uint32_t lead_full0;
       asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead_full0) : "r"(smem_u32(&raw_full[0])));
       int g = 0;
-      for (int u = pair0; u < args.units; u += npairs) {
+      for (int j = 0;; ++j) {
+        const int u = get_unit(j, crank == 0);
+        if (u >= args.units) break;
         int t, sp, c0, ncu, m0, n0, dev;
         unit_of(u, t, sp, c0, ncu);
         tile_of(t, m0, n0, dev);
@@ -356,7 +418,9 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       int rs = 0;
       uint32_t rph = 0;
       int cg = 0;
-      for (int u = pair0; u < args.units; u += npairs) {
+      for (int j = 0;; ++j) {
+        const int u = get_unit(j, false);
+        if (u >= args.units) break;
         int t, sp, c0, ncu;
         unit_of(u, t, sp, c0, ncu);
         const int kbe = min(nk, 2 * (c0 + ncu));
@@ -393,7 +457,9 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     const int q = warp & 3;
     const int dg = (warp - 4) >> 2;            // column group: columns [128 dg, 128 dg + 128)
     int cg = 0;
-    for (int u = pair0; u < args.units; u += npairs) {
+    for (int j = 0;; ++j) {
+      const int u = get_unit(j, false);
+      if (u >= args.units) break;
       int t, sp, c0, ncu, m0, n0, dev;
       unit_of(u, t, sp, c0, ncu);
       tile_of(t, m0, n0, dev);
@@ -601,6 +667,7 @@ void split_args(SplitArgs& s, const Operand& o, int64_t src_dev, uint64_t ws) {
 
 struct SpxGemmH3 {
   spx_gemm_params p;
+  uint32_t* sched = nullptr;            // dynamic-scheduling counters (H3Args::sched)
   Operand A, B;
   int64_t ws_bytes = 0;
   uint64_t ws = 0;
@@ -746,6 +813,19 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
   }
   a_.splits = g->splits;
   a_.units = a_.tiles * g->splits;
+  {
+    static int dyn = -1;
+    if (dyn < 0) {
+      const char* e = getenv("SPX_H3_DYNAMIC");
+      dyn = e ? atoi(e) != 0 : 1;
+    }
+    a_.dyn = dyn;
+    if (dyn && !g->sched) {
+      SPX_CUDA(cudaMalloc(&g->sched, 8));
+      SPX_CUDA(cudaMemset(g->sched, 0, 8));
+    }
+    a_.sched = reinterpret_cast<uint64_t>(g->sched);
+  }
   memset(&g->mw, 0, sizeof(g->mw));
   a_.flag_base = wsb;
   a_.flag_dev = H3_FLAG_DEV;
@@ -862,4 +942,7 @@ int spx_launch_split_batch(const spx_split_params* const* p, int n, cudaStream_t
   return 0;
 }
 
-void spx_gemm_h3_free(SpxGemmH3* g) { delete g; }
+void spx_gemm_h3_free(SpxGemmH3* g) {
+  if (g->sched) cudaFree(g->sched);
+  delete g;
+}

@@ -38,12 +38,11 @@ namespace {
 // Flag protocol and memory ordering.  Flags are written with system-scope
 // stores into the members' arenas and polled with relaxed system-scope loads.
 // Where a barrier publishes data written IN THE SAME KERNEL (the two-shot
-// all-reduce's reduced segments, read by the peers after phase 1) the
-// arriving thread issues the flag store with release semantics after the
-// block's __syncthreads, and the waiting thread follows its successful poll
-// with an acquire fence before the block's __syncthreads: the PTX
-// message-passing pattern at system scope (bar.sync makes the other threads'
-// writes/reads part of the release/acquire).  The arrive barrier of phase 0
+// all-reduce's reduced segments, read by the peers after phase 1) the block
+// fences at system scope between its writes and its flag stores, and again
+// between its successful polls and its reads of the peers' data: the
+// fence-based message-passing pattern of the PTX model (bar.sync makes the
+// other threads' writes/reads part of the release/acquire).  The arrive barrier of phase 0
 // publishes inputs completed by EARLIER kernels (kernel boundaries) and the
 // depart barrier orders only reads before a later overwrite (every load of
 // the block has returned when __syncthreads completes), so those use relaxed
@@ -84,12 +83,29 @@ struct PeerSync {
   uint32_t* err;         // mapped host error word
 };
 
-// publish: this barrier makes data written by this kernel visible to the peers
+// publish: this barrier makes data written by this kernel visible to the peers.
+// SPX_PEER_ORDER: 0 relaxed everywhere; 1 (default) release/acquire at system
+// scope on publishing barriers -- one fence.acq_rel.sys per block on each side
+// (after the block's __syncthreads, before the relaxed flag stores / after the
+// polls), the fence-based form of the release/acquire pattern; 2 the same on
+// every barrier; 3 publishing barriers at GPU scope (fence.acq_rel.gpu:
+// sufficient in practice, since a peer reads this GPU's memory through this
+// GPU's L2, but outside the PTX model's cross-GPU rules -- measurement only).
 SPX_DEV void block_barrier(const spx_peer_params& p, int phase, uint32_t epoch, PeerSync ps, bool publish) {
   const int t = threadIdx.x;
-  const bool ra = ps.order >= 2 || (ps.order == 1 && publish);
+  const bool ra = ps.order == 2 || ((ps.order == 1 || ps.order == 3) && publish);
+  const bool gpu = ps.order == 3;
+  if (ra) {
+    // every thread's writes are ordered before thread 0's fence by the caller's
+    // __syncthreads; the fence orders them before the flag stores below
+    if (t == 0) {
+      if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      else asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
+    __syncthreads();
+  }
   if (t < p.n) {
-    st_flag(flag_at(p.flags[t], p.slot, phase, blockIdx.x, p.me), epoch, ra);
+    st_flag(flag_at(p.flags[t], p.slot, phase, blockIdx.x, p.me), epoch, false);
     const uint32_t* mine = flag_at(p.flags[p.me], p.slot, phase, blockIdx.x, t);
     if (ld_flag(mine) < epoch) {
       const uint64_t t0 = globaltimer();
@@ -101,9 +117,17 @@ SPX_DEV void block_barrier(const spx_peer_params& p, int phase, uint32_t epoch, 
         }
       }
     }
-    if (ra) asm volatile("fence.acq_rel.sys;" ::: "memory");
   }
   __syncthreads();
+  if (ra) {
+    // acquire: the polls (relaxed) observed the peers' flags; one fence orders
+    // this block's subsequent reads of their data after them
+    if (t == 0) {
+      if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      else asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
+    __syncthreads();
+  }
 }
 
 SPX_DEV float4 fold4(int monoid, float4 a, float4 v) {

@@ -87,6 +87,8 @@ class Executable:
         self.peer_ag_all = os.environ.get("SPX_PEER_AG_ALL", "1") != "0"
         self.peer_rs = os.environ.get("SPX_PEER_RS", "1") != "0"
         self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
+        self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "0"))
+        self.one_stream = comm_mode == "nccl" and os.environ.get("SPX_COLL_ONE_STREAM", "1") != "0"
         self.peer_bases = None          # [arena base of rank r, mapped here]
         self._peer_handles = []
         self._layout()
@@ -437,6 +439,7 @@ class Executable:
                             pre.append(sk)
                         elif pk is not None and pk.kind == "ew" and off == 0 and ld == cols:
                             after.setdefault(id(pk), []).append(sk)
+                            sk.data["fusable"] = True
                         else:
                             out.append(sk)
                         self.n_splits += 1
@@ -449,6 +452,29 @@ class Executable:
             final.append(k)
             final.extend(after.get(id(k), []))
         c.kernels = final
+        # A fused split's source that every reader takes through its pieces (h3
+        # GEMMs reading this very split) and that is no result need not be stored
+        # in fp32 by the producing launch (SPX_SPLIT_PIECES_ONLY; the runtime
+        # honours it only when it really fuses the split into that launch).
+        results = set(c.result_bufs)
+        for k in final:
+            if k.kind != "split" or not k.data.get("fusable"):
+                continue
+            src = k.data["src"][0]
+            name = k.outs[0]
+            ok = src not in results
+            for r in final:
+                if r is k or src not in r.ins:
+                    continue
+                if not (r.kind == "gemm" and name in (r.data.get("h3a"), r.data.get("h3b"))):
+                    ok = False
+                    break
+                (ab, _, _, _), (bb, _, _, _) = r.data["a"], r.data["b"]
+                # both operands of the GEMM must come from pieces of this split when both read src
+                if ab == src and r.data.get("h3a") != name or bb == src and r.data.get("h3b") != name:
+                    ok = False
+                    break
+            k.data["pieces_only"] = ok
 
     def _first_side_gemm(self) -> int:
         if not hasattr(self, "_fsg"):
@@ -484,6 +510,7 @@ class Executable:
         p.dst_off = self.off[k.outs[0]]
         p.pitch = d["pitch"]
         p.scl_off = self.off[k.outs[0]] + d["scl_off"]
+        p.flags = R.SPLIT_PIECES_ONLY if d.get("pieces_only") else 0
         self._records.append((R.K_SPLIT, p))
 
     # streams of a two-level schedule (runtime.cu: SPX_SIDE_STREAMS)
@@ -589,13 +616,16 @@ class Executable:
         # (critical-path collectives on the main stream).
         one = c.comm_mode == "nccl" and os.environ.get("SPX_COLL_ONE_STREAM", "1") != "0"
         args = set(c.arg_bufs)
+        self.coll_offcrit = set()     # collectives nothing on the critical path waits for
         if c.comm_mode == "nccl":
             for i in reversed(range(len(ks))):
                 k = ks[i]
                 if k.kind == "coll" and k.data["kind"] != "all_slice":
-                    if (one or crit_coll or off_critical(i, side)
-                            or (prefetch and k.data["kind"] == "all_gather" and k.ins
-                                and all(b in args for b in k.ins))):
+                    off = off_critical(i, side) or (prefetch and k.data["kind"] == "all_gather" and k.ins
+                                                    and all(b in args for b in k.ins))
+                    if off:
+                        self.coll_offcrit.add(i)
+                    if one or crit_coll or off:
                         side[i] = self.COMM
         # splits of function arguments run on the compute stream from the start
         # of the step, overlapped with the forward pass (their GEMMs wait for them)
@@ -987,8 +1017,12 @@ class Executable:
                 p.flags[j] = self.peer_bases[r] + self.flag_off * 4
             p.dst = out_a
             p.counter = self.base + self.counter_off * 4
-            # off the critical path: leave most SMs to the concurrent GEMMs
-            p.max_blocks = self.peer_side_blocks if self._cur in self.side else 0
+            # off the critical path (ZeRO-3 parameter prefetch, gradient reductions):
+            # a few blocks stream it while the GEMMs keep the other SMs
+            if self._cur in getattr(self, "coll_offcrit", ()):
+                p.max_blocks = self.peer_offcrit_blocks
+            else:
+                p.max_blocks = self.peer_side_blocks if (self._cur in self.side and not self.one_stream) else 0
             self._records.append((R.K_PEER, p))
 
         if kind == "all_reduce":

@@ -73,12 +73,13 @@ class GemmParams(C.Structure):
 
 class SplitParams(C.Structure):
     _fields_ = [("base", C.c_uint64), ("dev_stride", C.c_int64),
-                ("ndev", C.c_int32), ("rows", C.c_int32), ("cols", C.c_int32), ("pad", C.c_int32),
+                ("ndev", C.c_int32), ("rows", C.c_int32), ("cols", C.c_int32), ("flags", C.c_int32),
                 ("src_off", C.c_int64), ("ld", C.c_int64),
                 ("dst_off", C.c_int64), ("pitch", C.c_int64), ("scl_off", C.c_int64)]
 
 
 DT_F32, DT_I32 = 0, 1
+SPLIT_PIECES_ONLY = 1
 EPI_NONE, EPI_ADD, EPI_SQUARE, EPI_MULSCALE, EPI_MOMENTUM = 0, 1, 2, 3, 4
 
 

@@ -118,7 +118,10 @@ def torch_broadcast(obj):
 class Session:
     def __init__(self, module, sharding=None, *, mode="local", device: R.Device | None = None,
                  rank: int = 0, world: int = 1, local_rank: int = 0, gemm_path: int = 0,
-                 func: str = "main", broadcast=torch_broadcast, allgather=torch_allgather):
+                 func: str = "main", broadcast=torch_broadcast, allgather=torch_allgather, io: bool = False):
+        """io=True: the plan also copies every argument in and every result out
+        (copy records overlapped with the step) -- use `call` / `call_local`, not
+        `step`, which would replay the copies with stale host buffers."""
         self.module = module
         self.sharding = sharding
         self.mode = mode
@@ -128,13 +131,13 @@ class Session:
             self.mesh = None
             self.coords = [{}]
             self.device = device or R.Device(local_rank)
-            self.ex = Executable(target, func, device=self.device, devices=[0], gemm_path=gemm_path)
+            self.ex = Executable(target, func, device=self.device, devices=[0], gemm_path=gemm_path, io=io)
             self.hosted = [0]
         elif mode == "local":
             self.mesh = module.mesh
             self.coords = self.mesh.coords()
             self.device = device or R.Device(local_rank)
-            self.ex = Executable(module, func, device=self.device, gemm_path=gemm_path)
+            self.ex = Executable(module, func, device=self.device, gemm_path=gemm_path, io=io)
             self.hosted = list(range(len(self.coords)))
         else:
             self.mesh = module.mesh
@@ -143,7 +146,7 @@ class Session:
                 raise ValueError(f"mesh has {self.mesh.device_count} devices, world size is {world}")
             self.device = device or R.Device(local_rank)
             self.ex = Executable(module, func, device=self.device, devices=[rank], comm_mode="nccl",
-                                 gemm_path=gemm_path,
+                                 gemm_path=gemm_path, io=io,
                                  comm_factory=lambda ex: make_nccl_comms(ex, rank, broadcast,
                                                                          allgather=allgather))
             self.hosted = [rank]
@@ -238,6 +241,11 @@ class Session:
 
     def call_local(self, local_inputs: list[dict]):
         """`call` with inputs already sharded: local_inputs[hosted device][arg]."""
+        if self.ex.io:
+            res = self.ex.call(local_inputs, replay=self.ex.plan.captured)
+            if not self.ex.plan.captured:
+                self.ex.plan.capture()
+            return res
         self.ex.upload_args(local_inputs)
         if self.ex.plan.captured:
             self.ex.plan.replay()

@@ -98,3 +98,27 @@ def test_fused_split_does_not_reuse_producer_inputs(name):
                 a0, a1 = iv(b)
                 assert p1 <= a0 or a1 <= p0, (name, i, b)
     assert n > 0
+
+
+@pytest.mark.parametrize("name", CONFIG_PROGRAMS + ["c2_tf8_dense", "c4_unet_dense", "c3_tf2_dense"])
+def test_pieces_only_sources_have_only_piece_readers(name):
+    """SPX_SPLIT_PIECES_ONLY lets the launch producing a split's source skip its
+    fp32 store: valid only if every reader of that source is a block-scaled
+    GEMM reading THIS split's pieces and the source is no function result."""
+    p = load_program(name)
+    dense = name.endswith("dense")
+    ex = Executable(_Dense(p.dense) if dense else p.local, devices=[0] if dense else None, dry=True)
+    ks = ex.comp.kernels
+    results = set(ex.comp.result_bufs)
+    n = 0
+    for k in ks:
+        if k.kind == "split" and k.data.get("pieces_only"):
+            n += 1
+            src, piece = k.data["src"][0], k.outs[0]
+            assert src not in results
+            for r in ks:
+                if r is not k and src in r.ins:
+                    assert r.kind == "gemm", (name, r.kind)
+                    assert piece in (r.data.get("h3a"), r.data.get("h3b")), name
+    if name.startswith(("c2", "c3", "c5")):
+        assert n > 0
