@@ -247,7 +247,9 @@ typedef struct {
   uint64_t dev;                    /* device address */
   uint64_t host;                   /* page-locked host address */
   uint64_t bytes;
-  int32_t dir, pad;                /* 0 host->device, 1 device->host */
+  int32_t dir, pad;                /* 0 host->device, 1 device->host, 2 device->device: `host` is then
+                                      the source device address -- possibly a peer's arena mapped
+                                      by CUDA IPC (a copy-engine all-gather over NVLink) */
 } spx_copy_params;
 
 /* ---- plan records --------------------------------------------------------- */

@@ -312,6 +312,11 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   // in both CTAs' queue slot (the peer's through distributed shared memory);
   // every other consumer warp reads its own CTA's slot and releases it on the
   // leader's empty barrier.  A unit >= units ends every role's loop.
+  // Claims: every pair's first unit is its static one (pair0, no atomic on the
+  // critical path of small GEMMs); later units come from the counter, claimed
+  // one unit AHEAD (right after publishing the current one) so the atomic's
+  // latency hides behind the current unit's loads.  Unit = npairs + claim.
+  int pref = 0;
   auto get_unit = [&](int j, bool fetcher) -> int {
     if (!args.dyn) return pair0 + j * npairs;
     const int slot = j & (UQ - 1);
@@ -321,7 +326,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       mbar_wait<true>(&uq_empty[slot], ph ^ 1u);
       if (lane == 0) {
         uint32_t* cnt = reinterpret_cast<uint32_t*>(args.sched);
-        u = (int)atomicAdd(cnt, 1u);
+        u = j == 0 ? pair0 : pref;
         uq[slot] = u;
         uint32_t r_uq, r_full;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(r_uq) : "r"(smem_u32((const void*)&uq[slot])));
@@ -329,12 +334,12 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r_uq), "r"(u) : "memory");
         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r_full) : "memory");
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&uq_full[slot])) : "memory");
-        if (u >= args.units) {
-          // this pair ran dry; the last pair to do so resets the counters for the next launch
-          if (atomicAdd(cnt + 1, 1u) == (uint32_t)(npairs - 1)) {
-            atomicExch(cnt, 0u);
-            atomicExch(cnt + 1, 0u);
-          }
+        if (u < args.units) {
+          pref = npairs + (int)atomicAdd(cnt, 1u);          // claim the next unit now
+        } else if (atomicAdd(cnt + 1, 1u) == (uint32_t)(npairs - 1)) {
+          // this pair ran dry, and it is the last one: reset for the next launch
+          atomicExch(cnt, 0u);
+          atomicExch(cnt + 1, 0u);
         }
       }
       u = __shfl_sync(0xffffffffu, u, 0);

@@ -391,7 +391,12 @@ int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   }
   // kind 2, reduce-scatter: the sources point at this member's chunk of every
   // member's input, and only that chunk is folded (one-shot kernel)
-  if (two && p.kind == 0 && p.max_blocks == 0 && (p.n == 4 || p.n == 8) && (p.count & 3) == 0 && (n4 % p.n) == 0 && n4 >= 131072 && !dbg) {
+  // two-shot from 2 MB with 8 members; with 4 from 8 MB: its publishing barrier's
+  // system-scope fences (release/acquire, SPX_PEER_ORDER=1) cost ~9 us, so below
+  // that the one-shot kernel is faster (profiles/r02_peer_order_variants.txt:
+  // 4 MB 26.1 vs 28.4 us, 16 MB 89.3 vs 57.9 us)
+  const int64_t two_min = (p.n == 4 && ps.order != 0 && ps.order != 3) ? (int64_t)524288 : (int64_t)131072;
+  if (two && p.kind == 0 && p.max_blocks == 0 && (p.n == 4 || p.n == 8) && (p.count & 3) == 0 && (n4 % p.n) == 0 && n4 >= two_min && !dbg) {
     const int64_t seg4 = n4 / p.n;
     int64_t b2 = (seg4 + 256 * 2 - 1) / (256 * 2);     // ~2 float4 per thread per phase
     if (b2 > cap) b2 = cap;

@@ -315,12 +315,15 @@ static int run_record_impl(Record& r, cudaStream_t s, int* nl) {
       if (c.dir == 0)
         SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.dev), reinterpret_cast<const void*>(c.host), c.bytes,
                                  cudaMemcpyHostToDevice, s));
-      else
+      else if (c.dir == 1)
         SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.host), reinterpret_cast<const void*>(c.dev), c.bytes,
                                  cudaMemcpyDeviceToHost, s));
+      else   // 2: device -> device, `host` holds the (possibly peer-mapped) source
+        SPX_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.dev), reinterpret_cast<const void*>(c.host), c.bytes,
+                                 cudaMemcpyDeviceToDevice, s));
       cudaStreamCaptureStatus st;
       SPX_CUDA(cudaStreamIsCapturing(s, &st));
-      if (st == cudaStreamCaptureStatusActive) {
+      if (c.dir != 2 && st == cudaStreamCaptureStatusActive) {
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
         SPX_CUDA(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd));

@@ -88,6 +88,7 @@ class Executable:
         self.peer_rs = os.environ.get("SPX_PEER_RS", "1") != "0"
         self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
         self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "0"))
+        self.ce_ag = os.environ.get("SPX_CE_AG", "1") != "0"
         self.one_stream = comm_mode == "nccl" and os.environ.get("SPX_COLL_ONE_STREAM", "1") != "0"
         self.peer_bases = None          # [arena base of rank r, mapped here]
         self._peer_handles = []
@@ -355,7 +356,8 @@ class Executable:
             # group kernel; NCCL mode: the NCCL call or peer kernel, not the
             # relayouts around it) and internal work without IR FLOPs
             if k.kind == "coll" and k.data["kind"] in R.TAG_COLL and end > first:
-                idx = next((r for r in range(first, end) if self._records[r][0] in (R.K_NCCL, R.K_PEER)), first)
+                idx = next((r for r in range(first, end) if self._records[r][0] in (R.K_NCCL, R.K_PEER)),
+                           next((r for r in range(first, end) if self._records[r][0] == R.K_COPY), first))
                 self._tags[idx] = R.TAG_COLL[k.data["kind"]]
             if k.data.get("internal"):
                 for r in range(first, end):
@@ -1044,6 +1046,20 @@ class Executable:
             # arguments, C3/C5) and the ZeRO-2 gathers of freshly updated
             # shards at the end of the step (C4); SPX_PEER_AG_ALL=0 keeps the
             # latter on NCCL
+            # gathers of function arguments (the ZeRO-3 parameter prefetch): the
+            # copy engines pull every member's shard over NVLink straight into
+            # the output -- no SM spins or copies, so the gather overlaps the
+            # GEMMs completely; arguments are immutable during the step, so no
+            # cross-rank handshake is needed (io calls barrier the ranks first)
+            if (direct and self.peer_bases is not None and src in c.arg_bufs and self.ce_ag):
+                for j, r in enumerate(grp):
+                    q = R.CopyParams()
+                    q.dev = out_a + j * nloc * 4
+                    q.host = self.peer_bases[r] + (src_a - self.base) if r != me else src_a
+                    q.bytes = nloc * 4
+                    q.dir = 2
+                    self._records.append((R.K_COPY, q))
+                return
             if (direct and use_peer and n in (2, 3, 4, 8) and nloc % 4 == 0 and n * nloc * 4 <= self.peer_max_bytes
                     and self.peer_ag and (src in c.arg_bufs or self.peer_ag_all)):
                 peer(1, nloc)

@@ -171,6 +171,13 @@ class Session:
     def load(self, global_inputs: dict):
         self.ex.upload_args(self.local_inputs(global_inputs))
         self.device.sync()
+        self._rank_barrier()      # peers may gather these arguments by copy engine (no device handshake)
+
+    def _rank_barrier(self):
+        if self.mode == "nccl":
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                dist.barrier()
 
     def arg_addr(self, name: str, p: int = 0) -> int:
         return self.ex.addr(p, name)
@@ -189,7 +196,9 @@ class Session:
         into one of two staging slots, overlapping the step that is running.
         The next `step()` waits for the copy, moves the slot into the arg
         buffers (device-to-device) and runs.  Hosted device 0 (nccl mode:
-        this rank's device)."""
+        this rank's device).  In nccl mode only feed arguments no other rank
+        gathers by copy engine (the sharded batch -- ZeRO-3 gathers parameters),
+        or set SPX_CE_AG=0: a step's argument update has no cross-rank handshake."""
         dev = self.device
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = dev.new_stream()
@@ -240,7 +249,11 @@ class Session:
         return self.call_local(self.local_inputs(global_inputs))
 
     def call_local(self, local_inputs: list[dict]):
-        """`call` with inputs already sharded: local_inputs[hosted device][arg]."""
+        """`call` with inputs already sharded: local_inputs[hosted device][arg].
+        One process per GPU: the ranks first meet at a barrier, since a peer may
+        still be reading this rank's arguments (copy-engine all-gathers of the
+        ZeRO-3 parameters) for the previous call."""
+        self._rank_barrier()
         if self.ex.io:
             res = self.ex.call(local_inputs, replay=self.ex.plan.captured)
             if not self.ex.plan.captured:

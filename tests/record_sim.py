@@ -297,11 +297,24 @@ def sim_dense(module, inputs):
     return [r[0] for r in sim.results()], ex
 
 
+PEER_SHIFT = 36
+
+
+def _peer_of(addr):
+    """(member rank or -1 for the own arena, address in that member's arena):
+    dry peer mappings sit at DRY_BASE + (rank + 1) << PEER_SHIFT."""
+    from paper_2401_11202_b200.executable import Executable
+    tag = (int(addr) - Executable.DRY_BASE) >> PEER_SHIFT
+    return (tag - 1 if tag > 0 else -1), int(addr) - (tag << PEER_SHIFT)
+
+
 def _dry_comms(ex, peer):
     if peer:
-        # every dry arena has base DRY_BASE: a peer address decodes to the same
-        # offset in that member's simulated arena
-        ex.peer_bases = [ex.base] * ex.comp.mesh.device_count
+        # every dry arena has base DRY_BASE; a peer's arena is "mapped" at
+        # DRY_BASE + (rank + 1) << PEER_SHIFT, so an address names its member
+        me = ex.comp.devices[0]
+        ex.peer_bases = [ex.base if r == me else ex.base + ((r + 1) << PEER_SHIFT)
+                         for r in range(ex.comp.mesh.device_count)]
     return {k: i for i, k in enumerate(ex.comm_keys())}
 
 
@@ -344,7 +357,7 @@ def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
                 assert grp.index(r) == p.me and len(grp) == p.n
                 acc = None
                 for j, m in enumerate(grp):
-                    o = sims[m].idx(p.src[j])
+                    o = sims[m].idx(_peer_of(p.src[j])[1])
                     x = sims[m].arena[o:o + p.count]
                     if p.kind == 1:          # all-gather: member chunks in member order
                         acc = x.copy() if acc is None else np.concatenate([acc, x])
@@ -353,6 +366,19 @@ def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
                 outs.append((r, sims[r].idx(p.dst), acc))
             for r, d0, acc in outs:
                 sims[r].arena[d0:d0 + acc.size] = acc
+            continue
+        if kind == R.K_COPY:
+            # device-to-device copies (copy-engine all-gather): read every source first
+            outs = []
+            for r in range(world):
+                p = exs[r].records()[i][1]
+                assert p.dir == 2
+                m, a = _peer_of(p.host)
+                m = r if m < 0 else m
+                o = sims[m].idx(a)
+                outs.append((r, sims[r].idx(p.dev), sims[m].arena[o:o + p.bytes // 4].copy()))
+            for r, d0, x in outs:
+                sims[r].arena[d0:d0 + x.size] = x
             continue
         if kind != R.K_NCCL:
             for s, e in zip(sims, exs):

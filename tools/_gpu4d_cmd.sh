@@ -1,0 +1,14 @@
+export NCCL_DEBUG=WARN
+for N in 2 4; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $((29510+N)) tools/nccl_parity.py > gpurun_out/r2d_par_n$N.log 2>&1
+  echo "parity N=$N rc=$?"; grep -v "^\[\|OMP_NUM\|^\*\*\*\|^NCCL version\|^\s*$" gpurun_out/r2d_par_n$N.log | tail -8
+done
+for v in "SPX_CE_AG=1" "SPX_CE_AG=0"; do
+  for c in c3 c5; do
+    st=30; [ "$c" = c3 ] && st=8
+    env $v timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29720 bench.py --gpus 4 --steps $st --warmup 3 --config $c --no-cpu-baseline --e2e-seconds 5 > gpurun_out/r2d_${c}_n4_$v.log 2>&1
+  done
+done
+SPX_CE_AG=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29730 bench.py --gpus 2 --steps 8 --warmup 3 --config c3 --no-cpu-baseline --e2e-seconds 5 > gpurun_out/r2d_c3_n2_SPX_CE_AG=1.log 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29740 bench.py --gpus 4 --steps 30 --warmup 3 --config c2 --no-cpu-baseline --e2e-seconds 5 > gpurun_out/r2d_c2_n4.log 2>&1
+python tools/bench_summary.py gpurun_out/r2d_c*.log
