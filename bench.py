@@ -420,7 +420,7 @@ def main():
     for idx, ((kind, p), t) in enumerate(zip(recs, rec_ms)):
         name = {R.K_EW: "elementwise", R.K_REDUCE: "reduce", R.K_GEMM: "gemm", R.K_GATHER: "relayout",
                 R.K_CREDUCE: "collective_local", R.K_NCCL: "nccl", R.K_PEER: "peer_allreduce",
-                R.K_SPLIT: "gemm_operand_split"}[kind]
+                R.K_SPLIT: "gemm_operand_split", R.K_COPY: "copy"}[kind]
         cls_ms[name] = cls_ms.get(name, 0.0) + float(t)
         if kind == R.K_GEMM:
             path = sess.ex.plan.record_info(idx)[1]

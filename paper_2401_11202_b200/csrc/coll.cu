@@ -64,6 +64,35 @@ __global__ void __launch_bounds__(256) creduce_kernel(const __grid_constant__ sp
   }
 }
 
+// Contiguous rank-1 fold (the copy-engine reduce-scatter's member chunks):
+// float4 per thread, all members' loads in flight before the fold.
+__global__ void __launch_bounds__(256) creduce_vec_kernel(const __grid_constant__ spx_creduce_params p) {
+  SPX_PDL_ENTRY();
+  const int d = blockIdx.y;
+  const float* const* src = reinterpret_cast<const float* const*>(p.src);
+  const int32_t* mem = reinterpret_cast<const int32_t*>(p.members) + (int64_t)d * p.n_members;
+  const int64_t b = reinterpret_cast<const int64_t*>(p.base_off)[d];
+  float4* out = reinterpret_cast<float4*>(reinterpret_cast<float* const*>(p.dst)[d]);
+  const int64_t n4 = p.numel >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < p.n_members) v[j] = reinterpret_cast<const float4*>(src[mem[j]] + b)[i];
+    float4 acc = v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      if (j >= p.n_members) break;
+      if (p.monoid == 0) {
+        acc.x = f_add(acc.x, v[j].x); acc.y = f_add(acc.y, v[j].y); acc.z = f_add(acc.z, v[j].z); acc.w = f_add(acc.w, v[j].w);
+      } else {
+        acc.x = f_max(acc.x, v[j].x); acc.y = f_max(acc.y, v[j].y); acc.z = f_max(acc.z, v[j].z); acc.w = f_max(acc.w, v[j].w);
+      }
+    }
+    out[i] = acc;
+  }
+}
+
 }  // namespace
 
 static unsigned grid_for(int64_t n) {
@@ -84,6 +113,13 @@ int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch) 
 
 int spx_launch_creduce(const spx_creduce_params& p, cudaStream_t s, int* nlaunch) {
   if (p.numel <= 0) return 0;
+  if (p.rank == 1 && p.sstride[0] == 1 && p.numel % 4 == 0 && p.n_members <= 8 && p.ndev == 1) {
+    // (the table's pointers are 16-byte aligned: arena buffers are 256 B aligned and chunks are whole float4s)
+    spx_launch(creduce_vec_kernel, dim3(grid_for(p.numel / 4), 1u), 256, 0, s, p);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+    return 0;
+  }
   spx_launch(creduce_kernel, dim3(grid_for(p.numel), (unsigned)p.ndev), 256, 0, s, p);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;

@@ -319,6 +319,18 @@ __global__ void __launch_bounds__(256, 2) peer_allgather(const __grid_constant__
   SPX_PEER_EXIT();
 }
 
+// One-block barrier (kind 3): every member arrives and waits for the others --
+// the handshakes around the copy-engine reduce-scatter (inputs complete /
+// inputs released).  Holds one SM while it waits.
+__global__ void __launch_bounds__(32) peer_barrier_kernel(const __grid_constant__ spx_peer_params p, PeerSync ps) {
+  SPX_PEER_ENTRY();
+  uint32_t* counter = reinterpret_cast<uint32_t*>(p.counter) + (int64_t)p.slot * SPX_PEER_MAX_BLOCKS;
+  const uint32_t epoch = *counter + 1u;
+  block_barrier(p, 0, epoch, ps, false);
+  if (threadIdx.x == 0) *counter = epoch;
+  SPX_PEER_EXIT();
+}
+
 }  // namespace
 
 static int peer_err_init() {
@@ -346,6 +358,21 @@ extern "C" int spx_peer_error_clear(void) {
 
 int spx_launch_peer(const spx_peer_params& p, cudaStream_t s, int* nlaunch) {
   if (p.n < 1 || p.n > 8) return spx_set_error("peer collective: group size %d", p.n);
+  if (p.kind == 3) {
+    static PeerSync bs = {~0ull, -1, nullptr};
+    if (bs.order < 0) {
+      if (peer_err_init()) return -1;
+      bs.err = g_err_dev;
+      const char* t = getenv("SPX_PEER_TIMEOUT_S");
+      const double sec = t ? atof(t) : 300.0;
+      bs.timeout_ns = sec > 0 ? (uint64_t)(sec * 1e9) : 0;
+      bs.order = 0;     // the inputs were completed by earlier kernels; the copies are stream-ordered
+    }
+    spx_launch(peer_barrier_kernel, dim3(1), 32, 0, s, p, bs);
+    SPX_CHECK_LAUNCH();
+    if (nlaunch) ++*nlaunch;
+    return 0;
+  }
   if ((p.dst & 15) || p.kind < 0 || p.kind > 2 || (p.kind == 1 && (p.count & 3)))
     return spx_set_error("peer collective: unsupported record");
   for (int m = 0; m < p.n; ++m)

@@ -89,6 +89,11 @@ class Executable:
         self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
         self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "0"))
         self.ce_ag = os.environ.get("SPX_CE_AG", "1") != "0"
+        self.ce_rs = os.environ.get("SPX_CE_RS", "0") != "0"
+        # copy-engine collectives pay a DMA setup per copy (~5-10 us): only large
+        # ones gain (C3's 16-64 MB parameter gathers +2.6%, C5's 4-8 MB ones -17%
+        # at N=4, profiles/r02_ce_ag_n4.txt)
+        self.ce_min_bytes = int(os.environ.get("SPX_CE_MIN_BYTES", str(16 << 20)))
         self.one_stream = comm_mode == "nccl" and os.environ.get("SPX_COLL_ONE_STREAM", "1") != "0"
         self.peer_bases = None          # [arena base of rank r, mapped here]
         self._peer_handles = []
@@ -1051,7 +1056,8 @@ class Executable:
             # the output -- no SM spins or copies, so the gather overlaps the
             # GEMMs completely; arguments are immutable during the step, so no
             # cross-rank handshake is needed (io calls barrier the ranks first)
-            if (direct and self.peer_bases is not None and src in c.arg_bufs and self.ce_ag):
+            if (direct and self.peer_bases is not None and src in c.arg_bufs and self.ce_ag
+                    and n * nloc * 4 >= self.ce_min_bytes):
                 for j, r in enumerate(grp):
                     q = R.CopyParams()
                     q.dev = out_a + j * nloc * 4
@@ -1080,6 +1086,43 @@ class Executable:
             offs = [sum(c._chunk_index(coords[m], apd[j]) * out_dims[j] * S[j] for j in range(len(apd)))
                     for m in grp]
             if offs == [j * nout for j in range(n)]:
+                if use_peer and self.ce_rs and (n - 1) * nout <= self.stage_elems and n * nout * 4 >= self.ce_min_bytes:
+                    # copy-engine reduce-scatter: a one-block barrier (every member's
+                    # input is complete), the copy engines pull this member's chunk of
+                    # every peer's input into staging, a local kernel folds the chunks
+                    # in member order (the reference's _combine, bit-identical), a
+                    # one-block barrier releases the inputs.  Only the two barriers
+                    # wait on peers, each holding one SM instead of every SM.
+                    k.data["stage"] = True
+                    mi = grp.index(me)
+                    peer(3, 0)
+                    ptrs = []
+                    for j, r in enumerate(grp):
+                        if r == me:
+                            ptrs.append(src_a + mi * nout * 4)
+                            continue
+                        dst = sa + (j - (j > mi)) * nout * 4
+                        q = R.CopyParams()
+                        q.dev = dst
+                        q.host = self.peer_bases[r] + (src_a - self.base) + mi * nout * 4
+                        q.bytes = nout * 4
+                        q.dir = 2
+                        self._records.append((R.K_COPY, q))
+                        ptrs.append(dst)
+                    r_ = R.CreduceParams()
+                    r_.ndev, r_.rank, r_.n_members, r_.monoid = 1, 1, n, monoid
+                    r_.numel = nout
+                    r_.dims[0] = nout
+                    r_.sstride[0] = 1
+                    r_.dtype = self.dt
+                    # src[j] = member j's chunk: member order is the fold order
+                    r_.src = self._tref(np.array(ptrs, dtype=np.uint64))
+                    r_.members = self._tref(np.arange(n, dtype=np.int32))
+                    r_.base_off = self._tref(np.zeros(1, dtype=np.int64))
+                    r_.dst = self._tref(np.array([out_a], dtype=np.uint64))
+                    self._records.append((R.K_CREDUCE, r_))
+                    peer(3, 0)
+                    return
                 if use_peer and nout % 4 == 0 and n * nout * 4 <= self.peer_max_bytes and self.peer_rs:
                     peer(2, nout, grp.index(me) * nout * 4)
                     return

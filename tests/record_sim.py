@@ -222,8 +222,8 @@ class Sim:
 
     def run_creduce(self, r: R.CreduceParams):
         dims = [r.dims[k] for k in range(r.rank)]
-        src = self.table(r.src, np.uint64, r.ndev)
         mem = self.table(r.members, np.int32, r.ndev * r.n_members)
+        src = self.table(r.src, np.uint64, max(r.ndev, int(mem.max()) + 1))
         base = self.table(r.base_off, np.int64, r.ndev)
         dst = self.table(r.dst, np.uint64, r.ndev)
         l = np.indices(dims).reshape(len(dims), -1) if dims else np.zeros((0, 1), np.int64)
@@ -346,6 +346,8 @@ def sim_nccl(module, spec, inputs, tol=1e-5, peer=False):
     assert all(len(e.records()) == nrec for e in exs)
     for i in range(nrec):
         kind = exs[0].records()[i][0]
+        if kind == R.K_PEER and exs[0].records()[i][1].kind == 3:
+            continue                     # barrier only (copy-engine reduce-scatter handshakes)
         if kind == R.K_PEER:
             # each member reads every member's source (same arena offset) and
             # folds in member order; all reads happen before any write

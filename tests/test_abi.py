@@ -45,4 +45,7 @@ def test_peer_kernels_leave_room_for_a_second_peer_kernel():
     with open(src) as fh:
         code = fh.read()
     assert "SPX_PDL_ENTRY" not in code.split("namespace {", 1)[1]
-    assert code.count("__global__ void __launch_bounds__(256, 2)") == code.count("__global__") == 3
+    # the data-moving kernels fit two blocks per SM; the one-block barrier kernel is 32 threads
+    assert code.count("__global__ void __launch_bounds__(256, 2)") == 3
+    assert code.count("__global__ void __launch_bounds__(32) peer_barrier_kernel") == 1
+    assert code.count("__global__") == 4

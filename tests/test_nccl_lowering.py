@@ -16,9 +16,14 @@ from record_sim import sim_nccl
 CASES = [c for c in golden_cases() if "local_ir" in c]
 
 
-@pytest.mark.parametrize("peer", [False, True], ids=["nccl", "peer"])
+@pytest.mark.parametrize("peer", [False, True, "ce"], ids=["nccl", "peer", "ce"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: c["key"])
-def test_nccl_mode_matches_reference(case, peer):
+def test_nccl_mode_matches_reference(case, peer, monkeypatch):
+    """'ce': the copy-engine all-gather and reduce-scatter at every size."""
+    if peer == "ce":
+        monkeypatch.setenv("SPX_CE_MIN_BYTES", "0")
+        monkeypatch.setenv("SPX_CE_RS", "1")
+        peer = True
     m = parse_module(case["local_ir"])
     spec = ShardingSpec.from_json(case["sharding"])
     base = parse_module(case["dense_ir"]) if "dense_ir" in case else m
@@ -110,3 +115,34 @@ def test_comm_setup_gloo_world2():
     assert s0[0][0] == s1[0][0]
     assert {s0[0][2], s1[0][2]} == {0, 1} and s0[0][1] == 2
     assert k0 == k1 == ["('B',)"]
+
+
+def test_copy_engine_collectives_lowering(monkeypatch):
+    """With the size threshold lifted, direct reduce-scatters become barrier +
+    copy-engine pulls + a member-order fold + barrier, and gathers of function
+    arguments become copy-engine pulls -- simulated across ranks, bit-identical
+    to the NCCL-semantics lowering."""
+    from paper_2401_11202_b200 import runtime as R
+    monkeypatch.setenv("SPX_CE_MIN_BYTES", "0")
+    monkeypatch.setenv("SPX_CE_RS", "1")
+    seen = set()
+    for key in ("rule_rs_raw", "rule_gather_merge_raw", "rule_surface_raw"):
+        case = next(c for c in CASES if c["key"] == key)
+        m = parse_module(case["local_ir"])
+        spec = ShardingSpec.from_json(case["sharding"])
+        base = parse_module(case["dense_ir"]) if "dense_ir" in case else m
+        ins = case_inputs(case, base, case["seeds"][0])
+        got, exs = sim_nccl(m, spec, ins, peer=True)
+        for k, p in exs[0].records():
+            if k == R.K_COPY:
+                seen.add("copy")
+            if k == R.K_PEER and p.kind == 3:
+                seen.add("barrier")
+        monkeypatch.setenv("SPX_CE_RS", "0")
+        monkeypatch.setenv("SPX_CE_AG", "0")
+        ref, _ = sim_nccl(m, spec, ins, peer=False)
+        monkeypatch.setenv("SPX_CE_RS", "1")
+        monkeypatch.setenv("SPX_CE_AG", "1")
+        for g, w in zip(got, ref):
+            np.testing.assert_array_equal(g, w)
+    assert seen == {"copy", "barrier"}, seen
