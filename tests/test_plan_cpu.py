@@ -194,3 +194,36 @@ def test_cross_rank_collectives_on_one_stream(name, monkeypatch):
     for idx, (kind, _) in enumerate(ex.records()):
         if kind in (R.K_NCCL, R.K_PEER):
             assert rec_stream.get(idx, 0) == ex.COMM, (name, idx)
+
+
+@pytest.mark.parametrize("name", ["c1_mlp_dense", "c3_tf2_dense", "c5_tf1_bpmpz3emb_B2M2E2"])
+def test_io_copies_in_the_plan(name):
+    """io=True (the drop-in call): one H2D copy record per (argument, device)
+    on the H2D stream, placed before the first record reading the argument,
+    one D2H copy per (result, device) on the D2H stream after the record that
+    last writes the result; every reader/writer ordering is a schedule edge."""
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.evaluator import _Dense
+    from paper_2401_11202_b200.executable import Executable
+    from paper_2401_11202_b200.programs import load_program
+    p = load_program(name)
+    dense = p.local is None or name.endswith("dense")
+    m = p.dense if dense else p.local
+    ex = Executable(_Dense(m) if dense else m, devices=[0] if dense else None, dry=True, io=True)
+    recs = ex.records()
+    stream = {i: s for i, s, _ in ex.sched}
+    nargs = len(ex.comp.arg_bufs) * ex.ndev
+    nres = len(ex.comp.result_bufs) * ex.ndev
+    assert len(ex.copy_in) == nargs and len(ex.copy_out) == nres
+    for idx in ex.copy_in.values():
+        assert recs[idx][0] == R.K_COPY and recs[idx][1].dir == 0 and stream[idx] == ex.H2D
+    for idx in ex.copy_out.values():
+        assert recs[idx][0] == R.K_COPY and recs[idx][1].dir == 1 and stream[idx] == ex.D2H
+    # kernel order: each argument's copy precedes its readers, each result's copy follows its writers
+    pos = {id(k): i for i, k in enumerate(ex.comp.kernels)}
+    for i, k in enumerate(ex.comp.kernels):
+        if k.kind == "copy" and k.data["dir"] == 0:
+            assert all(i < j for j, r in enumerate(ex.comp.kernels) if k.data["buf"] in r.ins)
+        if k.kind == "copy" and k.data["dir"] == 1:
+            assert all(j < i for j, r in enumerate(ex.comp.kernels) if k.data["buf"] in r.outs)
+    assert pos
