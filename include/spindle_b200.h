@@ -177,6 +177,12 @@ typedef struct {
 
 #define SPX_SPLIT_PIECES_ONLY 1
 
+/* 128 x 128 blocks split since the last reset whose maximum |x| lay outside
+ * [2^-45, 2^75], where the power-of-two scale is clamped to 2^+-60 and the
+ * block's small elements keep only ~2^-40-of-the-maximum accuracy (the host
+ * warns, or raises with SPX_STRICT_RANGE=1) */
+int spx_h3_range_events(uint32_t* out, int reset);
+
 enum spx_epilogue { SPX_EPI_NONE = 0, SPX_EPI_ADD = 1, SPX_EPI_SQUARE = 2, SPX_EPI_MULSCALE = 3,
                     SPX_EPI_MOMENTUM = 4 };
 

@@ -90,6 +90,8 @@ int spx_launch_ew_static_split(int id, const spx_ew_params& p, const spx_split_p
                                cudaStream_t s, int* nlaunch);
 
 int spx_num_sms();
+int spx_h3_range_split(uint32_t* out, int reset);   // gemm_h3.cu
+int spx_h3_range_ew(uint32_t* out, int reset);      // ew_static.cu
 
 // Programmatic dependent launch: every kernel starts with SPX_PDL_ENTRY --
 // it lets the NEXT kernel in the stream be scheduled once all of this grid's

@@ -10,6 +10,8 @@
 #include "interp.cuh"
 #include "h3_split.cuh"
 
+__device__ uint32_t g_h3_range_ew = 0;   // fused splits whose block scale was clamped
+
 namespace {
 
 constexpr uint32_t ins(int op, int a, int b, int d) {
@@ -179,8 +181,10 @@ ew_static_split_kernel(const __grid_constant__ spx_ew_params p, const __grid_con
     if (rb + 1 < rb1) load(rb + 1, r);
     const int ex = h3_scale_exp(m);
     const float up = h3_pow2(ex);
-    if (threadIdx.x == 0 && crank == 0)
+    if (threadIdx.x == 0 && crank == 0) {
       reinterpret_cast<float*>(q.scl + (uint64_t)((int64_t)d * q.dev_stride))[rb * q.cb + bx] = h3_pow2(-ex);
+      if (h3_out_of_range(m)) atomicAdd(&g_h3_range_ew, 1u);
+    }
 #pragma unroll
     for (int i = 0; i < H3_V; ++i) {
       const int row = rb * H3_BLOCK + crank * H3_ROWS + i * 8 + warp;
@@ -264,6 +268,15 @@ int spx_launch_ew_static(int id, const spx_ew_params& p, cudaStream_t s, int* nl
   kCatalog[id].launch(p, dim3((unsigned)b, (unsigned)p.ndev), s);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
+  return 0;
+}
+
+int spx_h3_range_ew(uint32_t* out, int reset) {
+  SPX_CUDA(cudaMemcpyFromSymbol(out, g_h3_range_ew, sizeof(uint32_t)));
+  if (reset && *out) {
+    const uint32_t z = 0;
+    SPX_CUDA(cudaMemcpyToSymbol(g_h3_range_ew, &z, sizeof(z)));
+  }
   return 0;
 }
 

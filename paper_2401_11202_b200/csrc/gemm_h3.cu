@@ -64,6 +64,8 @@ struct SplitArgs {
 // A cluster of H3_CL CTAs splits one 128 x 128 block (CTA rank r takes rows
 // 32r..32r+31): the block maximum is exchanged through distributed shared
 // memory, so a 1024 x 1024 operand spreads over 256 CTAs instead of 64.
+__device__ uint32_t g_h3_range_split = 0;   // blocks whose scale was clamped (h3_out_of_range)
+
 // split_block: block (by, bx) of operand `a` on device `dev`, this CTA's quarter.
 SPX_DEV void split_block(const SplitArgs& a, int bx, int by, int crank, int dev) {
   __shared__ float wmax[8];
@@ -96,8 +98,10 @@ SPX_DEV void split_block(const SplitArgs& a, int bx, int by, int crank, int dev)
   m = h3_cluster_max(m, wmax, cmax, crank);
   const int e = h3_scale_exp(m);
   const float up = h3_pow2(e);
-  if (threadIdx.x == 0 && crank == 0)
+  if (threadIdx.x == 0 && crank == 0) {
     reinterpret_cast<float*>(a.scl + (uint64_t)((int64_t)dev * a.scl_dev))[by * a.cb + bx] = h3_pow2(-e);
+    if (h3_out_of_range(m)) atomicAdd(&g_h3_range_split, 1u);
+  }
   __half* hi = reinterpret_cast<__half*>(a.dst + (uint64_t)((int64_t)dev * a.dst_dev));
   __half* lo = hi + (int64_t)a.rows * a.pitch;
 #pragma unroll
@@ -705,7 +709,16 @@ static void h3_shape(const spx_gemm_params& p, int& bn, int& splits) {
   const int64_t tm = (p.M + HB * H_CG - 1) / (HB * H_CG);
   const int64_t t128 = tm * ((p.N + 127) / 128) * p.ndev, t256 = tm * ((p.N + 255) / 256) * p.ndev;
   const double w128 = (double)((t128 + pairs - 1) / pairs), w256 = (double)((t256 + pairs - 1) / pairs);
-  bn = (p.N > 128 && w256 * 2 * 0.95 < w128) ? 256 : 128;
+  // a BN = 256 tile costs ~0.85 of two BN = 128 tiles on this power-capped board:
+  // the 256-wide MMA reads 52 instead of 73 B/cycle of operands from shared
+  // memory and half the B traffic from L2, and the energy saved raises the
+  // clock (C3 N=1 +2.7%, profiles/r02_c3_n1_variants.txt)
+  static double c256 = -1;
+  if (c256 < 0) {
+    const char* e = getenv("SPX_H3_BN256_COST");
+    c256 = e ? atof(e) : 0.85;
+  }
+  bn = (p.N > 128 && w256 * 2 * c256 < w128) ? 256 : 128;
   if (const char* e = getenv("SPX_H3_BN")) bn = atoi(e) == 256 ? 256 : 128;
   const int64_t tiles = bn == 256 ? t256 : t128;
   const int nch = (int)(((p.K + HBK - 1) / HBK + 1) / 2);
@@ -944,6 +957,15 @@ int spx_launch_split_batch(const spx_split_params* const* p, int n, cudaStream_t
   spx_launch(split_h16_batch_kernel, dim3((unsigned)(total * H3_CL), p[0]->ndev, 1), dim3(256), 0, s, b);
   SPX_CHECK_LAUNCH();
   if (nlaunch) ++*nlaunch;
+  return 0;
+}
+
+int spx_h3_range_split(uint32_t* out, int reset) {
+  SPX_CUDA(cudaMemcpyFromSymbol(out, g_h3_range_split, sizeof(uint32_t)));
+  if (reset && *out) {
+    const uint32_t z = 0;
+    SPX_CUDA(cudaMemcpyToSymbol(g_h3_range_split, &z, sizeof(z)));
+  }
   return 0;
 }
 

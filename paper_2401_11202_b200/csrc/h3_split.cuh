@@ -19,6 +19,16 @@ SPX_DEV int h3_scale_exp(float m) {
 }
 SPX_DEV float h3_pow2(int e) { return __uint_as_float((uint32_t)(127 + e) << 23); }
 
+// Would the block's scale have been clamped (finite, nonzero max outside
+// [2^-45, 2^75]: its small elements lose precision in the fp16 pieces)?
+// Counted so the host can report it instead of degrading silently.
+SPX_DEV bool h3_out_of_range(float m) {
+  const int E = (int)((__float_as_uint(m) >> 23) & 0xFF);
+  if (m == 0.f || E == 255) return false;
+  const int e = 141 - E;
+  return e < -60 || e > 60;
+}
+
 SPX_DEV float h3_absmax4(float m, float4 x) {
   return fmaxf(m, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
 }

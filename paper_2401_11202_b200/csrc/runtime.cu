@@ -939,6 +939,13 @@ int spx_plan_tag(uint64_t plan, int index, int tag) {
   return 0;
 }
 
+int spx_h3_range_events(uint32_t* out, int reset) {
+  uint32_t a = 0, b = 0;
+  if (spx_h3_range_split(&a, reset) || spx_h3_range_ew(&b, reset)) return -1;
+  *out = a + b;
+  return 0;
+}
+
 int spx_plan_set_host(uint64_t plan, int index, uint64_t host) {
   Plan* P = reinterpret_cast<Plan*>(plan);
   if (index < 0 || index >= (int)P->recs.size()) return spx_set_error("record index out of range");

@@ -255,7 +255,28 @@ def _io() -> bool:
     return os.environ.get("SPX_IO_OVERLAP", "1") != "0"
 
 
+def _check_range():
+    """The block-scaled fp16 splits clamp a block's scale to 2^+-60; a block whose
+    maximum lies outside [2^-45, 2^75] keeps only ~2^-40-of-its-maximum accuracy
+    for its small elements.  Report it (warning, or RangeError-like
+    FloatingPointError with SPX_STRICT_RANGE=1) instead of degrading silently."""
+    n = R.h3_range_events(reset=True)
+    if n:
+        msg = (f"{n} operand block(s) of the block-scaled fp16 GEMM split had a maximum outside "
+               f"[2^-45, 2^75]; their small elements lose precision (set SPX_GEMM_H3=0 for the 3xTF32 path)")
+        if os.environ.get("SPX_STRICT_RANGE", "0") == "1":
+            raise FloatingPointError(msg)
+        import warnings
+        warnings.warn(msg, RuntimeWarning, stacklevel=3)
+
+
 def _execute(ex, per_device, cached):
+    res = _execute_plan(ex, per_device, cached)
+    _check_range()
+    return res
+
+
+def _execute_plan(ex, per_device, cached):
     if ex.io:
         res = ex.call(per_device, replay=cached and ex.plan.captured)
         if cached and not ex.plan.captured:

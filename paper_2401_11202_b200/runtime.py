@@ -148,7 +148,7 @@ EXPORTS = [
     "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats", "spx_plan_set_host",
     "spx_host_register", "spx_host_unregister", "spx_host_copy",
     "spx_h2d_staged", "spx_d2h_staged",
-    "spx_mem_info",
+    "spx_mem_info", "spx_h3_range_events",
     "spx_comm_async_error", "spx_comm_abort", "spx_peer_error", "spx_peer_error_clear", "spx_stream_sync_watch",
 ]
 
@@ -201,6 +201,7 @@ def load(build_if_missing: bool = True):
         "spx_plan_tag": [C.c_uint64, C.c_int, C.c_int],
         "spx_plan_set_host": [C.c_uint64, C.c_int, C.c_uint64],
         "spx_mem_info": [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
+        "spx_h3_range_events": [C.POINTER(C.c_uint32), C.c_int],
         "spx_plan_exec_stats": [C.c_uint64, C.POINTER(ExecStats)],
         "spx_plan_reset_stats": [C.c_uint64],
         "spx_host_register": [C.c_void_p, C.c_uint64], "spx_host_unregister": [C.c_void_p],
@@ -338,6 +339,14 @@ class Device:
         for p in self._pinned:
             self.lib.spx_host_free(C.c_void_p(p))
         self._pinned = []
+
+
+def h3_range_events(reset: bool = True) -> int:
+    """Operand blocks whose fp16-split scale was clamped since the last reset
+    (include/spindle_b200.h spx_h3_range_events)."""
+    out = C.c_uint32()
+    call(load().spx_h3_range_events, C.byref(out), 1 if reset else 0)
+    return int(out.value)
 
 
 class PinnedPool:

@@ -473,3 +473,31 @@ def test_staged_copies_roundtrip(nbytes):
     dev.d2h_staged(b, d)
     np.testing.assert_array_equal(a, b)
     dev.free(d)
+
+
+@requires_gpu
+@pytest.mark.gpu
+def test_h3_range_detection(monkeypatch):
+    """A 128 x 128 operand block whose maximum lies outside [2^-45, 2^75] is
+    reported (the fp16 split clamps its scale and its small elements lose
+    precision) -- a warning by default, an error with SPX_STRICT_RANGE=1;
+    in-range data raise nothing."""
+    import warnings
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    mm = pkg.parse_module("func @main(%a: tensor<256x256xf32>, %b: tensor<256x256xf32>) -> tensor<256x256xf32> {\n"
+                          "  %c = matmul %a, %b : tensor<256x256xf32>\n  return %c\n}\n")
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((256, 256)).astype(np.float32)
+    b = rng.standard_normal((256, 256)).astype(np.float32)
+    R.h3_range_events(reset=True)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        pkg.interpret(mm, {"a": a, "b": b})               # in range: no warning
+    a2 = a.copy()
+    a2[:128, :128] *= np.float32(2.0 ** 90)
+    with pytest.warns(RuntimeWarning, match="outside"):
+        pkg.interpret(mm, {"a": a2, "b": b})
+    monkeypatch.setenv("SPX_STRICT_RANGE", "1")
+    with pytest.raises(FloatingPointError):
+        pkg.interpret(mm, {"a": a2, "b": b})
