@@ -158,27 +158,40 @@ ew_static_split_kernel(const __grid_constant__ spx_ew_params p, const __grid_con
   load(rb0, r);
   for (int rb = rb0; rb < rb1; ++rb) {
     float4 keep[H3_V];
+    float4 other[H3_V];     // the output that is not split (NOUT == 2)
     float m = 0.f;
 #pragma unroll
     for (int i = 0; i < H3_V; ++i) {
       const int row = rb * H3_BLOCK + crank * H3_ROWS + i * 8 + warp;
       keep[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      other[i] = keep[i];
       if (row >= q.rows || c >= q.cols) continue;
-      const int64_t e = (int64_t)row * q.cols + c;
       run_static<I...>(r[i], p.imm, std::make_integer_sequence<int, (int)sizeof...(I)>{});
       const float4 y0 = make_float4(r[i][O0].v[0], r[i][O0].v[1], r[i][O0].v[2], r[i][O0].v[3]);
-      if (!(q.skip && q.which == 0)) *reinterpret_cast<float4*>(out0 + e) = y0;
       if (NOUT > 1) {
         const float4 y1 = make_float4(r[i][O1].v[0], r[i][O1].v[1], r[i][O1].v[2], r[i][O1].v[3]);
-        if (!(q.skip && q.which == 1)) *reinterpret_cast<float4*>(out1 + e) = y1;
         keep[i] = q.which ? y1 : y0;
+        other[i] = q.which ? y0 : y1;
       } else {
         keep[i] = y0;
       }
       m = h3_absmax4(m, keep[i]);
     }
-    m = h3_cluster_max(m, wmax, cmax[rb & 1], crank);
+    // publish the partial maximum first, THEN issue the fp32 output stores and
+    // the next block's loads: the cluster barrier's release does not wait for them
+    h3_cluster_max_arrive(m, wmax, cmax[rb & 1], crank);
+#pragma unroll
+    for (int i = 0; i < H3_V; ++i) {
+      const int row = rb * H3_BLOCK + crank * H3_ROWS + i * 8 + warp;
+      if (row >= q.rows || c >= q.cols) continue;
+      const int64_t e = (int64_t)row * q.cols + c;
+      float* ok = q.which ? out1 : out0;       // the split output
+      float* oo = q.which ? out0 : out1;
+      if (!q.skip) *reinterpret_cast<float4*>(ok + e) = keep[i];
+      if (NOUT > 1) *reinterpret_cast<float4*>(oo + e) = other[i];
+    }
     if (rb + 1 < rb1) load(rb + 1, r);
+    m = h3_cluster_max_wait(cmax[rb & 1]);
     const int ex = h3_scale_exp(m);
     const float up = h3_pow2(ex);
     if (threadIdx.x == 0 && crank == 0) {

@@ -33,6 +33,37 @@ SPX_DEV float h3_absmax4(float m, float4 x) {
   return fmaxf(m, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
 }
 
+// Split form of h3_cluster_max: `arrive` publishes this CTA's partial maximum
+// to every CTA of the cluster and arrives on the cluster barrier (release);
+// `wait` completes the barrier (acquire) and returns the block maximum.  Work
+// issued between the two -- the elementwise kernel's fp32 output stores, the
+// next block's loads -- is not waited for by the release.
+SPX_DEV void h3_cluster_max_arrive(float m, float* wmax, float* cmax, int crank) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  if (tid < H3_CL) {
+    float mm = wmax[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mm = fmaxf(mm, wmax[w]);
+    uint32_t dst;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(dst)
+                 : "r"((uint32_t)__cvta_generic_to_shared(&cmax[crank])), "r"(tid));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst), "f"(mm) : "memory");
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+SPX_DEV float h3_cluster_max_wait(const float* cmax) {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  float r = cmax[0];
+#pragma unroll
+  for (int w = 1; w < H3_CL; ++w) r = fmaxf(r, cmax[w]);
+  return r;
+}
+
 // Maximum over the H3_CL CTAs of a cluster (each holding its partial max `m`
 // per thread); every thread of every CTA returns the block maximum.
 // wmax: __shared__ float[8], cmax: __shared__ float[H3_CL].
