@@ -90,6 +90,7 @@ class Executable:
         self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "0"))
         self.ce_ag = os.environ.get("SPX_CE_AG", "1") != "0"
         self.ce_rs = os.environ.get("SPX_CE_RS", "0") != "0"
+        self.peer_prebarrier = os.environ.get("SPX_PEER_PREBARRIER", "0") != "0"
         # copy-engine collectives pay a DMA setup per copy (~5-10 us): only large
         # ones gain (C3's 16-64 MB parameter gathers +2.6%, C5's 4-8 MB ones -17%
         # at N=4, profiles/r02_ce_ag_n4.txt)
@@ -1017,6 +1018,14 @@ class Executable:
         use_peer = self.peer_bases is not None and 1 < n <= 8 and slot is not None
 
         def peer(pkind, count, src_shift=0):
+            # off the critical path, a one-block barrier kernel first: the full
+            # grid launches only once every member has arrived, so it does not
+            # hold an SM on every SM while it waits for slower ranks
+            if (pkind != 3 and self.peer_prebarrier and self._cur in getattr(self, "coll_offcrit", ())
+                    and not getattr(self, "_in_prebarrier", False)):
+                self._in_prebarrier = True
+                peer(3, 0)
+                self._in_prebarrier = False
             p = R.PeerParams()
             p.kind, p.n, p.me, p.monoid, p.count, p.slot = pkind, n, grp.index(me), monoid, count, slot
             for j, r in enumerate(grp):
