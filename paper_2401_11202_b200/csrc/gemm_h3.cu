@@ -174,6 +174,7 @@ struct H3Args {
   // back a static share
   int dyn;
   uint64_t sched;                      // uint32[2], zero between launches
+  int fold_tma;                        // split-K: the last unit pulls the other partials by TMA
 };
 
 template <bool LEADER_BAR>
@@ -246,6 +247,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
   uint64_t* uq_full = tempty + 4;             // 8 B after tmem_slot
   uint64_t* uq_empty = uq_full + UQ;
   volatile int* uq = reinterpret_cast<volatile int*>(uq_empty + UQ);
+  uint64_t* fold_bar = uq_empty + UQ + 2;     // split-K fold: one barrier per drain warp (4)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (args.K + HBK - 1) / HBK;
@@ -269,6 +271,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
       // consumers: the leader's MMA warp and drain warps, the peer's producer and drain warps
       mbar_init(&uq_empty[q], 2 + 2 * 4 * S::NDG);
     }
+    for (int q = 0; q < 4; ++q) mbar_init(&fold_bar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -466,6 +469,7 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     const int q = warp & 3;
     const int dg = (warp - 4) >> 2;            // column group: columns [128 dg, 128 dg + 128)
     int cg = 0;
+    uint32_t fold_ph = 0;
     for (int j = 0;; ++j) {
       const int u = get_unit(j, false);
       if (u >= args.units) break;
@@ -553,6 +557,54 @@ gemm_h3_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         }
         old = __shfl_sync(0xffffffffu, old, 0);
         if (old != (uint32_t)(args.splits - 1)) continue;
+        if (args.fold_tma) {
+          // last: the other S-1 partial slices come in by TMA (4 KB 32 x 32
+          // boxes into the operand stages, idle now: a split GEMM gives every
+          // pair one unit) and fold with this unit's own partial, in split order
+          uint8_t* fbuf = smem + (warp - 4) * (12 * 4096);
+          uint64_t* fb = &fold_bar[warp - 4];
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_expect_tx(fb, (uint32_t)((args.splits - 1) * 4 * 4096));
+            int slot = 0;
+            for (int s2 = 0; s2 < args.splits; ++s2) {
+              if (s2 == sp) continue;
+              for (int cc = 0; cc < 4; ++cc, ++slot)
+                tma_load_3d(fbuf + slot * 4096, &tma_w, fb, col0 + cc * 32, s2 * args.M + row0, dev);
+            }
+          }
+          __syncwarp();
+          mbar_wait(fb, fold_ph);
+          fold_ph ^= 1u;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 v;
+              for (int s2 = 0; s2 < args.splits; ++s2) {
+                float4 x;
+                if (s2 == sp) {
+                  x = make_float4(acc[cc * 32 + 4 * j], acc[cc * 32 + 4 * j + 1], acc[cc * 32 + 4 * j + 2],
+                                  acc[cc * 32 + 4 * j + 3]);
+                } else {
+                  const int slot = (s2 < sp ? s2 : s2 - 1) * 4 + cc;
+                  x = *reinterpret_cast<const float4*>(fbuf + slot * 4096 + lane * 128 + ((j ^ (lane & 7)) << 4));
+                }
+                if (s2 == 0) {
+                  v = x;
+                } else {
+                  v.x = __fadd_rn(v.x, x.x); v.y = __fadd_rn(v.y, x.y);
+                  v.z = __fadd_rn(v.z, x.z); v.w = __fadd_rn(v.w, x.w);
+                }
+              }
+              acc[cc * 32 + 4 * j] = v.x; acc[cc * 32 + 4 * j + 1] = v.y;
+              acc[cc * 32 + 4 * j + 2] = v.z; acc[cc * 32 + 4 * j + 3] = v.w;
+            }
+          store_slice(&tma_c, row0);
+          if (lane == 0) *flag = 0u;          // consumed: ready for the next launch
+          continue;
+        }
+
         // last: fold the S partials in split order (own one re-read from L2)
         // straight from global to C: lane = column, every load and store one
         // 128-byte line (row-per-lane reads were L2-request bound)
@@ -843,6 +895,12 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
       SPX_CUDA(cudaMemset(g->sched, 0, 8));
     }
     a_.sched = reinterpret_cast<uint64_t>(g->sched);
+    static int ft = -1;
+    if (ft < 0) {
+      const char* e = getenv("SPX_H3_FOLD_TMA");
+      ft = e ? atoi(e) != 0 : 1;
+    }
+    a_.fold_tma = ft;
   }
   memset(&g->mw, 0, sizeof(g->mw));
   a_.flag_base = wsb;

@@ -88,6 +88,7 @@ class Executable:
         self.peer_rs = os.environ.get("SPX_PEER_RS", "1") != "0"
         self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
         self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "0"))
+        self.peer_offcrit_min_bytes = int(os.environ.get("SPX_PEER_OFFCRIT_MIN_BYTES", "0"))
         self.ce_ag = os.environ.get("SPX_CE_AG", "1") != "0"
         self.ce_rs = os.environ.get("SPX_CE_RS", "0") != "0"
         self.peer_prebarrier = os.environ.get("SPX_PEER_PREBARRIER", "0") != "0"
@@ -1035,7 +1036,7 @@ class Executable:
             p.counter = self.base + self.counter_off * 4
             # off the critical path (ZeRO-3 parameter prefetch, gradient reductions):
             # a few blocks stream it while the GEMMs keep the other SMs
-            if self._cur in getattr(self, "coll_offcrit", ()):
+            if self._cur in getattr(self, "coll_offcrit", ()) and count * 4 * n >= self.peer_offcrit_min_bytes:
                 p.max_blocks = self.peer_offcrit_blocks
             else:
                 p.max_blocks = self.peer_side_blocks if (self._cur in self.side and not self.one_stream) else 0
