@@ -337,6 +337,23 @@ int spx_event_destroy(uint64_t event);
 
 /* per-record timing of one eager run (ms per record, length = record count) */
 int spx_plan_profile(uint64_t plan, uint64_t stream, float* out_ms, int n);
+/* Timeline of one multi-stream run (dev tool): per record, ms from the start
+   of the run to the point its stream reached it with its cross-stream waits
+   met (ready_ms) and to its completion (end_ms). */
+int spx_plan_trace(uint64_t plan, uint64_t stream, float* ready_ms, float* end_ms, int n);
+
+/* ---- run-time specialised elementwise kernels (csrc/ew_jit.cu) ------------
+ * f32 elementwise records outside the static catalog get a kernel generated
+ * from the record (program as straight-line IEEE code, shape and strides as
+ * constants) and compiled by NVRTC for sm_100a when the plan is built; record
+ * path -3 (spx_plan_record_info).  SPX_EW_JIT=0 keeps the interpreter.  These
+ * entry points need no GPU. */
+int spx_ew_jit_available(void);                 /* 1 if NVRTC loaded */
+/* the generated source for a record (NUL-terminated); length or -1 */
+int spx_ew_jit_source(const spx_ew_params* p, char* buf, int64_t cap);
+/* generate + compile (cached by source) */
+int spx_ew_jit_compile(const spx_ew_params* p);
+int spx_ew_jit_stats(int* compiles, int* cached);
 
 /* ---- executed-work accounting ---------------------------------------------
  * The reference's simulator predicts, per device, the collectives of a

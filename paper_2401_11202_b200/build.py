@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libspindle_b200.so")
-SOURCES = ["runtime.cu", "ew.cu", "ew_static.cu", "reduce.cu", "coll.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_h3.cu", "peer.cu", "int32.cu"]
+SOURCES = ["runtime.cu", "ew.cu", "ew_static.cu", "reduce.cu", "coll.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_h3.cu", "peer.cu", "int32.cu", "ew_jit.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr"]

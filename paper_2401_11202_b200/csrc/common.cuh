@@ -58,6 +58,11 @@ int spx_set_error(const char* fmt, ...);
 int spx_launch_ew(const spx_ew_params& p, cudaStream_t s, int* nlaunch);
 int spx_ew_static_match(const spx_ew_params& p);     // catalog index or -1 (ew_static.cu)
 int spx_launch_ew_static(int id, const spx_ew_params& p, cudaStream_t s, int* nlaunch);
+struct SpxEwJit;                                      // run-time specialised kernel (ew_jit.cu)
+bool spx_ew_jit_enabled();
+int spx_ew_jit_prepare(const spx_ew_params& p, SpxEwJit** out);
+int spx_ew_jit_launch(const SpxEwJit* j, cudaStream_t s, int* nlaunch);
+void spx_ew_jit_free(SpxEwJit* j);
 int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_creduce(const spx_creduce_params& p, cudaStream_t s, int* nlaunch);

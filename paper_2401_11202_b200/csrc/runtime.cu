@@ -178,6 +178,7 @@ struct Record {
   std::vector<uint8_t> params;
   SpxGemmTC* tc = nullptr;
   SpxGemmH3* h3 = nullptr;      // path 3: block-scaled 3xFP16 (gemm_h3.cu)
+  SpxEwJit* jit = nullptr;      // EW path -3: run-time specialised kernel (ew_jit.cu)
   int fused_split = -1;         // EW: the next record (SPX_K_SPLIT of output `split_out`) runs inside this launch
   int split_out = -1;
   std::vector<uint8_t> split_params;
@@ -292,6 +293,7 @@ static int run_record_impl(Record& r, cudaStream_t s, int* nl) {
                                           *reinterpret_cast<const spx_split_params*>(r.split_params.data()),
                                           r.split_out, s, nl);
       if (r.path > 0) return spx_launch_ew_static(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
+      if (r.jit) return spx_ew_jit_launch(r.jit, s, nl);
       return spx_launch_ew(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
     case SPX_K_REDUCE: {
       const spx_reduce_params& q = *reinterpret_cast<const spx_reduce_params*>(r.params.data());
@@ -726,6 +728,11 @@ int spx_plan_add(uint64_t plan, int kind, const void* params, uint64_t bytes) {
     const char* e = getenv("SPX_EW_STATIC");
     if (!(e && e[0] == '0') && reinterpret_cast<const spx_ew_params*>(r.params.data())->dtype == SPX_DT_F32)
       r.path = 1 + spx_ew_static_match(*reinterpret_cast<const spx_ew_params*>(r.params.data()));
+    const spx_ew_params& q = *reinterpret_cast<const spx_ew_params*>(r.params.data());
+    if (r.path == 0 && q.dtype == SPX_DT_F32 && spx_ew_jit_enabled()) {
+      if (spx_ew_jit_prepare(q, &r.jit)) return -1;
+      r.path = -3;
+    }
   }
   if (kind == SPX_K_GEMM && reinterpret_cast<const spx_gemm_params*>(r.params.data())->dtype == SPX_DT_I32) {
     const spx_gemm_params& g = *reinterpret_cast<const spx_gemm_params*>(r.params.data());
@@ -991,6 +998,7 @@ int spx_plan_destroy(uint64_t plan) {
   for (auto& r : P->recs) {
     if (r.tc) spx_gemm_tc_free(r.tc);
     if (r.h3) spx_gemm_h3_free(r.h3);
+    if (r.jit) spx_ew_jit_free(r.jit);
     if (r.done) cudaEventDestroy(r.done);
   }
   for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
@@ -1025,6 +1033,61 @@ int spx_event_elapsed_ms(uint64_t a, uint64_t b, float* out) {
 }
 int spx_event_destroy(uint64_t ev) {
   SPX_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev)));
+  return 0;
+}
+
+// Timeline of one multi-stream run (dev tool, tools/timeline.py): every record
+// issued on its own stream as in issue_all, with an event after its waits
+// (`ready`: the stream reached it and its cross-stream dependencies were met)
+// and one after it (`end`), both in ms from the start of the run.  The host
+// enqueues the whole run behind a hold kernel, so the times carry no host
+// launch gaps (like a graph replay).
+int spx_plan_trace(uint64_t plan, uint64_t stream, float* ready_ms, float* end_ms, int n) {
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (!P->finalized && spx_plan_finalize(plan)) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nr = (int)P->recs.size();
+  std::vector<cudaEvent_t> ev(2 * nr + 1);
+  for (auto& e : ev) SPX_CUDA(cudaEventCreate(&e));
+  long long hold = 40000LL * nr + 2000000LL;
+  if (hold > 400000000LL) hold = 400000000LL;
+  hold_stream_kernel<<<1, 32, 0, s>>>(hold);
+  SPX_CUDA(cudaGetLastError());
+  SPX_CUDA(cudaEventRecord(ev[0], s));
+  if (P->two_streams) {
+    SPX_CUDA(cudaEventRecord(P->fork, s));
+    for (int k = 1; k <= SPX_SIDE_STREAMS; ++k)
+      if (P->used[k]) SPX_CUDA(cudaStreamWaitEvent(P->side[k], P->fork, 0));
+  }
+  int nl = 0;
+  spx_exec_stats t = {};
+  t.runs = 1;
+  for (int i = 0; i < nr; ++i) {
+    Record& r = P->recs[i];
+    cudaStream_t rs = (P->two_streams && r.stream) ? P->side[r.stream] : s;
+    if (P->two_streams)
+      for (int w : r.waits) SPX_CUDA(cudaStreamWaitEvent(rs, P->recs[w].done, 0));
+    SPX_CUDA(cudaEventRecord(ev[1 + 2 * i], rs));
+    if (run_record(r, rs, &nl)) return -1;
+    tally_record(r, &t);
+    SPX_CUDA(cudaEventRecord(ev[2 + 2 * i], rs));
+    if (P->two_streams && r.signal) SPX_CUDA(cudaEventRecord(r.done, rs));
+  }
+  if (P->two_streams) {
+    for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {
+      if (!P->used[k]) continue;
+      SPX_CUDA(cudaEventRecord(P->join[k], P->side[k]));
+      SPX_CUDA(cudaStreamWaitEvent(s, P->join[k], 0));
+    }
+  }
+  t.launches = nl;
+  stats_add(&P->stats, t);
+  SPX_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < nr && i < n; ++i) {
+    SPX_CUDA(cudaEventElapsedTime(&ready_ms[i], ev[0], ev[1 + 2 * i]));
+    SPX_CUDA(cudaEventElapsedTime(&end_ms[i], ev[0], ev[2 + 2 * i]));
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
   return 0;
 }
 

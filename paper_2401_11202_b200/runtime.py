@@ -143,7 +143,8 @@ EXPORTS = [
     "spx_plan_replay", "spx_plan_launch_count", "spx_plan_destroy", "spx_plan_record_info",
     "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
     "spx_stream_wait_event", "spx_memcpy_d2d",
-    "spx_plan_profile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
+    "spx_plan_profile", "spx_plan_trace", "spx_ew_jit_available", "spx_ew_jit_source",
+    "spx_ew_jit_compile", "spx_ew_jit_stats", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
     "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
     "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats", "spx_plan_set_host",
     "spx_host_register", "spx_host_unregister", "spx_host_copy",
@@ -191,6 +192,11 @@ def load(build_if_missing: bool = True):
         "spx_event_elapsed_ms": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float)],
         "spx_event_destroy": [C.c_uint64],
         "spx_plan_profile": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float), C.c_int],
+        "spx_plan_trace": [C.c_uint64, C.c_uint64, C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int],
+        "spx_ew_jit_available": [],
+        "spx_ew_jit_source": [C.c_void_p, C.c_char_p, C.c_int64],
+        "spx_ew_jit_compile": [C.c_void_p],
+        "spx_ew_jit_stats": [C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "spx_nccl_get_unique_id": [C.c_void_p],
         "spx_comm_init": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)],
         "spx_comm_destroy": [C.c_int], "spx_device_init": [C.c_int], "spx_params_size": [C.c_int],
@@ -487,6 +493,13 @@ class NativePlan:
         out = (C.c_float * self.n_records)()
         call(self.lib.spx_plan_profile, self.h, self.dev.stream, out, self.n_records)
         return np.array(out[:], dtype=np.float64)
+
+    def trace(self) -> tuple:
+        """One multi-stream run with per-record (ready, end) times in ms."""
+        r = (C.c_float * self.n_records)()
+        e = (C.c_float * self.n_records)()
+        call(self.lib.spx_plan_trace, self.h, self.dev.stream, r, e, self.n_records)
+        return np.array(r[:], dtype=np.float64), np.array(e[:], dtype=np.float64)
 
     def destroy(self):
         if self.h:

@@ -41,9 +41,10 @@ CONFIGS = [
 def plan_paths(ex):
     """Which kernels the plan launches: GEMM paths (3 = block-scaled 3xFP16,
     1 = 3xTF32, 2 = SIMT), operand splits (-1 fused into the producing
-    elementwise kernel, -2 inside a batched launch), static elementwise."""
+    elementwise kernel, -2 inside a batched launch), static elementwise,
+    run-time specialised elementwise (ew_jit.cu, path -3), interpreter."""
     from paper_2401_11202_b200 import runtime as R
-    out = {"gemm": {}, "split": {}, "ew_static": 0, "ew_generic": 0}
+    out = {"gemm": {}, "split": {}, "ew_static": 0, "ew_jit": 0, "ew_generic": 0}
     for i, (kind, _) in enumerate(ex.records()):
         k, path = ex.plan.record_info(i)
         if k == R.K_GEMM:
@@ -51,7 +52,7 @@ def plan_paths(ex):
         elif k == R.K_SPLIT:
             out["split"][path] = out["split"].get(path, 0) + 1
         elif k == R.K_EW:
-            out["ew_static" if path > 0 else "ew_generic"] += 1
+            out["ew_static" if path > 0 else "ew_jit" if path == -3 else "ew_generic"] += 1
     return out
 
 
@@ -88,6 +89,7 @@ def test_config_program_parity(name, mode, scale, seeds):
     assert paths["gemm"].get(2, 0) == 0, paths
     assert paths["gemm"].get(3, 0) >= 1, paths
     assert paths["ew_static"] > 0, paths
+    assert paths["ew_generic"] == 0, paths               # the rest run as NVRTC-compiled kernels
     if not name.startswith("c1"):
         assert paths["split"].get(-1, 0) > 0, paths      # elementwise kernels emit the fp16 pieces
 

@@ -274,12 +274,14 @@ def test_launch_counts_and_graph_replay():
             np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("static", ["0", "1"])
-def test_elementwise_static_catalog_bitexact(static, monkeypatch):
-    """The compile-time-specialised kernels (ew_static.cu) and the generic
-    interpreter (ew.cu) both reproduce numpy bit-for-bit on the model zoo's
-    programs (momentum update, square, square-grad, add, scale, sub)."""
+@pytest.mark.parametrize("static,jit", [("1", "1"), ("0", "1"), ("0", "0")])
+def test_elementwise_static_catalog_bitexact(static, jit, monkeypatch):
+    """The compile-time-specialised kernels (ew_static.cu), the run-time
+    specialised ones (ew_jit.cu) and the generic interpreter (ew.cu) all
+    reproduce numpy bit-for-bit on the model zoo's programs (momentum update,
+    square, square-grad, add, scale, sub)."""
     monkeypatch.setenv("SPX_EW_STATIC", static)
+    monkeypatch.setenv("SPX_EW_JIT", jit)
     pkg = _pkg()
     text = """func @main(%p: tensor<512x1024xf32>, %m: tensor<512x1024xf32>, %g: tensor<512x1024xf32>, %z: tensor<512x1024xf32>) -> (tensor<512x1024xf32>, tensor<512x1024xf32>, tensor<512x1024xf32>, tensor<512x1024xf32>, tensor<512x1024xf32>, tensor<512x1024xf32>) {
   %c1 = constant 0.9 : tensor<512x1024xf32>
@@ -501,3 +503,73 @@ def test_h3_range_detection(monkeypatch):
     monkeypatch.setenv("SPX_STRICT_RANGE", "1")
     with pytest.raises(FloatingPointError):
         pkg.interpret(mm, {"a": a2, "b": b})
+
+
+JIT_PROGRAMS = {
+    # nearest 2x2 upsample (the U-Net analog's rank-5 broadcast) times a full tensor
+    "upsample": """func @main(%x: tensor<64x16x32xf32>, %y: tensor<64x2x16x2x32xf32>) -> tensor<64x2x16x2x32xf32> {
+  %u = broadcast %x {dims = [0, 2, 4]} : tensor<64x2x16x2x32xf32>
+  %p = mul %u, %y : tensor<64x2x16x2x32xf32>
+  return %p
+}
+""",
+    # a 3-D transpose (no float4 path) into exp and an add
+    "transpose_exp": """func @main(%x: tensor<32x48x64xf32>, %z: tensor<64x32x48xf32>) -> tensor<64x32x48xf32> {
+  %t = transpose %x {perm = [2, 0, 1]} : tensor<64x32x48xf32>
+  %e = exp %t : tensor<64x32x48xf32>
+  %s = add %e, %z : tensor<64x32x48xf32>
+  return %s
+}
+""",
+    # -(a) * b and a three-input chain, flat (the U-Net analog's gradient products)
+    "neg_mul": """func @main(%a: tensor<1048576xf32>, %b: tensor<1048576xf32>, %c: tensor<1048576xf32>) -> (tensor<1048576xf32>, tensor<1048576xf32>) {
+  %n = neg %a : tensor<1048576xf32>
+  %p = mul %n, %b : tensor<1048576xf32>
+  %q = mul %a, %b : tensor<1048576xf32>
+  %k = constant 0.25 : tensor<1048576xf32>
+  %r = mul %k, %c : tensor<1048576xf32>
+  %s = mul %q, %r : tensor<1048576xf32>
+  return %p, %s
+}
+""",
+    # odd sizes (scalar path), row and column broadcasts, two outputs of one fused program
+    "ragged_bcast": """func @main(%x: tensor<33x17xf32>, %r: tensor<17xf32>, %c: tensor<33xf32>) -> (tensor<33x17xf32>, tensor<33x17xf32>) {
+  %rb = broadcast %r {dims = [1]} : tensor<33x17xf32>
+  %cb = broadcast %c {dims = [0]} : tensor<33x17xf32>
+  %a = add %x, %rb : tensor<33x17xf32>
+  %m = mul %a, %cb : tensor<33x17xf32>
+  %n = neg %m : tensor<33x17xf32>
+  %o = add %n, %x : tensor<33x17xf32>
+  return %m, %o
+}
+""",
+}
+
+
+@pytest.mark.parametrize("name", sorted(JIT_PROGRAMS))
+def test_ew_jit_bitexact(name, monkeypatch):
+    """Records outside the static catalog run as NVRTC-compiled kernels
+    (record path -3) and match the interpreter bit-for-bit and numpy
+    bit-for-bit (exp: within 1 ulp-scale rtol of numpy's, as the golden
+    `op_exp` cases)."""
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.evaluator import last_executable
+    m = pkg.parse_module(JIT_PROGRAMS[name])
+    rng = np.random.default_rng(11)
+    ins = {n: rng.standard_normal(t.dims).astype(np.float32) for n, t in m.func("main").args}
+    monkeypatch.setenv("SPX_EW_JIT", "1")
+    got = pkg.interpret(m, ins)
+    ex = last_executable()
+    paths = [ex.plan.record_info(i)[1] for i, (k, _) in enumerate(ex.records()) if k == R.K_EW]
+    assert -3 in paths, paths
+    monkeypatch.setenv("SPX_EW_JIT", "0")
+    interp = pkg.interpret(m, ins)
+    want = O.interpret(m, ins)
+    for g, i, w in zip(got, interp, want):
+        assert np.isfinite(g).all()
+        np.testing.assert_array_equal(g, i)
+        if name == "transpose_exp":
+            np.testing.assert_allclose(g, w, rtol=1e-6, atol=0)
+        else:
+            np.testing.assert_array_equal(g, w)
