@@ -16,6 +16,7 @@ intermediates and results | reduce scratch], identical on every device.
 from __future__ import annotations
 
 import ctypes as C
+import os as _os
 
 import numpy as np
 
@@ -58,7 +59,8 @@ class Executable:
         self.dt = R.DT_I32 if self.dtype == np.dtype(np.int32) else R.DT_F32
         if self.dt == R.DT_I32 and comm_mode != "local":
             raise TypeError("int32 programs run in local mode (the drop-in spmd_interpret / interpret)")
-        self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode, dtype=self.dtype).compile()
+        h3 = gemm_path == 0 and _os.environ.get("SPX_GEMM_H3", "1") != "0" and self.dtype == np.float32
+        self.comp = Compiler(module, func, devices=devices, comm_mode=comm_mode, dtype=self.dtype, h3=h3).compile()
         self.dry = dry
         self.device = None if dry else (device or R.Device(0))
         self.ndev = len(self.comp.devices)
@@ -824,7 +826,7 @@ class Executable:
             p.h3_shared = 1
             # split-K (opt-in, SPX_H3_SPLITK) only while nothing else computes:
             # before the first GEMM of a side stream (the forward pass)
-            p.h3_splitk = 0 if self._cur < self._first_side_gemm() else 1
+            p.h3_splitk = d.get("h3_splitk") or (0 if self._cur < self._first_side_gemm() else 1)
             p.h3_a_off = self.off[d["h3a"]]
             p.h3_b_off = self.off[d["h3b"]]
             p.h3_a_scl = p.h3_a_off + d["h3a_scl"]

@@ -108,8 +108,9 @@ class Compiler:
     in-GPU mode, [rank] for the one-process-per-GPU NCCL mode).
     """
 
-    def __init__(self, module, func="main", devices=None, comm_mode="local", dtype=np.float32):
+    def __init__(self, module, func="main", devices=None, comm_mode="local", dtype=np.float32, h3=False):
         self.module = module
+        self.h3 = h3              # GEMMs run on the block-scaled 3xFP16 kernel (gemm_h3.cu)
         self.dtype = np.dtype(dtype)
         if self.dtype not in (np.dtype(np.float32), np.dtype(np.int32)):
             raise TypeError(f"compute type {self.dtype}: the backend computes float32 or int32")
@@ -348,7 +349,16 @@ class Compiler:
         N = b_dims[1]
         splits = 1 if self.is_int else self._splitk(M, N, K, aoff, lda, boff, ldb)
         sk = self._splitk_inkernel(M, N, K, aoff, lda, boff, ldb) if splits == 1 and not at and not self.is_int else 1
-        if sk > 1:
+        h3sk = self._h3_splitk(M, N, K, aoff, lda, boff, ldb) if splits > 1 and self.h3 else 1
+        if h3sk > 1:
+            # few-tile long-K GEMM (weight gradients, K = N*H*W): the 3xFP16
+            # kernel splits K in-kernel (the last unit of a tile folds the
+            # partials in split order) and reads the operands' shared fp16
+            # pieces -- no workspace reduction launch, no tf32 operand passes
+            self.kernels.append(Kernel("gemm", [out], {ab, bb}, op_index=i,
+                                       data=dict(M=M, N=N, K=K, a=(ab, aoff, lda, at), b=(bb, boff, ldb, bt),
+                                                 splits=1, h3_splitk=h3sk, tc_ok=True)))
+        elif sk > 1:
             # few-tile activation GEMM on the critical path: partials reduced
             # inside the kernel (no workspace reduction launch)
             self.kernels.append(Kernel("gemm", [out], {ab, bb}, op_index=i,
@@ -403,6 +413,23 @@ class Compiler:
         # the split-0 CTAs stage (S-1) partial 128x128 tiles in their idle TMA
         # ring (144 KB): S <= 3
         return max(1, min(3, nk // 8, (self.NUM_SMS // 2) // pairs))
+
+    def _h3_splitk(self, M, N, K, aoff, lda, boff, ldb) -> int:
+        """In-kernel split count for the 3xFP16 kernel, or 1 when its split-K
+        does not apply (gemm_h3.cu h3_shape: BN = 128 tiles, N % 128 == 0,
+        M % 32 == 0, the tiles fill at most half the CTA pairs, >= 2 chunks of
+        128 per unit)."""
+        import os
+        if os.environ.get("SPX_H3_LONGK", "1") == "0":
+            return 1
+        if any(v % 4 for v in (aoff, lda, boff, ldb)) or M < 64 or N % 128 or M % 32:
+            return 1
+        pairs = self.NUM_SMS // 2
+        tiles = -(-M // 256) * (N // 128) * len(self.devices)
+        nch = -(-K // 128)
+        if tiles * 2 > pairs or nch < 4:
+            return 1
+        return max(1, min(pairs // tiles, nch // 2))
 
     def _splitk(self, M, N, K, aoff, lda, boff, ldb) -> int:
         """Split K when the output has too few 128x128 tiles to fill the SMs

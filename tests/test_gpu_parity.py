@@ -157,6 +157,31 @@ def test_gemm_h3_splitk(shape, at, bt, monkeypatch):
     assert O.relative_error(g0, want) < TOL
 
 
+@pytest.mark.parametrize("shape", [(512, 131072, 256), (256, 32768, 512), (128, 65536, 256)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_gemm_h3_longk_weight_gradient(shape):
+    """Few-tile long-K weight-gradient GEMMs (act^T @ dy, K = N*H*W) take the
+    3xFP16 kernel with in-kernel split-K by default (plan.py _h3_splitk): record
+    path 3, within 1e-5 of float64, bit-identical across runs."""
+    pkg = _pkg()
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.evaluator import last_executable
+    M, K, N = shape
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((K, M)).astype(np.float32)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    m = _mm_module(M, K, N, True, False)
+    (g1,) = pkg.interpret(m, {"a": a, "b": b})
+    ex = last_executable()
+    paths = [ex.plan.record_info(i)[1] for i, (k, _) in enumerate(ex.records()) if k == R.K_GEMM]
+    assert paths == [3], paths
+    (g2,) = pkg.interpret(m, {"a": a, "b": b})
+    np.testing.assert_array_equal(g1, g2)
+    want = a.T.astype(np.float64) @ b.astype(np.float64)
+    assert np.all(np.isfinite(g1))
+    assert O.relative_error(g1, want) < TOL
+
+
 @pytest.mark.parametrize("at,bt", [(False, False), (True, True)])
 @pytest.mark.parametrize("bn", ["128", "256"])
 def test_gemm_h3_dynamic_range(at, bt, bn, monkeypatch):

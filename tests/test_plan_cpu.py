@@ -81,8 +81,11 @@ def test_momentum_update_is_one_kernel():
         np.testing.assert_array_equal(g, w)
 
 
-def test_split_k_gemm_sim():
-    """Few-tile GEMMs with long K split into partials + a deterministic reduction."""
+def test_split_k_gemm_sim(monkeypatch):
+    """Few-tile GEMMs with long K split into partials + a deterministic
+    reduction (the 3xTF32 form; by default such GEMMs take the 3xFP16
+    kernel's in-kernel split, test_longk_weight_gradient_takes_h3_splitk)."""
+    monkeypatch.setenv("SPX_H3_LONGK", "0")
     from paper_2401_11202_b200 import runtime as R
     from paper_2401_11202_b200.executable import Executable
     text = """func @main(%a: tensor<4096x128xf32>, %b: tensor<4096x256xf32>) -> tensor<128x256xf32> {
@@ -227,3 +230,22 @@ def test_io_copies_in_the_plan(name):
         if k.kind == "copy" and k.data["dir"] == 1:
             assert all(j < i for j, r in enumerate(ex.comp.kernels) if k.data["buf"] in r.outs)
     assert pos
+
+
+def test_longk_weight_gradient_takes_h3_splitk(monkeypatch):
+    """A few-tile long-K GEMM (act^T @ dy) is one 3xFP16 record with an
+    in-kernel split count (no workspace + reduce records); with the 3xFP16
+    kernel off it keeps the 3xTF32 workspace split-K and its reduction."""
+    from paper_2401_11202_b200 import runtime as R
+    from paper_2401_11202_b200.executable import Executable
+    from test_gpu_parity import _mm_module
+    m = _mm_module(512, 131072, 256, True, False)
+    ex = Executable(m, devices=[0], dry=True)
+    g = [p for k, p in ex.records() if k == R.K_GEMM]
+    assert len(g) == 1 and g[0].path == 3 and g[0].h3_splitk > 1 and g[0].h3_shared == 1
+    assert not any(k == R.K_REDUCE for k, _ in ex.records())
+    monkeypatch.setenv("SPX_GEMM_H3", "0")
+    ex = Executable(m, devices=[0], dry=True)
+    g = [p for k, p in ex.records() if k == R.K_GEMM]
+    assert len(g) == 1 and g[0].splits > 1
+    assert any(k == R.K_REDUCE for k, _ in ex.records())
