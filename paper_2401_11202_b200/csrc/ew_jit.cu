@@ -9,8 +9,8 @@
 // other f32 record gets its own kernel, generated from the record and
 // compiled by NVRTC when the plan is built:
 //   * the program becomes straight-line SSA code (same IEEE operations and
-//     order as the interpreter: __fadd_rn / __fmul_rn, never contracted into
-//     FMAs (--fmad=false), expf, NaN-propagating max), so results are
+//     order as the interpreter: __fadd_rn / __fmul_rn, which are never
+//     contracted into FMAs, expf, NaN-propagating max), so results are
 //     bit-identical to the interpreter and to the reference's numpy ops;
 //   * the shape and every input's strides are compile-time constants: the
 //     index decomposition is multiply-high by constants, stride-0 (broadcast)
@@ -262,8 +262,11 @@ int compile(const std::string& src, std::string& cubin) {
   nvrtcProgram prog;
   if (nv.create(&prog, src.c_str(), "spx_ewj.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return spx_set_error("ew jit: nvrtcCreateProgram failed");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-default-device"};
-  const nvrtcResult r = nv.compile(prog, 4, opts);
+  // nvcc's defaults otherwise (the interpreter's expf comes from the same
+  // libdevice code under the same flags); the program's own adds and
+  // multiplies are __fadd_rn / __fmul_rn, which are never contracted
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
+  const nvrtcResult r = nv.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nv.log_size(prog, &n);

@@ -593,7 +593,7 @@ def test_ew_jit_bitexact(name, monkeypatch):
     want = O.interpret(m, ins)
     for g, i, w in zip(got, interp, want):
         assert np.isfinite(g).all()
-        np.testing.assert_array_equal(g, i)
+        np.testing.assert_array_equal(g, i, err_msg="jit vs interpreter")
         if name == "transpose_exp":
             np.testing.assert_allclose(g, w, rtol=1e-6, atol=0)
         else:
