@@ -900,7 +900,10 @@ int spx_gemm_h3_bind(SpxGemmH3* g, uint64_t ws) {
       const char* e = getenv("SPX_H3_FOLD_TMA");
       ft = e ? atoi(e) != 0 : 1;
     }
-    a_.fold_tma = ft;
+    // the TMA fold stages the other S-1 partial slices (4 boxes of 4 KB each)
+    // in the drain warp's 48 KB share of the operand stages: S <= 4; more
+    // splits (long-K weight gradients) fold straight from global memory
+    a_.fold_tma = ft && (g->splits - 1) * 4 * 4096 <= 12 * 4096;
   }
   memset(&g->mw, 0, sizeof(g->mw));
   a_.flag_base = wsb;

@@ -420,7 +420,10 @@ class Compiler:
         M % 32 == 0, the tiles fill at most half the CTA pairs, >= 2 chunks of
         128 per unit)."""
         import os
-        if os.environ.get("SPX_H3_LONGK", "1") == "0":
+        # opt-in: measured slower than the 3xTF32 workspace split on the U-Net
+        # analog's weight gradients (512x256x131072 ...: 3 GEMMs 0.2 -> 0.64 ms,
+        # profiles/r02_h3_longk_c4.txt) -- operand-stream bound at 1.3 TB/s
+        if os.environ.get("SPX_H3_LONGK", "0") == "0":
             return 1
         if any(v % 4 for v in (aoff, lda, boff, ldb)) or M < 64 or N % 128 or M % 32:
             return 1

@@ -233,9 +233,11 @@ def test_io_copies_in_the_plan(name):
 
 
 def test_longk_weight_gradient_takes_h3_splitk(monkeypatch):
-    """A few-tile long-K GEMM (act^T @ dy) is one 3xFP16 record with an
-    in-kernel split count (no workspace + reduce records); with the 3xFP16
-    kernel off it keeps the 3xTF32 workspace split-K and its reduction."""
+    """SPX_H3_LONGK=1: a few-tile long-K GEMM (act^T @ dy) is one 3xFP16
+    record with an in-kernel split count (no workspace + reduce records); with
+    the 3xFP16 kernel off it keeps the 3xTF32 workspace split-K and its
+    reduction."""
+    monkeypatch.setenv("SPX_H3_LONGK", "1")
     from paper_2401_11202_b200 import runtime as R
     from paper_2401_11202_b200.executable import Executable
     from test_gpu_parity import _mm_module
