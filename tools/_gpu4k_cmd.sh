@@ -1,15 +1,10 @@
 set -u
 mkdir -p gpurun_out
-for c in c3 c2; do
+for c in c3 c2 c4; do
   for n in 4; do
     timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29531 \
       tools/timeline.py --config $c --json gpurun_out/r2_tl_${c}_n$n.json > gpurun_out/r2_tl_${c}_n$n.log 2> gpurun_out/r2_tl_${c}_n$n.err
     echo "timeline $c N=$n rc=$?"
-    head -1 gpurun_out/r2_tl_${c}_n$n.log | cut -c1-1500
+    head -1 gpurun_out/r2_tl_${c}_n$n.log | cut -c1-2500
   done
-done
-for n in 2 4; do
-  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29532 \
-    bench.py --gpus $n --config c4 --steps 30 --warmup 3 > gpurun_out/r2n_c4_n$n.log 2>&1
-  python tools/bench_summary.py gpurun_out/r2n_c4_n$n.log | head -2
 done

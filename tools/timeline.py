@@ -28,11 +28,11 @@ def main():
     args = ap.parse_args()
     import bench
     from paper_2401_11202_b200 import runtime as R
-    from paper_2401_11202_b200.programs import load_program, synthetic_inputs
+    from paper_2401_11202_b200.programs import WORKLOADS, load_program, synthetic_inputs
     from paper_2401_11202_b200.session import Session
     world, rank, local = bench.dist_env()
     dist = bench.init_dist(world, rank)
-    wl = bench.WORKLOADS[args.config]
+    wl = WORKLOADS[args.config]
     prog = load_program(args.program or wl["programs"][world])
     inputs = synthetic_inputs(prog.dense, seed=0, scale=wl["scale"])
     if world == 1:
