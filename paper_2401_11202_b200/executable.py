@@ -566,24 +566,62 @@ class Executable:
         backward pass, in forward order (models.py:152-220), so as written the
         first update waits for the LAST weight gradient; hoisted, each update
         runs (on its own stream) as soon as its gradient exists."""
+        import os
         ks = self.comp.kernels
-        readers = {b for k in ks for b in k.ins}
-        prod = {}
-        after: dict = {}
-        keep = []
+        n = len(ks)
+        readers: dict = {}
         for i, k in enumerate(ks):
-            if self._terminal(k) and not any(b in readers for b in k.outs):
-                dep = max((prod[b] for b in k.ins if b in prod), default=-1)
-                after.setdefault(dep, []).append(k)
-            else:
-                keep.append((i, k))
+            for b in k.ins:
+                readers.setdefault(b, []).append(i)
+        results = set(self.comp.result_bufs)
+        # Gradient collectives (reduce-scatters / all-reduces whose outputs
+        # feed only the updates) move too, to just after their gradient: as
+        # written they all follow the backward pass, and the collective stream
+        # runs collectives in order, so the first one waited for the LAST
+        # gradient and the whole queue drained after the compute (C3 N=4: a
+        # 9.4 ms tail of reduce-scatters, profiles/r02_timeline_n4.txt).  The
+        # order stays deterministic, hence identical on every rank.
+        hoist_coll = os.environ.get("SPX_HOIST_COLL", "1") != "0"
+        movable = [False] * n
+        for i in reversed(range(n)):
+            k = ks[i]
+            rd = [j for b in k.outs for j in readers.get(b, [])]
+            if self._terminal(k) and not rd:
+                movable[i] = True
+            elif (hoist_coll and k.kind == "coll" and rd and all(movable[j] for j in rd)
+                  and not any(b in results for b in k.outs)):
+                movable[i] = True
+        # a moved kernel is emitted right after the LAST of its producers to
+        # be emitted (producers may themselves have moved)
+        prod = {}
+        waiters: dict = {}
+        remaining = {}
+        for i, k in enumerate(ks):
+            if movable[i]:
+                deps = {prod[b] for b in k.ins if b in prod}
+                remaining[i] = len(deps)
+                for d in deps:
+                    waiters.setdefault(d, []).append(i)
             for b in k.outs:
                 prod[b] = i
-        order = list(after.get(-1, []))
-        for i, k in keep:
-            order.append(k)
-            order.extend(after.get(i, []))
-        assert len(order) == len(ks)
+        order = []
+        done = set()
+
+        def emit(i):
+            order.append(ks[i])
+            done.add(i)
+            for j in waiters.get(i, []):
+                remaining[j] -= 1
+                if remaining[j] == 0:
+                    emit(j)
+
+        for i in range(n):
+            if movable[i] and remaining[i] == 0 and i not in done:
+                emit(i)
+        for i in range(n):
+            if not movable[i]:
+                emit(i)
+        assert len(order) == n
         self.comp.kernels = order
 
     def _streams(self) -> dict:
@@ -606,11 +644,13 @@ class Executable:
 
         results = set(c.result_bufs)
 
+        crit_coll_set = set()     # collectives on the collective stream that the critical path waits for
+
         def off_critical(i, side):
             rd = [j for b in ks[i].outs for j in readers.get(b, [])]
             if not rd:       # writes only results: a GEMM with a fused update
                 return ks[i].kind == "gemm" and all(b in results for b in ks[i].outs)
-            return all(self._terminal(ks[j]) or j in side for j in rd)
+            return all(self._terminal(ks[j]) or (j in side and j not in crit_coll_set) for j in rd)
 
         side: dict = {}
         crit_coll = os.environ.get("SPX_SIDE_ALL_COLLECTIVES", "0") == "1"
@@ -638,6 +678,11 @@ class Executable:
                         self.coll_offcrit.add(i)
                     if one or crit_coll or off:
                         side[i] = self.COMM
+                        if not off and os.environ.get("SPX_CRIT_PRODUCERS_MAIN", "1") != "0":
+                            # on the collective stream only for forward progress:
+                            # its producers (the row-parallel GEMM before an
+                            # all-reduce) stay on the main stream
+                            crit_coll_set.add(i)
         # splits of function arguments run on the compute stream from the start
         # of the step, overlapped with the forward pass (their GEMMs wait for them)
         for i, k in enumerate(ks):
