@@ -89,8 +89,13 @@ class Executable:
         self.peer_ag_all = os.environ.get("SPX_PEER_AG_ALL", "1") != "0"
         self.peer_rs = os.environ.get("SPX_PEER_RS", "1") != "0"
         self.peer_side_blocks = int(os.environ.get("SPX_PEER_SIDE_BLOCKS", "0"))
-        self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "0"))
-        self.peer_offcrit_min_bytes = int(os.environ.get("SPX_PEER_OFFCRIT_MIN_BYTES", "0"))
+        # large off-critical peer collectives (C3's 64 MB gradient reduce-scatters,
+        # now overlapped with the backward GEMMs since they are hoisted) run on
+        # 32 blocks so the GEMMs keep the other SMs: C3 N=4 129.2k -> 137.2k;
+        # smaller ones (C2/C5 gradient all-reduces, <= 16 MB) keep the full grid
+        # (profiles/r02_hoist_variants_n4.txt)
+        self.peer_offcrit_blocks = int(os.environ.get("SPX_PEER_OFFCRIT_BLOCKS", "32"))
+        self.peer_offcrit_min_bytes = int(os.environ.get("SPX_PEER_OFFCRIT_MIN_BYTES", str(32 << 20)))
         self.ce_ag = os.environ.get("SPX_CE_AG", "1") != "0"
         self.ce_rs = os.environ.get("SPX_CE_RS", "0") != "0"
         self.peer_prebarrier = os.environ.get("SPX_PEER_PREBARRIER", "0") != "0"

@@ -251,3 +251,46 @@ def test_longk_weight_gradient_takes_h3_splitk(monkeypatch):
     g = [p for k, p in ex.records() if k == R.K_GEMM]
     assert len(g) == 1 and g[0].splits > 1
     assert any(k == R.K_REDUCE for k, _ in ex.records())
+
+
+@pytest.mark.parametrize("name", ["c2_tf8_bpmp_B2M2", "c3_tf2_bpz3_B4", "c5_tf1_bpmpz3emb_B2M2E2"])
+def test_gradient_collectives_hoisted_and_critical_producers_on_main(name, monkeypatch):
+    """Gradient collectives (outputs read only by the updates) follow their
+    gradient instead of the whole backward pass; the kernel order stays a
+    valid topological order; GEMMs whose output feeds a critical-path
+    collective stay on the main stream (timelines in
+    profiles/r02_timeline_n4.txt)."""
+    from record_sim import _dry_comms
+    from paper_2401_11202_b200.executable import Executable
+    from paper_2401_11202_b200.programs import load_program
+    for k in ("SPX_HOIST_COLL", "SPX_CRIT_PRODUCERS_MAIN", "SPX_COLL_ONE_STREAM"):
+        monkeypatch.delenv(k, raising=False)
+    p = load_program(name)
+    ex = Executable(p.local, devices=[0], comm_mode="nccl", dry=True, comm_factory=lambda e: _dry_comms(e, True))
+    ks = ex.comp.kernels
+    made = set(ex.comp.arg_bufs)
+    for k in ks:                                      # topological
+        assert all(b in made for b in k.ins), k
+        made.update(k.outs)
+    prod = {b: i for i, k in enumerate(ks) for b in k.outs}
+    readers = {}
+    for i, k in enumerate(ks):
+        for b in k.ins:
+            readers.setdefault(b, []).append(i)
+    grad_colls = 0
+    for i, k in enumerate(ks):
+        if k.kind != "coll" or k.data["kind"] in ("all_slice",):
+            continue
+        rd = [j for b in k.outs for j in readers.get(b, [])]
+        if rd and all(ex._terminal(ks[j]) or ks[j].kind == "coll" for j in rd):
+            grad_colls += 1
+            # hoisted: right after (or within a few kernels of) its gradient
+            src = max(prod[b] for b in k.ins if b in prod)
+            assert i - src <= 3, (name, i, src)
+        elif i not in ex.coll_offcrit:
+            # a critical collective: its GEMM producers run on the main stream
+            for b in k.ins:
+                j = prod.get(b)
+                if j is not None and ks[j].kind == "gemm":
+                    assert ex.stream_of.get(j, 0) == 0, (name, i, j)
+    assert grad_colls > 0
