@@ -609,23 +609,54 @@ class Executable:
                     waiters.setdefault(d, []).append(i)
             for b in k.outs:
                 prod[b] = i
+        # A moved collective yields to the next critical collective: it is
+        # emitted after the next collective that stays in place, or after
+        # `window` further kernels, whichever comes first.  On the collective
+        # stream (in-order) a gradient all-reduce queued right after its
+        # weight-gradient GEMM would otherwise hold back the row-parallel
+        # all-reduce of the same layer, which the critical path waits for
+        # (C2 N=4 timeline: ~45 us per block).
+        window = int(os.environ.get("SPX_HOIST_YIELD", "8"))
         order = []
         done = set()
+        deferred: list = []
+
+        def talks(k):          # a collective that moves data between ranks / devices
+            return k.kind == "coll" and k.data.get("kind") != "all_slice"
+
+        def release(j):
+            if window > 0 and talks(ks[j]):
+                deferred.append([j, window])
+                done.add(j)            # queued: emitted by flush()
+            else:
+                emit(j)
 
         def emit(i):
             order.append(ks[i])
-            done.add(i)
+            done.add(i)     # (already there for a deferred collective)
             for j in waiters.get(i, []):
                 remaining[j] -= 1
                 if remaining[j] == 0:
-                    emit(j)
+                    release(j)
+
+        def flush(all_=True):
+            while deferred and (all_ or deferred[0][1] <= 0):
+                emit(deferred.pop(0)[0])
 
         for i in range(n):
             if movable[i] and remaining[i] == 0 and i not in done:
-                emit(i)
+                release(i)
         for i in range(n):
-            if not movable[i]:
-                emit(i)
+            if movable[i]:
+                continue
+            emit(i)
+            if talks(ks[i]):
+                flush()
+            else:
+                for d in deferred:
+                    d[1] -= 1
+                flush(all_=False)
+        flush()
         assert len(order) == n
         self.comp.kernels = order
 
