@@ -353,6 +353,11 @@ int spx_ew_jit_available(void);                 /* 1 if NVRTC loaded */
 int spx_ew_jit_source(const spx_ew_params* p, char* buf, int64_t cap);
 /* generate + compile (cached by source) */
 int spx_ew_jit_compile(const spx_ew_params* p);
+/* the same record with the split `sp` of output `which` fused in (4-CTA
+   clusters per 128 x 128 block, fp16 pieces bit-identical to the standalone
+   split; skip = 1: output `which` not stored in fp32) */
+int spx_ew_jit_split_source(const spx_ew_params* p, int which, int skip, char* buf, int64_t cap);
+int spx_ew_jit_split_compile(const spx_ew_params* p, const spx_split_params* sp, int which, int skip);
 int spx_ew_jit_stats(int* compiles, int* cached);
 
 /* ---- executed-work accounting ---------------------------------------------

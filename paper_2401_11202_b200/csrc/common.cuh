@@ -63,6 +63,7 @@ bool spx_ew_jit_enabled();
 int spx_ew_jit_prepare(const spx_ew_params& p, SpxEwJit** out);
 int spx_ew_jit_launch(const SpxEwJit* j, cudaStream_t s, int* nlaunch);
 void spx_ew_jit_free(SpxEwJit* j);
+int spx_ew_jit_split_prepare(const spx_ew_params& p, const spx_split_params& sp, int which, int skip, SpxEwJit** out);
 int spx_launch_reduce(const spx_reduce_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_gather(const spx_gather_params& p, cudaStream_t s, int* nlaunch);
 int spx_launch_creduce(const spx_creduce_params& p, cudaStream_t s, int* nlaunch);

@@ -284,6 +284,12 @@ int spx_launch_ew_static(int id, const spx_ew_params& p, cudaStream_t s, int* nl
   return 0;
 }
 
+uint32_t* spx_h3_range_ew_counter() {
+  void* a = nullptr;
+  if (cudaGetSymbolAddress(&a, g_h3_range_ew) != cudaSuccess) return nullptr;
+  return static_cast<uint32_t*>(a);
+}
+
 int spx_h3_range_ew(uint32_t* out, int reset) {
   SPX_CUDA(cudaMemcpyFromSymbol(out, g_h3_range_ew, sizeof(uint32_t)));
   if (reset && *out) {

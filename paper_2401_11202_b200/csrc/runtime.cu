@@ -179,6 +179,7 @@ struct Record {
   SpxGemmTC* tc = nullptr;
   SpxGemmH3* h3 = nullptr;      // path 3: block-scaled 3xFP16 (gemm_h3.cu)
   SpxEwJit* jit = nullptr;      // EW path -3: run-time specialised kernel (ew_jit.cu)
+  SpxEwJit* jit_split = nullptr;  // EW path -3 with the next record's split fused in
   int fused_split = -1;         // EW: the next record (SPX_K_SPLIT of output `split_out`) runs inside this launch
   int split_out = -1;
   std::vector<uint8_t> split_params;
@@ -288,6 +289,7 @@ static int run_record_impl(Record& r, cudaStream_t s, int* nl) {
     case SPX_K_EW:
       if (reinterpret_cast<const spx_ew_params*>(r.params.data())->dtype == SPX_DT_I32)
         return spx_launch_ew_i32(*reinterpret_cast<const spx_ew_params*>(r.params.data()), s, nl);
+      if (r.fused_split >= 0 && r.jit_split) return spx_ew_jit_launch(r.jit_split, s, nl);
       if (r.fused_split >= 0)
         return spx_launch_ew_static_split(r.path - 1, *reinterpret_cast<const spx_ew_params*>(r.params.data()),
                                           *reinterpret_cast<const spx_split_params*>(r.split_params.data()),
@@ -781,14 +783,29 @@ int spx_plan_finalize(uint64_t plan) {
     const char* e = getenv("SPX_EW_SPLIT_FUSE");
     fuse = e ? atoi(e) != 0 : 1;
   }
+  const char* jse = getenv("SPX_EW_JIT_SPLIT");
+  const bool jit_split = !(jse && atoi(jse) == 0);
+  const char* poe = getenv("SPX_PIECES_ONLY");
+  const bool pieces_only = !(poe && atoi(poe) == 0);
   for (size_t i = 0; fuse && i + 1 < P->recs.size(); ++i) {
     Record &a = P->recs[i], &b = P->recs[i + 1];
-    if (a.kind != SPX_K_EW || a.path <= 0 || b.kind != SPX_K_SPLIT || a.stream != b.stream || !b.waits.empty() ||
-        a.fused_split >= 0)
+    const bool jit = a.path == -3 && a.jit && jit_split;
+    if (a.kind != SPX_K_EW || (a.path <= 0 && !jit) || b.kind != SPX_K_SPLIT || a.stream != b.stream ||
+        !b.waits.empty() || a.fused_split >= 0)
       continue;
     const int j = spx_ew_split_match(*reinterpret_cast<const spx_ew_params*>(a.params.data()),
                                      *reinterpret_cast<const spx_split_params*>(b.params.data()));
     if (j < 0) continue;
+    if (jit) {
+      // the generated kernel with the split's cluster structure around it
+      const spx_split_params& sp = *reinterpret_cast<const spx_split_params*>(b.params.data());
+      const int skip = pieces_only && (sp.flags & SPX_SPLIT_PIECES_ONLY) ? 1 : 0;
+      if (spx_ew_jit_split_prepare(*reinterpret_cast<const spx_ew_params*>(a.params.data()), sp, j, skip,
+                                   &a.jit_split)) {
+        g_err[0] = 0;
+        continue;                 // not fusable (e.g. >= 2^31 elements): the split runs on its own
+      }
+    }
     a.fused_split = (int)(i + 1);
     a.split_out = j;
     a.split_params = b.params;
@@ -999,6 +1016,7 @@ int spx_plan_destroy(uint64_t plan) {
     if (r.tc) spx_gemm_tc_free(r.tc);
     if (r.h3) spx_gemm_h3_free(r.h3);
     if (r.jit) spx_ew_jit_free(r.jit);
+    if (r.jit_split) spx_ew_jit_free(r.jit_split);
     if (r.done) cudaEventDestroy(r.done);
   }
   for (int k = 1; k <= SPX_SIDE_STREAMS; ++k) {

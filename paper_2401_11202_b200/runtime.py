@@ -144,7 +144,7 @@ EXPORTS = [
     "spx_event_create", "spx_event_record", "spx_event_elapsed_ms", "spx_event_destroy",
     "spx_stream_wait_event", "spx_memcpy_d2d",
     "spx_plan_profile", "spx_plan_trace", "spx_ew_jit_available", "spx_ew_jit_source",
-    "spx_ew_jit_compile", "spx_ew_jit_stats", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
+    "spx_ew_jit_compile", "spx_ew_jit_stats", "spx_ew_jit_split_source", "spx_ew_jit_split_compile", "spx_host_alloc", "spx_host_free", "spx_plan_set_sched",
     "spx_ipc_get_handle", "spx_ipc_open", "spx_ipc_close",
     "spx_plan_tag", "spx_plan_exec_stats", "spx_plan_reset_stats", "spx_plan_set_host",
     "spx_host_register", "spx_host_unregister", "spx_host_copy",
@@ -197,6 +197,8 @@ def load(build_if_missing: bool = True):
         "spx_ew_jit_source": [C.c_void_p, C.c_char_p, C.c_int64],
         "spx_ew_jit_compile": [C.c_void_p],
         "spx_ew_jit_stats": [C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "spx_ew_jit_split_source": [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_int64],
+        "spx_ew_jit_split_compile": [C.c_void_p, C.c_void_p, C.c_int, C.c_int],
         "spx_nccl_get_unique_id": [C.c_void_p],
         "spx_comm_init": [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)],
         "spx_comm_destroy": [C.c_int], "spx_device_init": [C.c_int], "spx_params_size": [C.c_int],

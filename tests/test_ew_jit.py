@@ -154,3 +154,34 @@ def test_config_programs_generic_records_compile(lib):
             _compile(lib, p)
             n += 1
     assert n >= 4
+
+
+def test_fused_split_variant_compiles(lib):
+    """The elementwise records of the U-Net analog whose output is split for a
+    3xFP16 GEMM right after them (rank > 2: outside the static kernels) get
+    the fused-split variant (4-CTA clusters, pieces bit-identical to the
+    standalone split), with and without the fp32 store."""
+    from paper_2401_11202_b200.executable import Executable
+    from paper_2401_11202_b200.programs import load_program
+    prog = load_program("c4_unet_dense")
+    ex = Executable(prog.dense, devices=[0], dry=True)
+    recs = ex.records()
+    match = getattr(lib, "_Z19spx_ew_static_matchRK13spx_ew_params")
+    match.restype = C.c_int
+    n = 0
+    for (ka, a), (kb, b) in zip(recs, recs[1:]):
+        if ka != R.K_EW or kb != R.K_SPLIT or (a.rank <= 2 and match(C.byref(a)) >= 0):
+            continue
+        which = [a.out_off[j] for j in range(a.n_out)].index(b.src_off) if b.src_off in \
+            [a.out_off[j] for j in range(a.n_out)] else -1
+        if which < 0:
+            continue
+        buf = C.create_string_buffer(1 << 20)
+        for skip in (0, 1):
+            assert lib.spx_ew_jit_split_source(C.byref(a), which, skip, buf, len(buf)) > 0
+            src = buf.value.decode()
+            assert "__cluster_dims__(4, 1, 1)" in src and "cvt.rn.f16x2.f32" in src
+            rc = lib.spx_ew_jit_split_compile(C.byref(a), C.byref(b), which, skip)
+            assert rc == 0, lib.spx_last_error()
+        n += 1
+    assert n >= 2
