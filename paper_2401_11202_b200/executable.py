@@ -609,14 +609,14 @@ class Executable:
                     waiters.setdefault(d, []).append(i)
             for b in k.outs:
                 prod[b] = i
-        # A moved collective yields to the next critical collective: it is
-        # emitted after the next collective that stays in place, or after
-        # `window` further kernels, whichever comes first.  On the collective
-        # stream (in-order) a gradient all-reduce queued right after its
-        # weight-gradient GEMM would otherwise hold back the row-parallel
-        # all-reduce of the same layer, which the critical path waits for
-        # (C2 N=4 timeline: ~45 us per block).
-        window = int(os.environ.get("SPX_HOIST_YIELD", "8"))
+        # SPX_HOIST_YIELD=w (opt-in): a moved collective yields to the next
+        # critical collective -- emitted after the next collective that stays
+        # in place, or after w further kernels -- so that on the in-order
+        # collective stream a gradient all-reduce does not hold back the
+        # row-parallel all-reduce of the same layer (C2 N=4 timeline: ~45 us
+        # per block).  Measured slower (C2 N=4 894k -> 874k, C5 853k -> 837k,
+        # C3 137.9k -> 136.4k, profiles/r02_hoist_yield_n4.txt): off.
+        window = int(os.environ.get("SPX_HOIST_YIELD", "0"))
         order = []
         done = set()
         deferred: list = []

@@ -284,8 +284,7 @@ def test_gradient_collectives_hoisted_and_critical_producers_on_main(name, monke
         rd = [j for b in k.outs for j in readers.get(b, [])]
         if rd and all(ex._terminal(ks[j]) or ks[j].kind == "coll" for j in rd):
             grad_colls += 1
-            # hoisted: within a few kernels of its gradient (it yields to the
-            # next critical collective, or SPX_HOIST_YIELD = 8 kernels)
+            # hoisted: within a few kernels of its gradient
             src = max(prod[b] for b in k.ins if b in prod)
             assert i - src <= 16, (name, i, src)
         elif i not in ex.coll_offcrit:
