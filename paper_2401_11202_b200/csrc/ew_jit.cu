@@ -167,13 +167,14 @@ bool gen_prog(const spx_ew_params& p, std::ostringstream& s) {
 
 // Loads of every input at flat element `ev` (an expression) into x<u>_<j>[W]:
 // the index decomposition over the record's dims with constant divisors.
-void gen_loads(const spx_ew_params& p, std::ostringstream& s, int u, const std::string& ev, bool vec, bool wide) {
+void gen_loads(const spx_ew_params& p, std::ostringstream& s, int u, const std::string& ev, bool vec, bool wide,
+               bool declare = true) {
   const int W = vec ? 4 : 1;
   const int rk = p.rank > 0 ? p.rank : 1;
   const char* IX = wide ? "u64" : "u32";
   const char* SUF = wide ? "ull" : "u";
   const int64_t last = p.rank > 0 ? p.dims[rk - 1] : 1;
-  if (p.n_in > 0) {
+  if (p.n_in > 0 && declare) {
     s << "    float x" << u << "_0[" << W << "]";
     for (int j = 1; j < p.n_in; ++j) s << ", x" << u << "_" << j << "[" << W << "]";
     s << ";\n";
@@ -382,7 +383,7 @@ __device__ __forceinline__ void store4(unsigned short* hi, unsigned short* lo, i
 }
 extern "C" __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256) spx_ewjs(const __grid_constant__ A a) {
   __shared__ float wmax[8];
-  __shared__ float cmax[4];
+  __shared__ float cmax[2][4];
   asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = blockIdx.z;
@@ -397,49 +398,71 @@ extern "C" __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256) spx_
   const int rbs = (int)((a.rows + 127) / 128);
   const int rb0 = blockIdx.y * (int)a.nb;
   const int rb1 = rb0 + (int)a.nb < rbs ? rb0 + (int)a.nb : rbs;
+)SRC";
+  // the inputs of the CTA's 4 rows (32 rows / 8 warps) of one row block, kept
+  // across iterations: block rb+1 is loaded while the cluster exchanges
+  // block rb's maximum (as ew_static_split_kernel)
+  for (int i = 0; i < 4; ++i)
+    if (p.n_in > 0) {
+      s << "  float x" << i << "_0[4]";
+      for (int k = 1; k < p.n_in; ++k) s << ", x" << i << "_" << k << "[4]";
+      s << ";\n";
+    }
+  s << "  auto load = [&](int rb) {\n";
+  for (int i = 0; i < 4; ++i) {
+    s << "   {\n    const i64 row = (i64)rb * 128 + crank * 32 + " << i * 8 << " + warp;\n"
+      << "    if (row < a.rows && cc < a.cols) {\n";
+    gen_loads(p, s, i, "(u32)(row * a.cols + cc)", true, false, false);
+    s << "    }\n   }\n";
+  }
+  s << "  };\n";
+  s << R"SRC(  if (rb0 < rb1) load(rb0);
   for (int rb = rb0; rb < rb1; ++rb) {
     float keep[4][4];
     float m = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const i64 row = (i64)rb * 128 + crank * 32 + i * 8 + warp;
-      keep[i][0] = keep[i][1] = keep[i][2] = keep[i][3] = 0.f;
-      if (row >= a.rows || cc >= a.cols) continue;
 )SRC";
-  gen_loads(p, s, 0, "(u32)(row * a.cols + cc)", true, false);
-  s << "      float y[" << p.n_out << "][4];\n";
-  for (int k = 0; k < 4; ++k) {
-    s << "      prog(a.imm";
-    for (int j = 0; j < p.n_in; ++j) s << ", x0_" << j << "[" << k << "]";
-    for (int o = 0; o < p.n_out; ++o) s << ", y[" << o << "][" << k << "]";
-    s << ");\n";
+  for (int i = 0; i < 4; ++i) {
+    s << "    {\n      const i64 row = (i64)rb * 128 + crank * 32 + " << i * 8 << " + warp;\n"
+      << "      keep[" << i << "][0] = keep[" << i << "][1] = keep[" << i << "][2] = keep[" << i << "][3] = 0.f;\n"
+      << "      if (row < a.rows && cc < a.cols) {\n"
+      << "        float y[" << p.n_out << "][4];\n";
+    for (int k = 0; k < 4; ++k) {
+      s << "        prog(a.imm";
+      for (int jj = 0; jj < p.n_in; ++jj) s << ", x" << i << "_" << jj << "[" << k << "]";
+      for (int o = 0; o < p.n_out; ++o) s << ", y[" << o << "][" << k << "]";
+      s << ");\n";
+    }
+    s << "        const i64 e = row * a.cols + cc;\n";
+    for (int o = 0; o < p.n_out; ++o) {
+      if (o == which && skip) continue;
+      s << "        *(float4*)(q" << o << " + e) = make_float4(y[" << o << "][0], y[" << o << "][1], y[" << o
+        << "][2], y[" << o << "][3]);\n";
+    }
+    s << "        for (int k = 0; k < 4; ++k) { keep[" << i << "][k] = y[" << which << "][k]; m = fmaxf(m, fabsf(keep["
+      << i << "][k])); }\n      }\n    }\n";
   }
-  s << "      const i64 e = row * a.cols + cc;\n";
-  for (int o = 0; o < p.n_out; ++o) {
-    if (o == which && skip) continue;
-    s << "      *(float4*)(q" << o << " + e) = make_float4(y[" << o << "][0], y[" << o << "][1], y[" << o << "][2], y["
-      << o << "][3]);\n";
-  }
-  s << "      for (int k = 0; k < 4; ++k) { keep[i][k] = y[" << which << "][k]; m = fmaxf(m, fabsf(keep[i][k])); }\n";
-  s << R"SRC(    }
-    // block maximum over the cluster (distributed shared memory)
+  s << R"SRC(    // block maximum over the cluster (distributed shared memory); the next
+    // block's loads are issued between the barrier's arrive and its wait
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) wmax[warp] = m;
     __syncthreads();
+    float* cm = cmax[rb & 1];
     if (threadIdx.x < 4) {
       float mm = wmax[0];
 #pragma unroll
       for (int w = 1; w < 8; ++w) mm = fmaxf(mm, wmax[w]);
       u32 dst;
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst)
-                   : "r"((u32)__cvta_generic_to_shared(&cmax[crank])), "r"((u32)threadIdx.x));
+                   : "r"((u32)__cvta_generic_to_shared(&cm[crank])), "r"((u32)threadIdx.x));
       asm volatile("st.shared::cluster.f32 [%0], %1;" :: "r"(dst), "f"(mm) : "memory");
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    float bm = cmax[0];
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (rb + 1 < rb1) load(rb + 1);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    float bm = cm[0];
 #pragma unroll
-    for (int w = 1; w < 4; ++w) bm = fmaxf(bm, cmax[w]);
+    for (int w = 1; w < 4; ++w) bm = fmaxf(bm, cm[w]);
     const int ex = sc_exp(bm);
     const float up = pw2(ex);
     if (threadIdx.x == 0 && crank == 0) {
@@ -452,8 +475,6 @@ extern "C" __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256) spx_
       if (row >= a.rows || cc >= a.cols) continue;
       store4(hi, lo, row * a.pitch + cc, keep[i], up);
     }
-    // cmax / wmax are rewritten by the next block: every CTA has read them
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 }
 )SRC";

@@ -704,6 +704,7 @@ class Executable:
         one = c.comm_mode == "nccl" and os.environ.get("SPX_COLL_ONE_STREAM", "1") != "0"
         args = set(c.arg_bufs)
         self.coll_offcrit = set()     # collectives nothing on the critical path waits for
+        self.crit_colls = set()       # cross-rank collectives the critical path waits for
         if c.comm_mode == "nccl":
             for i in reversed(range(len(ks))):
                 k = ks[i]
@@ -714,6 +715,8 @@ class Executable:
                         self.coll_offcrit.add(i)
                     if one or crit_coll or off:
                         side[i] = self.COMM
+                        if not off:
+                            self.crit_colls.add(i)
                         if not off and os.environ.get("SPX_CRIT_PRODUCERS_MAIN", "1") != "0":
                             # on the collective stream only for forward progress:
                             # its producers (the row-parallel GEMM before an
@@ -914,6 +917,10 @@ class Executable:
             p.h3_b_scl = p.h3_b_off + d["h3b_scl"]
         # with collectives overlapped on a side stream, leave SMs for NCCL's CTAs
         p.reserve_sms = self.reserve_sms
+        if self.stream_of.get(self._cur) == self.COMPUTE and getattr(self, "crit_colls", None):
+            # a side-stream GEMM (persistent, whole-SM CTAs) would otherwise hold
+            # every SM when a critical-path collective is launched next to it
+            p.reserve_sms = max(p.reserve_sms, int(_os.environ.get("SPX_SIDE_GEMM_RESERVE", "0")))
         p.dtype = self.dt
         self._records.append((R.K_GEMM, p))
 
