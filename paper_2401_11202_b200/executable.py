@@ -724,8 +724,14 @@ class Executable:
                             crit_coll_set.add(i)
         # splits of function arguments run on the compute stream from the start
         # of the step, overlapped with the forward pass (their GEMMs wait for them)
+        # ... and so do splits of prefetched parameter gathers (ZeRO-3): they
+        # depend only on the gather, not on the forward pass, so on the compute
+        # stream they run as soon as it lands instead of in front of their GEMM
+        # on the main stream (C3 N=4: ~4 ms of main-stream splits per step)
+        pref_split = os.environ.get("SPX_PREFETCH_SPLITS", "1") != "0"
+        coll_out = {b: j for j in self.coll_offcrit for b in ks[j].outs}
         for i, k in enumerate(ks):
-            if k.kind == "split" and k.data["src"][0] in args:
+            if k.kind == "split" and (k.data["src"][0] in args or (pref_split and k.data["src"][0] in coll_out)):
                 side[i] = self.COMPUTE
         # side-stream GEMMs (whole-SM CTAs): with every collective on one stream
         # they cannot close a cross-rank residency cycle; under the round-1
