@@ -724,11 +724,11 @@ class Executable:
                             crit_coll_set.add(i)
         # splits of function arguments run on the compute stream from the start
         # of the step, overlapped with the forward pass (their GEMMs wait for them)
-        # ... and so do splits of prefetched parameter gathers (ZeRO-3): they
-        # depend only on the gather, not on the forward pass, so on the compute
-        # stream they run as soon as it lands instead of in front of their GEMM
-        # on the main stream (C3 N=4: ~4 ms of main-stream splits per step)
-        pref_split = os.environ.get("SPX_PREFETCH_SPLITS", "1") != "0"
+        # ... and, with SPX_PREFETCH_SPLITS=1, the splits of prefetched
+        # parameter gathers (ZeRO-3), which depend only on the gather: measured
+        # neutral (C3 N=4 140.3k vs 140.7k, profiles/r02_prefetch_splits_n4.txt),
+        # so they stay in front of their GEMM on the main stream
+        pref_split = os.environ.get("SPX_PREFETCH_SPLITS", "0") != "0"
         coll_out = {b: j for j in self.coll_offcrit for b in ks[j].outs}
         for i, k in enumerate(ks):
             if k.kind == "split" and (k.data["src"][0] in args or (pref_split and k.data["src"][0] in coll_out)):
