@@ -218,7 +218,6 @@ void gen_loads(const spx_ew_params& p, std::ostringstream& s, int u, const std::
 std::string gen_source(const spx_ew_params& p) {
   const bool vec = jit_vec(p);
   const int W = vec ? 4 : 1;
-  const int rk = p.rank > 0 ? p.rank : 1;
   const bool wide = p.numel >= (int64_t(1) << 31);
   const char* IX = wide ? "u64" : "u32";
   const char* SUF = wide ? "ull" : "u";     // constants in the index type (32-bit divisions stay 32-bit)
@@ -226,37 +225,8 @@ std::string gen_source(const spx_ew_params& p) {
   std::ostringstream s;
   s << "typedef unsigned int u32; typedef unsigned long long u64; typedef long long i64;\n"
     << "struct A { u64 base; i64 dev_stride; i64 in[" << ni << "]; i64 out[" << p.n_out << "]; float imm[" << np
-    << "]; };\n"
-    << "__device__ __forceinline__ float fmx(float a, float b) { return (a != a || a > b) ? a : b; }\n";
-  // the program, one scalar lane
-  s << "__device__ __forceinline__ void prog(const float* __restrict__ im";
-  for (int j = 0; j < p.n_in; ++j) s << ", float x" << j;
-  for (int o = 0; o < p.n_out; ++o) s << ", float& y" << o;
-  s << ") {\n";
-  for (int k = 0; k < SPX_NREG; ++k) s << "  float r" << k << " = " << (k < p.n_in ? "x" + std::to_string(k) : "0.f") << ";\n";
-  for (int i = 0; i < p.n_prog; ++i) {
-    const spx_insn& in = p.prog[i];
-    if (in.a < 0 || in.a >= SPX_NREG || in.b < 0 || in.b >= SPX_NREG || in.dst < 0 || in.dst >= SPX_NREG) {
-      spx_set_error("ew jit: slot out of range");
-      return std::string();
-    }
-    std::string e;
-    if (op_expr(in.op, "r" + std::to_string(in.a), "r" + std::to_string(in.b), "im[" + std::to_string(i) + "]", e)) {
-      spx_set_error("ew jit: bad opcode %d", in.op);
-      return std::string();
-    }
-    s << "  r" << in.dst << " = " << e << ";\n";
-  }
-  for (int o = 0; o < p.n_out; ++o) {
-    if (p.out_reg[o] < 0 || p.out_reg[o] >= SPX_NREG) {
-      spx_set_error("ew jit: output slot out of range");
-      return std::string();
-    }
-    s << "  y" << o << " = r" << p.out_reg[o] << ";\n";
-  }
-  s << "}\n";
-  // the kernel
-  const int64_t last = p.rank > 0 ? p.dims[rk - 1] : 1;
+    << "]; };\n";
+  if (!gen_prog(p, s)) return std::string();
   const int64_t n = p.numel / W;
   s << "extern \"C\" __global__ void __launch_bounds__(256) spx_ewj(const __grid_constant__ A a) {\n"
     << "  asm volatile(\"griddepcontrol.launch_dependents;\\n\\tgriddepcontrol.wait;\" ::: \"memory\");\n"
@@ -265,45 +235,9 @@ std::string gen_source(const spx_ew_params& p) {
   for (int o = 0; o < p.n_out; ++o) s << "  float* __restrict__ q" << o << " = (float*)b + a.out[" << o << "];\n";
   s << "  const " << IX << " n = " << n << SUF << ";\n"
     << "  const " << IX << " step = (" << IX << ")gridDim.x * 256u;\n";
-  // granule loads: x<u>_<j>[W]
+  // granule u at index expression v: loads, then the program and the stores
   auto load = [&](int u, const char* v) {
-    if (p.n_in > 0) {
-      s << "    float x" << u << "_0[" << W << "]";
-      for (int j = 1; j < p.n_in; ++j) s << ", x" << u << "_" << j << "[" << W << "]";
-      s << ";\n";
-    }
-    s << "    {\n      const " << IX << " e = (" << v << ") * " << W << "u;\n";
-    bool need_outer = false;
-    for (int j = 0; j < p.n_in; ++j)
-      for (int k = 0; k < rk - 1; ++k)
-        if (p.in[j].stride[k] != 0) need_outer = true;
-    s << "      const " << IX << " c = e % " << last << SUF << ";\n";
-    if (need_outer) {
-      s << "      " << IX << " q = e / " << last << SUF << ";\n";
-      for (int k = rk - 2; k >= 0; --k) {
-        if (k == 0) s << "      const " << IX << " i0 = q;\n";
-        else s << "      const " << IX << " i" << k << " = q % " << p.dims[k] << SUF << "; q /= " << p.dims[k] << SUF << ";\n";
-      }
-    }
-    for (int j = 0; j < p.n_in; ++j) {
-      s << "      const i64 o" << j << " = 0";
-      for (int k = 0; k < rk - 1; ++k)
-        if (p.in[j].stride[k] != 0) s << " + (i64)i" << k << " * " << p.in[j].stride[k] << "ll";
-      const int64_t sl = p.rank > 0 ? p.in[j].stride[rk - 1] : 0;
-      if (sl != 0) s << " + (i64)c * " << sl << "ll";
-      s << ";\n";
-      if (vec && sl == 1) {
-        s << "      { const float4 t = __ldg((const float4*)(p" << j << " + o" << j << ")); x" << u << "_" << j
-          << "[0] = t.x; x" << u << "_" << j << "[1] = t.y; x" << u << "_" << j << "[2] = t.z; x" << u << "_" << j
-          << "[3] = t.w; }\n";
-      } else if (vec) {
-        s << "      { const float t = __ldg(p" << j << " + o" << j << "); x" << u << "_" << j << "[0] = t; x" << u << "_"
-          << j << "[1] = t; x" << u << "_" << j << "[2] = t; x" << u << "_" << j << "[3] = t; }\n";
-      } else {
-        s << "      x" << u << "_" << j << "[0] = __ldg(p" << j << " + o" << j << ");\n";
-      }
-    }
-    s << "    }\n";
+    gen_loads(p, s, u, std::string("(") + v + ") * " + std::to_string(W) + "u", vec, wide);
   };
   auto compute = [&](int u, const char* v) {
     s << "    {\n      float y[" << p.n_out << "][" << W << "];\n";
