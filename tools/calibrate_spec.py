@@ -51,16 +51,39 @@ def sim_inputs(prog_name):
     return F, B, n
 
 
-def main():
-    rows = []
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_c*_n*.json"))):
-        if "first" in path or "reference" in path:
+def bench_lines(rnd):
+    """(tag, bench JSON line) of round `rnd`'s committed measurements."""
+    out = []
+    if rnd == 1:
+        for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_c*_n*.json"))):
+            if "first" in path or "reference" in path:
+                continue
+            out.append((os.path.basename(path)[10:-5], json.load(open(path))))
+        return out
+    # round 2: the N=1 lines and the final N=2/4 lines of one 4-GPU box
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_bench_c*_n1.json"))):
+        if "reference" in path:
             continue
-        line = json.load(open(path))
+        line = json.loads(open(path).read().strip().splitlines()[-1])
+        out.append((os.path.basename(path)[10:-5], line))
+    for raw in open(os.path.join(ROOT, "profiles", "r02_scale_final_lines.jsonl")):
+        raw = raw.strip()
+        if raw.startswith("{"):
+            line = json.loads(raw)
+            cfg = line["config"].get("config") or line["config"]["program"][:2]
+            out.append((f"{cfg}_n{line['n_gpus']}", line))
+    return out
+
+
+def main():
+    rnd = 2 if "--round" not in sys.argv else int(sys.argv[sys.argv.index("--round") + 1])
+    rows = []
+    for tag, line in bench_lines(rnd):
         prog = line["config"]["program"]
+        if prog.startswith("c1"):
+            continue                 # launch-bound toy step: no information on peak or links
         F, B, n = sim_inputs(prog)
-        rows.append(dict(cfg=os.path.basename(path)[10:-5], prog=prog, N=line["n_gpus"],
-                         t=line["ms_per_step"] / 1e3, F=F, B=B, n=n))
+        rows.append(dict(cfg=tag, prog=prog, N=line["n_gpus"], t=line["ms_per_step"] / 1e3, F=F, B=B, n=n))
     # peak: N=1 transformer steps (the simulator has no HBM term; C4's
     # memory-bound U-Net is reported but not fitted)
     fit1 = [r for r in rows if r["N"] == 1 and not r["cfg"].startswith("c4")]
@@ -80,8 +103,8 @@ def main():
     bw = 1.0 / inv_bw
     os.makedirs(os.path.dirname(OUT_SPEC), exist_ok=True)
     with open(OUT_SPEC, "w") as fh:
-        fh.write("# B200 running the spindle_b200 evaluator (fp32 semantics, 3xTF32 tensor-core GEMMs),\n"
-                 "# calibrated by tools/calibrate_spec.py from profiles/r01_bench_*.json.\n"
+        fh.write("# B200 running the spindle_b200 evaluator (fp32 semantics, block-scaled 3xFP16\n"
+                 f"# tensor-core GEMMs), calibrated by tools/calibrate_spec.py from round {rnd}'s bench lines.\n"
                  "# peak_flops: effective f32 rate of whole N=1 transformer steps (all ops);\n"
                  "# link_bandwidth / collective_latency_s: fitted to the multi-GPU residuals\n"
                  "# (collectives partly overlap compute here, so these are effective values).\n"
