@@ -566,11 +566,13 @@ class Executable:
         return k.kind in ("ew", "reduce") and all(b in results for b in k.data.get("outs_keep", k.outs))
 
     def _hoist_terminal(self):
-        """Move every terminal kernel to just after its last producer.  The
-        reference's training steps emit all parameter updates after the whole
-        backward pass, in forward order (models.py:152-220), so as written the
-        first update waits for the LAST weight gradient; hoisted, each update
-        runs (on its own stream) as soon as its gradient exists."""
+        """Move every terminal kernel -- and every collective whose outputs
+        only terminal kernels read -- to just after its last producer.  The
+        reference's training steps emit all parameter updates (and, once
+        partitioned, their gradient reductions) after the whole backward pass,
+        in forward order (models.py:152-220), so as written the first update
+        waits for the LAST weight gradient; hoisted, each gradient collective
+        and update runs (on its own stream) as soon as its gradient exists."""
         import os
         ks = self.comp.kernels
         n = len(ks)
