@@ -20,6 +20,47 @@ import numpy as np
 sys.path.insert(0, ".")
 
 
+def analyse(cls, stream, ready, end, waits) -> dict:
+    """Per-stream busy time and main-stream stalls of one traced run: a main
+    record that became ready later than the previous main record ended waited
+    for another stream -- attributed to the waited-on record whose end came
+    last (its class @ its stream)."""
+    ready = np.asarray(ready, dtype=np.float64)
+    end = np.asarray(end, dtype=np.float64)
+    n = len(cls)
+    t0 = float(ready.min())
+    span = float(end.max()) - t0
+    busy = collections.Counter()
+    by_cls = collections.Counter()
+    for i in range(n):
+        busy[stream[i]] += end[i] - ready[i]
+        by_cls[(stream[i], cls[i])] += end[i] - ready[i]
+    stalls = collections.Counter()
+    stall_n = collections.Counter()
+    stall_total = 0.0
+    prev_end = t0
+    worst = []
+    for i in range(n):
+        if stream[i] != 0:
+            continue
+        gap = ready[i] - prev_end
+        if gap > 0.002 and waits[i]:
+            j = max(waits[i], key=lambda w: end[w])
+            key = f"{cls[j]}@s{stream[j]}"
+            stalls[key] += gap
+            stall_n[key] += 1
+            stall_total += gap
+            worst.append((gap, i, cls[i], j, cls[j], stream[j]))
+        prev_end = max(prev_end, end[i])
+    return {"records": n, "span_ms": round(span, 3),
+            "busy_ms_by_stream": {int(k): round(v, 3) for k, v in sorted(busy.items())},
+            "busy_ms_by_stream_class": {f"s{k[0]}:{k[1]}": round(v, 3) for k, v in sorted(by_cls.items())},
+            "main_stall_ms": round(stall_total, 3),
+            "main_stall_by_cause": {k: [round(v, 3), stall_n[k]] for k, v in stalls.most_common()},
+            "worst_stalls": [{"ms": round(g, 3), "rec": i, "cls": c, "waited_on": j, "on": f"{cj}@s{sj}"}
+                             for g, i, c, j, cj, sj in sorted(worst, reverse=True)[:12]]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
@@ -58,39 +99,8 @@ def main():
         stream[idx] = st
         waits[idx] = list(w)
     cls = [names[k] for k, _ in recs]
-    t0 = float(ready.min())
-    span = float(end.max()) - t0
-    busy = collections.Counter()
-    by_cls = collections.Counter()
-    for i in range(n):
-        busy[stream[i]] += end[i] - ready[i]
-        by_cls[(stream[i], cls[i])] += end[i] - ready[i]
-    # main-stream stalls: record i on stream 0 became ready later than the
-    # previous main record ended -> it waited for another stream
-    stalls = collections.Counter()
-    stall_n = collections.Counter()
-    stall_total = 0.0
-    prev_end = t0
-    worst = []
-    for i in range(n):
-        if stream[i] != 0:
-            continue
-        gap = ready[i] - prev_end
-        if gap > 0.002 and waits[i]:
-            j = max(waits[i], key=lambda w: end[w])
-            key = f"{cls[j]}@s{stream[j]}"
-            stalls[key] += gap
-            stall_n[key] += 1
-            stall_total += gap
-            worst.append((gap, i, cls[i], j, cls[j], stream[j]))
-        prev_end = max(prev_end, end[i])
-    out = {"rank": rank, "records": n, "span_ms": round(span, 3),
-           "busy_ms_by_stream": {int(k): round(v, 3) for k, v in sorted(busy.items())},
-           "busy_ms_by_stream_class": {f"s{k[0]}:{k[1]}": round(v, 3) for k, v in sorted(by_cls.items())},
-           "main_stall_ms": round(stall_total, 3),
-           "main_stall_by_cause": {k: [round(v, 3), stall_n[k]] for k, v in stalls.most_common()},
-           "worst_stalls": [{"ms": round(g, 3), "rec": i, "cls": c, "waited_on": j, "on": f"{cj}@s{sj}"}
-                            for g, i, c, j, cj, sj in sorted(worst, reverse=True)[:12]]}
+    out = analyse(cls, stream, ready, end, waits)
+    out["rank"] = rank
     lines = [None] * world
     if dist is not None:
         dist.all_gather_object(lines, out)
