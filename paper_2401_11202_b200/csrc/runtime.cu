@@ -816,11 +816,20 @@ int spx_plan_finalize(uint64_t plan) {
   // weights, ...): one batched launch at the first (gemm_h3.cu split_h16_batch_kernel)
   const char* be = getenv("SPX_SPLIT_BATCH");
   const int batch = be ? atoi(be) != 0 : 1;
+  // SPX_SPLIT_BATCH_FIRST=k: the first batch of a stream holds only k splits,
+  // so the step's first GEMM does not wait for every weight's split (0.29 ms
+  // in the eager C2 N=1 timeline); measured neutral under graph replay (C2
+  // N=1 558.7k, C4 84.7k), so off by default
+  const char* bfe = getenv("SPX_SPLIT_BATCH_FIRST");
+  const int first_cap = bfe ? atoi(bfe) : 0;
+  bool first_done[SPX_SIDE_STREAMS + 1] = {};
   for (size_t i = 0; batch && i < P->recs.size(); ++i) {
     Record& a = P->recs[i];
     if (a.kind != SPX_K_SPLIT || a.fused) continue;
+    const int cap = (!first_done[a.stream] && first_cap > 0) ? first_cap : spx_split_batch_max();
+    first_done[a.stream] = true;
     size_t j = i + 1;
-    for (; j < P->recs.size() && (int)a.batch.size() + 1 < spx_split_batch_max(); ++j) {
+    for (; j < P->recs.size() && (int)a.batch.size() + 1 < cap; ++j) {
       Record& b = P->recs[j];
       if (b.kind != SPX_K_SPLIT || b.fused || b.stream != a.stream || !b.waits.empty()) break;
       a.batch.push_back((int)j);

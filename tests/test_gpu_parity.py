@@ -466,6 +466,7 @@ def test_split_batch_bitexact(monkeypatch):
            "w2": (rng.standard_normal((384, 640)) * 30).astype(np.float32),
            "w3": rng.standard_normal((640, 328)).astype(np.float32)}
     monkeypatch.setenv("SPX_SPLITK_F", "100000")      # no split-K: every GEMM on the 3xFP16 path
+    monkeypatch.setenv("SPX_SPLIT_BATCH_FIRST", "0")  # one batch
     outs = {}
     for mode in ("0", "1"):
         monkeypatch.setenv("SPX_SPLIT_BATCH", mode)
